@@ -1,0 +1,99 @@
+/* ssg.h -- C ABI of the B200 servesim hot path ("ssg" = servesim-gpu).
+ *
+ * Plain pointers and sizes only; no C++ or torch types cross this boundary.
+ * Every entry point is synchronous on the library's own stream unless its
+ * name ends in _device (those enqueue on the caller's stream and return).
+ * Each entry point names the reference interface it replaces
+ * (paths relative to /root/reference/proj/include/servesim/).
+ *
+ * Status codes (ssg_status.code and return value):
+ *   0 SSG_STATUS_OK
+ *   1 SSG_STATUS_INPUT     servesim::Error      -- bad input; message is the
+ *                                                 reference's message verbatim
+ *   2 SSG_STATUS_INTERNAL  servesim::InternalError (violated invariant)
+ *   3 SSG_STATUS_CUDA      CUDA runtime failure (no device, launch error, OOM)
+ * There is no CPU fallback: without a B200 every compute entry returns 3.
+ */
+#ifndef SSG_H
+#define SSG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SSG_STATUS_OK 0
+#define SSG_STATUS_INPUT 1
+#define SSG_STATUS_INTERNAL 2
+#define SSG_STATUS_CUDA 3
+
+typedef struct ssg_status {
+  int32_t code;
+  char message[4096];
+} ssg_status;
+
+typedef struct ssg_estimator ssg_estimator;
+
+/* ---- runtime ------------------------------------------------------------ */
+/* Selects the GPU and probes which glibc exp/log1p contraction this host's
+ * libm runs (the device then reproduces exactly that one). */
+int ssg_init(int device, ssg_status* st);
+int ssg_shutdown(void);
+/* 1 if the host libm is the FMA-contracted glibc variant, 0 if plain, -1 before init. */
+int ssg_math_variant(void);
+/* Library build identifier (sm arch, git-independent). */
+const char* ssg_version(void);
+/* Frees any buffer this library returned (JSON/CSV text). */
+void ssg_free(void* p);
+
+/* ---- estimator (predictor plugin) --------------------------------------- */
+/* EstimatorModel::from_json (estimator.hpp:158-177). */
+int ssg_estimator_from_json(const char* json, size_t len, ssg_estimator** out, ssg_status* st);
+/* generate_synthetic_profile + train (profiler.hpp:314-347, estimator.hpp:201-275):
+ * regressor is "interp" or "forest"; tps lists the tp degrees to profile. */
+int ssg_estimator_train(const char* model_spec_json, const char* device_json, const int64_t* tps,
+                        size_t n_tps, const char* regressor, uint64_t seed, ssg_estimator** out,
+                        ssg_status* st);
+/* EstimatorModel::to_json (estimator.hpp:137-156); free *out with ssg_free. */
+int ssg_estimator_to_json(const ssg_estimator* e, char** out, size_t* len, ssg_status* st);
+void ssg_estimator_free(ssg_estimator* e);
+/* Dense model slot of (op, tp) for the *_mixed/_device calls; -1 if untrained.
+ * op follows servesim::OpName order (qkv_proj = 0 ... send_recv = 10). */
+int32_t ssg_estimator_slot(const ssg_estimator* e, int32_t op, int64_t tp);
+/* Bytes the estimator occupies in HBM (uploads on first call). */
+int64_t ssg_estimator_device_bytes(const ssg_estimator* e, ssg_status* st);
+
+/* EstimatorModel::predict (estimator.hpp:105-123) over n queries of one
+ * (op, tp).  f0 = num_tokens | payload_bytes, f1 = kv_read_bytes (attention
+ * only, else may be NULL).  HOST buffers; copies are part of the call.  On a
+ * guard violation returns 1 with the reference's message for the
+ * lowest-index failing query. */
+int ssg_predict(const ssg_estimator* e, int32_t op, int64_t tp, size_t n, const double* f0,
+                const double* f1, double* out, ssg_status* st);
+/* Same over mixed models: slots[i] from ssg_estimator_slot. HOST buffers. */
+int ssg_predict_mixed(const ssg_estimator* e, size_t n, const int32_t* slots, const double* f0,
+                      const double* f1, double* out, ssg_status* st);
+/* Device-pointer form, enqueued on `stream` (cudaStream_t, may be NULL for
+ * the legacy stream).  d_slots may be NULL to use uniform_slot.  d_first_error
+ * must hold ~0ull on entry and receives (index << 8 | code) of the first
+ * failure. Returns after enqueueing. */
+int ssg_predict_device(const ssg_estimator* e, size_t n, const int32_t* d_slots,
+                       int32_t uniform_slot, const double* d_f0, const double* d_f1, double* d_out,
+                       unsigned long long* d_first_error, void* stream, ssg_status* st);
+
+/* predict_batch over many batch compositions (estimator.hpp:294-348), CSR
+ * layout: composition c owns prefill entries [p_off[c], p_off[c+1]) of
+ * (p_len, p_prior) and decode entries [d_off[c], d_off[c+1]) of d_ctx.  The
+ * operator set is derive_operators(model, {tp, pp=1}) of `model_spec_json`.
+ * Also returns batch_device_flops (estimator.hpp:353-380) when flops != NULL. */
+int ssg_predict_batch(const ssg_estimator* e, const char* model_spec_json, int64_t tp, size_t n,
+                      const int64_t* p_off, const int64_t* p_len, const int64_t* p_prior,
+                      const int64_t* d_off, const int64_t* d_ctx, double* seconds,
+                      double* flops, ssg_status* st);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SSG_H */

@@ -1,0 +1,149 @@
+"""B200-native servesim hot path: predictor, replica simulation, capacity search.
+
+Python is the test/bench harness only; every call below goes through the C
+ABI in include/ssg.h into libssg.so (sm_100a kernels + host C++).  See
+DESIGN.md for the architecture and INTEGRATION.md for the reference-side
+bindings.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _ffi
+from ._ffi import CudaError, InputError, InternalError, SsgError
+
+OPS = ["qkv_proj", "attn_out_proj", "mlp_up_proj", "mlp_down_proj", "act_fn", "add_norm",
+       "attn_prefill", "attn_decode", "allreduce", "allgather", "send_recv"]
+OP_INDEX = {n: i for i, n in enumerate(OPS)}
+
+__all__ = ["init", "Estimator", "OPS", "OP_INDEX", "SsgError", "InputError", "InternalError",
+           "CudaError", "math_variant", "simulate", "search"]
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def init(device: int = 0) -> None:
+    """Selects the GPU (ssg_init); also probes the host libm variant."""
+    _ffi.call("ssg_init", device)
+
+
+def math_variant() -> int:
+    return _ffi.lib().ssg_math_variant()
+
+
+class Estimator:
+    """Trained per-operator predictors (reference EstimatorModel, estimator.hpp:90-181)."""
+
+    def __init__(self, handle: C.c_void_p):
+        self._h = handle
+
+    @classmethod
+    def from_json(cls, text: str) -> "Estimator":
+        h = C.c_void_p()
+        b = text.encode()
+        _ffi.call("ssg_estimator_from_json", b, len(b), C.byref(h))
+        return cls(h)
+
+    @classmethod
+    def train(cls, model_spec: dict, device: dict, tps: Sequence[int], regressor: str = "interp",
+              seed: int = 0) -> "Estimator":
+        h = C.c_void_p()
+        arr = np.asarray(tps, dtype=np.int64)
+        _ffi.call("ssg_estimator_train", json.dumps(model_spec).encode(), json.dumps(device).encode(),
+                  arr.ctypes.data_as(_ffi.pi64), len(arr), regressor.encode(), seed, C.byref(h))
+        return cls(h)
+
+    def to_json(self) -> str:
+        out = C.c_void_p()
+        n = C.c_size_t()
+        _ffi.call("ssg_estimator_to_json", self._h, C.byref(out), C.byref(n))
+        return _ffi.take_text(out)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def slot(self, op: str, tp: int) -> int:
+        return _ffi.lib().ssg_estimator_slot(self._h, OP_INDEX[op], tp)
+
+    def device_bytes(self) -> int:
+        st = _ffi.Status()
+        n = _ffi.lib().ssg_estimator_device_bytes(self._h, C.byref(st))
+        _ffi.check(st.code, st)
+        return n
+
+    def predict(self, op: str, tp: int, f0, f1=None) -> np.ndarray:
+        """EstimatorModel::predict over arrays of features (host buffers)."""
+        f0 = np.ascontiguousarray(f0, dtype=np.float64)
+        f1 = None if f1 is None else np.ascontiguousarray(f1, dtype=np.float64)
+        out = np.empty_like(f0)
+        _ffi.call("ssg_predict", self._h, OP_INDEX[op], tp, len(f0), _ptr(f0), _ptr(f1), _ptr(out))
+        return out
+
+    def predict_mixed(self, slots, f0, f1=None, out=None) -> np.ndarray:
+        slots = np.ascontiguousarray(slots, dtype=np.int32)
+        f0 = np.ascontiguousarray(f0, dtype=np.float64)
+        f1 = None if f1 is None else np.ascontiguousarray(f1, dtype=np.float64)
+        if out is None:
+            out = np.empty_like(f0)
+        _ffi.call("ssg_predict_mixed", self._h, len(f0), _ptr(slots), _ptr(f0), _ptr(f1), _ptr(out))
+        return out
+
+    def predict_device(self, n: int, slots_ptr: int, uniform_slot: int, f0_ptr: int, f1_ptr: int,
+                       out_ptr: int, err_ptr: int, stream: int = 0) -> None:
+        """Device-pointer form (e.g. torch tensors' data_ptr()), enqueued on `stream`."""
+        _ffi.call("ssg_predict_device", self._h, n, slots_ptr or None, uniform_slot, f0_ptr,
+                  f1_ptr or None, out_ptr, err_ptr, stream or None)
+
+    def predict_batch(self, model_spec: dict, tp: int, batches):
+        """predict_batch + batch_device_flops over compositions
+        [(prefill_lengths, prefill_priors, decode_contexts), ...]."""
+        p_off, p_len, p_prior, d_off, d_ctx = [0], [], [], [0], []
+        for pl, pp, dc in batches:
+            p_len += list(pl)
+            p_prior += list(pp)
+            d_ctx += list(dc)
+            p_off.append(len(p_len))
+            d_off.append(len(d_ctx))
+        arrs = [np.asarray(a, dtype=np.int64) for a in (p_off, p_len, p_prior, d_off, d_ctx)]
+        secs = np.empty(len(batches))
+        flops = np.empty(len(batches))
+        _ffi.call("ssg_predict_batch", self._h, json.dumps(model_spec).encode(), tp, len(batches),
+                  *[_ptr(a) for a in arrs], _ptr(secs), _ptr(flops))
+        return secs, flops
+
+    def __del__(self):
+        try:
+            if self._h:
+                _ffi.lib().ssg_estimator_free(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
+def simulate(cluster: dict, estimator: Estimator, ids, arrivals, prefill, decode,
+             record_batches: bool = False, abort_delay: float = 0.0, abort_max_late: int = 0,
+             static_mode: bool = False) -> dict:
+    """run_simulation + build_report through ssg_simulate (sim.hpp:135-320)."""
+    ids = np.ascontiguousarray(ids, dtype=np.int64)
+    arr = np.ascontiguousarray(arrivals, dtype=np.float64)
+    pre = np.ascontiguousarray(prefill, dtype=np.int64)
+    dec = np.ascontiguousarray(decode, dtype=np.int64)
+    out = C.c_void_p()
+    _ffi.call("ssg_simulate", json.dumps(cluster).encode(), estimator.handle, len(ids), _ptr(ids),
+              _ptr(arr), _ptr(pre), _ptr(dec), int(record_batches), abort_delay, abort_max_late,
+              int(static_mode), C.byref(out))
+    return json.loads(_ffi.take_text(out))
+
+
+def search(config_path: str, shard: int = 0, num_shards: int = 1) -> dict:
+    """run_search from a reference-format search config (config.hpp:111, search.hpp:369)."""
+    out = C.c_void_p()
+    _ffi.call("ssg_search", config_path.encode(), shard, num_shards, C.byref(out))
+    return json.loads(_ffi.take_text(out))

@@ -1,0 +1,125 @@
+"""ctypes binding of libssg.so (include/ssg.h).
+
+The library is built in-tree (`make -C paper_2405_05465_b200/csrc`, or
+`__graft_entry__.build()`); importing this module without it raises -- there
+is no Python or CPU fallback for any compute entry point.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libssg.so")
+
+OK, INPUT, INTERNAL, CUDA = 0, 1, 2, 3
+
+
+class Status(C.Structure):
+    _fields_ = [("code", C.c_int32), ("message", C.c_char * 4096)]
+
+
+class SsgError(RuntimeError):
+    """Base of the library's errors; `.code` is the ssg.h status."""
+
+    code = INTERNAL
+
+
+class InputError(SsgError):
+    """servesim::Error -- the message is the reference's verbatim."""
+
+    code = INPUT
+
+
+class InternalError(SsgError):
+    code = INTERNAL
+
+
+class CudaError(SsgError):
+    code = CUDA
+
+
+_ERRORS = {INPUT: InputError, INTERNAL: InternalError, CUDA: CudaError}
+
+_lib = None
+
+P = C.c_void_p
+pd = C.POINTER(C.c_double)
+pi64 = C.POINTER(C.c_int64)
+pi32 = C.POINTER(C.c_int32)
+
+_SIGNATURES = {
+    "ssg_init": (C.c_int, [C.c_int, C.POINTER(Status)]),
+    "ssg_shutdown": (C.c_int, []),
+    "ssg_math_variant": (C.c_int, []),
+    "ssg_version": (C.c_char_p, []),
+    "ssg_free": (None, [P]),
+    "ssg_estimator_from_json": (C.c_int, [C.c_char_p, C.c_size_t, C.POINTER(P), C.POINTER(Status)]),
+    "ssg_estimator_train": (C.c_int, [C.c_char_p, C.c_char_p, pi64, C.c_size_t, C.c_char_p,
+                                      C.c_uint64, C.POINTER(P), C.POINTER(Status)]),
+    "ssg_estimator_to_json": (C.c_int, [P, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t),
+                                        C.POINTER(Status)]),
+    "ssg_estimator_free": (None, [P]),
+    "ssg_estimator_slot": (C.c_int32, [P, C.c_int32, C.c_int64]),
+    "ssg_estimator_device_bytes": (C.c_int64, [P, C.POINTER(Status)]),
+    "ssg_predict": (C.c_int, [P, C.c_int32, C.c_int64, C.c_size_t, P, P, P, C.POINTER(Status)]),
+    "ssg_predict_mixed": (C.c_int, [P, C.c_size_t, P, P, P, P, C.POINTER(Status)]),
+    "ssg_predict_device": (C.c_int, [P, C.c_size_t, P, C.c_int32, P, P, P, P, P,
+                                     C.POINTER(Status)]),
+    "ssg_predict_batch": (C.c_int, [P, C.c_char_p, C.c_int64, C.c_size_t, P, P, P, P, P, P, P,
+                                    C.POINTER(Status)]),
+    "ssg_simulate": (C.c_int, [C.c_char_p, P, C.c_size_t, P, P, P, P, C.c_int, C.c_double,
+                               C.c_size_t, C.c_int, C.POINTER(C.c_void_p), C.POINTER(Status)]),
+    "ssg_search": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.POINTER(C.c_void_p),
+                             C.POINTER(Status)]),
+    "ssg_search_shard": (C.c_int, [C.c_char_p, C.c_int, C.c_int, P, C.c_size_t,
+                                   C.POINTER(C.c_size_t), C.POINTER(Status)]),
+    "ssg_search_finalize": (C.c_int, [C.c_char_p, P, C.c_size_t, C.POINTER(C.c_void_p),
+                                      C.POINTER(Status)]),
+    "ssg_search_record_size": (C.c_size_t, []),
+}
+
+
+def lib():
+    """Loads libssg.so once; raises if it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            "libssg.so not built (%s); run `make -C paper_2405_05465_b200/csrc` "
+            "or __graft_entry__.build()" % LIB_PATH)
+    L = C.CDLL(LIB_PATH)
+    for name, (res, args) in _SIGNATURES.items():
+        fn = getattr(L, name, None)
+        if fn is None:
+            continue
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+def exported_symbols():
+    return list(_SIGNATURES)
+
+
+def check(rc: int, st: Status):
+    if rc != OK:
+        raise _ERRORS.get(rc, SsgError)(st.message.decode("utf-8", "replace"))
+
+
+def call(name, *args):
+    st = Status()
+    rc = getattr(lib(), name)(*args, C.byref(st))
+    check(rc, st)
+    return rc
+
+
+def take_text(ptr: C.c_void_p) -> str:
+    """Copies and frees a NUL-terminated buffer returned by the library."""
+    if not ptr.value:
+        return ""
+    s = C.string_at(ptr.value).decode("utf-8")
+    lib().ssg_free(ptr)
+    return s

@@ -1,0 +1,90 @@
+// runtime.cpp -- device context and the host-libm variant probe.
+#include "runtime.h"
+
+#include <cmath>
+#include <cstring>
+#include <mutex>
+
+#include "glibc_math.h"
+
+namespace ssg {
+
+namespace {
+Context g_ctx;
+std::mutex g_mu;
+}  // namespace
+
+int probe_host_math_variant() {
+  // Walk inputs until both routines have separated the two contractions at
+  // least a few times; the host libm must agree with exactly one of them on
+  // every sample, or device parity with this host is impossible.
+  std::uint64_t s = 0x9e3779b97f4a7c15ULL;
+  auto next = [&] {
+    s ^= s << 13;
+    s ^= s >> 7;
+    s ^= s << 17;
+    return s;
+  };
+  int agree[2] = {0, 0}, seen = 0;
+  for (int i = 0; i < 400000 && seen < 64; ++i) {
+    const double xe = -25.0 + 35.0 * (static_cast<double>(next() >> 11) * 0x1p-53);
+    const double xl = static_cast<double>(next() % 4000000) * static_cast<double>(1u << (next() % 12));
+    const double he = std::exp(xe), hl = std::log1p(xl);
+    double v[2][2];
+    for (int k = 0; k < 2; ++k) {
+      v[k][0] = ssg_exp(xe, k);
+      v[k][1] = ssg_log1p(xl, k);
+    }
+    const bool differ_e = std::memcmp(&v[0][0], &v[1][0], 8) != 0;
+    const bool differ_l = std::memcmp(&v[0][1], &v[1][1], 8) != 0;
+    for (int k = 0; k < 2; ++k) {
+      if (std::memcmp(&he, &v[k][0], 8) != 0 || std::memcmp(&hl, &v[k][1], 8) != 0)
+        agree[k] = -1;
+      else if (agree[k] >= 0 && (differ_e || differ_l))
+        ++agree[k];
+    }
+    if (differ_e || differ_l) ++seen;
+  }
+  if (agree[SSG_MATH_FMA] > 0 && agree[SSG_MATH_PLAIN] < 0) return SSG_MATH_FMA;
+  if (agree[SSG_MATH_PLAIN] > 0 && agree[SSG_MATH_FMA] < 0) return SSG_MATH_PLAIN;
+  throw servesim::InternalError(
+      "host libm exp/log1p match neither glibc contraction variant; device predictions "
+      "cannot be made bit-identical to this host");
+}
+
+void init_context(int device) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g_ctx.device == device && g_ctx.stream) return;
+  if (g_ctx.stream) {
+    cudaStreamDestroy(g_ctx.stream);
+    g_ctx.stream = nullptr;
+  }
+  int n = 0;
+  cuda_check(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+  if (device < 0 || device >= n)
+    throw CudaError("ssg_init: device " + std::to_string(device) + " not present (" +
+                    std::to_string(n) + " visible)");
+  cuda_check(cudaSetDevice(device), "cudaSetDevice");
+  cudaDeviceProp prop{};
+  cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+  if (prop.major != 10)
+    throw CudaError(std::string("ssg: built for sm_100a, found ") + prop.name);
+  cuda_check(cudaStreamCreateWithFlags(&g_ctx.stream, cudaStreamNonBlocking), "stream");
+  g_ctx.device = device;
+  g_ctx.num_sms = prop.multiProcessorCount;
+  if (g_ctx.math_fma < 0) g_ctx.math_fma = probe_host_math_variant();
+}
+
+Context& context() {
+  if (!g_ctx.stream) init_context(0);
+  cuda_check(cudaSetDevice(g_ctx.device), "cudaSetDevice");
+  return g_ctx;
+}
+
+void shutdown_context() {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g_ctx.stream) cudaStreamDestroy(g_ctx.stream);
+  g_ctx = Context{};
+}
+
+}  // namespace ssg

@@ -1,0 +1,684 @@
+// training.cpp -- synthetic profiling and per-operator predictor fitting.
+//
+// Runs once per (model, SKU) on the host before any simulation: it is the
+// "data loader" of the framework, producing the tables and tree ensembles the
+// predictor kernels evaluate.  Arithmetic is kept operation-for-operation
+// equal to the reference (built with -ffp-contract=off, libstdc++ RNG) so the
+// trained models are bit-identical and the JSON handoff round-trips exactly.
+//
+// reference: op_cost.hpp:21-98, profiler.hpp:54-347, regressor.hpp:26-386,
+//            estimator.hpp:137-275
+#include <algorithm>
+#include <cmath>
+#include <random>
+
+#include "json.hpp"
+#include "servesim_b200.hpp"
+
+namespace servesim {
+
+using json = nlohmann::json;
+
+// ------------------------------------------------------------------ costs
+namespace {
+
+struct Work {
+  double flops = 0, bytes = 0, wire_bytes = 0;
+  std::int64_t hops = 0;
+};
+
+Work token_work(const OperatorDescriptor& d, double n) {  // op_cost.hpp:21-48
+  Work w;
+  const double e = static_cast<double>(d.elem_bytes);
+  const double in = static_cast<double>(d.in_dim), out = static_cast<double>(d.out_dim);
+  switch (d.op) {
+    case OpName::QkvProj:
+    case OpName::AttnOutProj:
+    case OpName::MlpUpProj:
+    case OpName::MlpDownProj:
+      w.flops = 2.0 * n * in * out;
+      w.bytes = n > 0 ? e * (in * out + n * (in + out)) : 0.0;
+      break;
+    case OpName::ActFn:
+      w.flops = n * in;
+      w.bytes = 2.0 * e * n * in;
+      break;
+    case OpName::AddNorm:
+      w.flops = 8.0 * n * in;
+      w.bytes = 6.0 * e * n * in;
+      break;
+    default:
+      throw InternalError("token_level_cost: not a token-level op");
+  }
+  return w;
+}
+
+Work attention_work(const OperatorDescriptor& d, double n, double kv_read) {  // op_cost.hpp:52-73
+  Work w;
+  const double e = static_cast<double>(d.elem_bytes);
+  const double hq = static_cast<double>(d.q_heads_per_device * d.head_dim);
+  const double hkv = static_cast<double>(d.kv_heads_per_device * d.head_dim);
+  const double ctx = kv_read / (2.0 * e * hkv);
+  if (d.op == OpName::AttnPrefill) {
+    w.flops = 4.0 * n * (n + ctx) * hq;
+    w.bytes = kv_read + e * n * (2.0 * hq + 2.0 * hkv);
+  } else if (d.op == OpName::AttnDecode) {
+    w.flops = 4.0 * ctx * hq;
+    w.bytes = kv_read;
+  } else {
+    throw InternalError("attention_cost: not an attention op");
+  }
+  return w;
+}
+
+Work comm_work(const OperatorDescriptor& d, double payload) {  // op_cost.hpp:78-98
+  Work w;
+  const double t = static_cast<double>(d.tp_degree);
+  switch (d.op) {
+    case OpName::AllReduce:
+      w.wire_bytes = payload * 2.0 * (t - 1.0) / t;
+      w.hops = d.tp_degree - 1;
+      break;
+    case OpName::AllGather:
+      w.wire_bytes = payload * (t - 1.0) / t;
+      w.hops = d.tp_degree - 1;
+      break;
+    case OpName::SendRecv:
+      w.wire_bytes = payload;
+      w.hops = 1;
+      break;
+    default:
+      throw InternalError("communication_cost: not a communication op");
+  }
+  return w;
+}
+
+double feature_or(const FeatureMap& f, const char* name, double fallback) {
+  auto it = f.find(name);
+  return it == f.end() ? fallback : it->second;
+}
+
+}  // namespace
+
+std::vector<std::string> feature_schema(OpClass c) {
+  switch (c) {
+    case OpClass::TokenLevel: return {kFeatNumTokens};
+    case OpClass::SequenceLevel: return {kFeatNumTokens, kFeatKvReadBytes};
+    case OpClass::Communication: return {kFeatPayloadBytes};
+  }
+  throw InternalError("feature_schema: bad op class");
+}
+
+double synthetic_oracle(const OperatorDescriptor& d, const FeatureMap& f, const DeviceProfile& dev) {
+  switch (d.op_class) {
+    case OpClass::TokenLevel: {
+      Work w = token_work(d, feature_or(f, kFeatNumTokens, 0.0));
+      return std::max(w.flops / dev.peak_flops, w.bytes / dev.mem_bandwidth) + dev.kernel_overhead;
+    }
+    case OpClass::SequenceLevel: {
+      Work w = attention_work(d, feature_or(f, kFeatNumTokens, 0.0),
+                              feature_or(f, kFeatKvReadBytes, 0.0));
+      return std::max(w.flops / dev.peak_flops, w.bytes / dev.mem_bandwidth) + dev.kernel_overhead;
+    }
+    case OpClass::Communication: {
+      Work w = comm_work(d, feature_or(f, kFeatPayloadBytes, 0.0));
+      return w.wire_bytes / dev.link_bandwidth + static_cast<double>(w.hops) * dev.kernel_overhead;
+    }
+  }
+  throw InternalError("synthetic_oracle: bad op class");
+}
+
+// ------------------------------------------------------------------ grids
+namespace {
+
+std::vector<std::int64_t> doubling_levels(std::int64_t lo, std::int64_t hi) {
+  std::vector<std::int64_t> v;
+  for (std::int64_t x = lo; x < hi; x *= 2) v.push_back(x);
+  v.push_back(hi);
+  return v;
+}
+
+std::vector<std::int64_t> ratio_levels(std::int64_t lo, std::int64_t hi, double ratio) {
+  std::vector<std::int64_t> v;
+  for (double x = static_cast<double>(lo); x < static_cast<double>(hi); x *= ratio) {
+    const std::int64_t level = std::llround(x);
+    if (v.empty() || level > v.back()) v.push_back(level);
+  }
+  if (v.empty() || v.back() != hi) v.push_back(hi);
+  return v;
+}
+
+// Axis levels of the base profiling grid per op class (profiler.hpp:97-128).
+std::vector<std::vector<double>> base_axes(OpClass c, std::int64_t max_context,
+                                           std::int64_t kv_per_token_block) {
+  std::vector<std::vector<double>> axes;
+  switch (c) {
+    case OpClass::TokenLevel: {
+      std::vector<double> n;
+      for (auto v : doubling_levels(1, max_context)) n.push_back(static_cast<double>(v));
+      axes.push_back(n);
+      break;
+    }
+    case OpClass::SequenceLevel: {
+      require(kv_per_token_block > 0,
+              "profile_grid: kv_bytes_per_token_block unset for sequence-level grid");
+      const double r = std::sqrt(2.0);
+      std::vector<double> n, kv;
+      for (auto v : ratio_levels(1, max_context, r)) n.push_back(static_cast<double>(v));
+      kv.push_back(0.0);
+      for (auto k : ratio_levels(1, 512 * max_context, r))
+        kv.push_back(static_cast<double>(k * kv_per_token_block));
+      axes.push_back(n);
+      axes.push_back(kv);
+      break;
+    }
+    case OpClass::Communication: {
+      std::vector<double> p;
+      for (std::int64_t e = 10; e <= 30; ++e) p.push_back(static_cast<double>(std::int64_t(1) << e));
+      axes.push_back(p);
+      break;
+    }
+  }
+  // sorted-unique already holds for these generators; keep the invariant explicit
+  for (auto& ax : axes) {
+    std::sort(ax.begin(), ax.end());
+    ax.erase(std::unique(ax.begin(), ax.end()), ax.end());
+  }
+  return axes;
+}
+
+FeatureMap feature_point(const std::vector<std::string>& schema, const std::vector<double>& v) {
+  FeatureMap f;
+  for (std::size_t i = 0; i < schema.size(); ++i) f[schema[i]] = v[i];
+  return f;
+}
+
+// Adaptive bisection of axis gaps where log-space interpolation of the oracle
+// is worst (profiler.hpp:241-309); returns the refined per-axis levels.
+std::vector<std::vector<double>> refine_axes(const OperatorDescriptor& d,
+                                             std::vector<std::vector<double>> axes,
+                                             const DeviceProfile& dev) {
+  const double tol = 0.015;
+  const int max_extra = 24;
+  const auto schema = feature_schema(d.op_class);
+  const std::size_t nf = axes.size();
+  for (int round = 0; round < max_extra; ++round) {
+    double worst = 0.0, worst_mid = 0.0;
+    std::size_t worst_axis = 0;
+    for (std::size_t f = 0; f < nf; ++f) {
+      // cross sections over the other axes, earlier axes outermost
+      std::vector<std::vector<double>> sections{std::vector<double>(nf, 0.0)};
+      for (std::size_t g = 0; g < nf; ++g) {
+        if (g == f) continue;
+        std::vector<std::vector<double>> next;
+        for (const auto& base : sections)
+          for (double v : axes[g]) {
+            auto m = base;
+            m[g] = v;
+            next.push_back(std::move(m));
+          }
+        sections = std::move(next);
+      }
+      for (std::size_t i = 0; i + 1 < axes[f].size(); ++i) {
+        const double a = axes[f][i], b = axes[f][i + 1];
+        const double mid = std::expm1(0.5 * (std::log1p(a) + std::log1p(b)));
+        for (auto sec : sections) {
+          sec[f] = a;
+          const double ya = std::log(synthetic_oracle(d, feature_point(schema, sec), dev));
+          sec[f] = b;
+          const double yb = std::log(synthetic_oracle(d, feature_point(schema, sec), dev));
+          sec[f] = mid;
+          const double truth = synthetic_oracle(d, feature_point(schema, sec), dev);
+          const double err = std::fabs(std::exp(0.5 * (ya + yb)) - truth) / truth;
+          if (err > worst) {
+            worst = err;
+            worst_axis = f;
+            worst_mid = mid;
+          }
+        }
+      }
+    }
+    if (worst <= tol) break;
+    auto& ax = axes[worst_axis];
+    ax.insert(std::upper_bound(ax.begin(), ax.end(), worst_mid), worst_mid);
+  }
+  return axes;
+}
+
+}  // namespace
+
+std::vector<ProfileRecord> generate_synthetic_profile(const ModelSpec& spec,
+                                                      const DeviceProfile& dev,
+                                                      const std::vector<std::int64_t>& tps) {
+  std::vector<ProfileRecord> out;
+  for (std::int64_t tp : tps) {
+    ParallelismConfig par{tp, 1, 1};
+    validate(spec, par);
+    auto ops = derive_operators(spec, par);
+    OperatorDescriptor sr;
+    sr.op = OpName::SendRecv;
+    sr.op_class = OpClass::Communication;
+    sr.count = 1;
+    sr.tp_degree = tp;
+    sr.payload_bytes_per_token = spec.hidden_dim * spec.param_bytes_per_element;
+    sr.elem_bytes = spec.param_bytes_per_element;
+    ops.push_back(sr);
+    const std::int64_t kvb = kv_bytes_per_token_per_block(spec, par);
+    for (const auto& d : ops) {
+      const auto schema = feature_schema(d.op_class);
+      auto axes = refine_axes(d, base_axes(d.op_class, spec.max_context, kvb), dev);
+      std::size_t cells = 1;
+      for (auto& ax : axes) cells *= ax.size();
+      std::vector<double> pt(axes.size());
+      for (std::size_t c = 0; c < cells; ++c) {  // last axis fastest
+        std::size_t rem = c;
+        for (std::size_t k = axes.size(); k-- > 0;) {
+          pt[k] = axes[k][rem % axes[k].size()];
+          rem /= axes[k].size();
+        }
+        ProfileRecord r;
+        r.op = d.op;
+        r.features = feature_point(schema, pt);
+        r.runtime = synthetic_oracle(d, r.features, dev);
+        r.features[kFeatTpDegree] = static_cast<double>(tp);
+        out.push_back(std::move(r));
+      }
+    }
+  }
+  return out;
+}
+
+// ------------------------------------------------------------------ regressors
+namespace {
+
+using Rows = std::vector<std::vector<double>>;
+
+RegressorData fit_interp(const Rows& x, const std::vector<double>& y) {  // regressor.hpp:278-306
+  require(!x.empty() && x.size() == y.size(), "interp fit: empty or mismatched data");
+  RegressorData g;
+  g.type = "interp";
+  const std::size_t nf = x.front().size();
+  g.axes.resize(nf);
+  for (std::size_t f = 0; f < nf; ++f) {
+    auto& ax = g.axes[f];
+    for (const auto& row : x) ax.push_back(row[f]);
+    std::sort(ax.begin(), ax.end());
+    ax.erase(std::unique(ax.begin(), ax.end()), ax.end());
+  }
+  std::size_t cells = 1;
+  for (auto& ax : g.axes) cells *= ax.size();
+  require(cells == x.size(), "interp fit: training points do not form a full grid (" +
+                                 std::to_string(x.size()) + " points vs " + std::to_string(cells) +
+                                 " cells); train scattered data with the forest regressor");
+  g.values.assign(cells, 0.0);
+  std::vector<char> seen(cells, 0);
+  for (std::size_t i = 0; i < x.size(); ++i) {
+    std::size_t flat = 0, stride = 1;
+    for (std::size_t f = nf; f-- > 0;) {
+      auto it = std::lower_bound(g.axes[f].begin(), g.axes[f].end(), x[i][f]);
+      internal_check(it != g.axes[f].end() && *it == x[i][f], "interp fit: off-axis point");
+      flat += static_cast<std::size_t>(it - g.axes[f].begin()) * stride;
+      stride *= g.axes[f].size();
+    }
+    require(!seen[flat], "interp fit: duplicate grid point");
+    seen[flat] = 1;
+    g.values[flat] = y[i];
+  }
+  return g;
+}
+
+// Least squares plane of a leaf: normal equations + ridge 1e-9, Gaussian
+// elimination with partial pivoting (regressor.hpp:42-67, 234-254).
+std::vector<double> fit_plane(const Rows& x, const std::vector<double>& y,
+                              const std::vector<std::size_t>& idx, std::size_t nf) {
+  const std::size_t n = nf + 1;
+  std::vector<double> a(n * n, 0.0), b(n, 0.0);
+  std::vector<double> row(n);
+  for (auto i : idx) {
+    row[0] = 1.0;
+    for (std::size_t f = 0; f < nf; ++f) row[f + 1] = x[i][f];
+    for (std::size_t r = 0; r < n; ++r) {
+      b[r] += row[r] * y[i];
+      for (std::size_t c = 0; c < n; ++c) a[r * n + c] += row[r] * row[c];
+    }
+  }
+  for (std::size_t i = 0; i < n; ++i) a[i * n + i] += 1e-9;
+  bool ok = true;
+  for (std::size_t col = 0; col < n && ok; ++col) {
+    std::size_t piv = col;
+    for (std::size_t r = col + 1; r < n; ++r)
+      if (std::fabs(a[r * n + col]) > std::fabs(a[piv * n + col])) piv = r;
+    if (std::fabs(a[piv * n + col]) < 1e-30) {
+      ok = false;
+      break;
+    }
+    if (piv != col) {
+      for (std::size_t c = 0; c < n; ++c) std::swap(a[piv * n + c], a[col * n + c]);
+      std::swap(b[piv], b[col]);
+    }
+    for (std::size_t r = col + 1; r < n; ++r) {
+      const double m = a[r * n + col] / a[col * n + col];
+      for (std::size_t c = col; c < n; ++c) a[r * n + c] -= m * a[col * n + c];
+      b[r] -= m * b[col];
+    }
+  }
+  std::vector<double> w(n, 0.0);
+  if (ok) {
+    for (std::size_t i = n; i-- > 0;) {
+      double s = b[i];
+      for (std::size_t c = i + 1; c < n; ++c) s -= a[i * n + c] * w[c];
+      w[i] = s / a[i * n + i];
+    }
+    return w;
+  }
+  double m = 0.0;
+  for (auto i : idx) m += y[i];
+  w[0] = m / static_cast<double>(idx.size());
+  return w;
+}
+
+struct ForestBuilder {
+  const Rows& x;
+  const std::vector<double>& y;
+  const ForestConfig& cfg;
+  std::size_t nf;
+  std::size_t min_leaf;
+
+  int grow(ForestTree& t, const std::vector<std::size_t>& idx, int depth, std::mt19937_64& rng) {
+    const int node = static_cast<int>(t.feature.size());
+    t.feature.push_back(0);
+    t.threshold.push_back(0.0);
+    t.left.push_back(-1);
+    t.right.push_back(-1);
+    int split_f = -1;
+    double split_th = 0.0;
+    if (depth < cfg.max_depth && idx.size() >= 2 * min_leaf) pick_split(idx, rng, split_f, split_th);
+    if (split_f < 0) {
+      t.feature[node] = -static_cast<int>(t.leaf_weights.size()) - 1;
+      t.leaf_weights.push_back(fit_plane(x, y, idx, nf));
+      return node;
+    }
+    std::vector<std::size_t> lo_side, hi_side;
+    for (auto i : idx) (x[i][split_f] <= split_th ? lo_side : hi_side).push_back(i);
+    t.feature[node] = split_f;
+    t.threshold[node] = split_th;
+    const int l = grow(t, lo_side, depth + 1, rng);
+    t.left[node] = l;
+    const int r = grow(t, hi_side, depth + 1, rng);
+    t.right[node] = r;
+    return node;
+  }
+
+  // Random thresholds per feature, best variance-reduction surrogate wins
+  // (regressor.hpp:193-232).
+  void pick_split(const std::vector<std::size_t>& idx, std::mt19937_64& rng, int& best_f,
+                  double& best_th) const {
+    double best = -1.0;
+    const std::size_t n = idx.size();
+    double total = 0.0;
+    for (auto i : idx) total += y[i];
+    std::uniform_real_distribution<double> unit(0.0, 1.0);
+    for (std::size_t f = 0; f < nf; ++f) {
+      double lo = x[idx[0]][f], hi = lo;
+      for (auto i : idx) {
+        lo = std::min(lo, x[i][f]);
+        hi = std::max(hi, x[i][f]);
+      }
+      if (lo == hi) continue;
+      for (int k = 0; k < cfg.threshold_draws; ++k) {
+        const double th = lo + (hi - lo) * unit(rng);
+        std::size_t nl = 0;
+        double ls = 0.0;
+        for (auto i : idx)
+          if (x[i][f] <= th) {
+            ++nl;
+            ls += y[i];
+          }
+        const std::size_t nr = n - nl;
+        if (nl < min_leaf || nr < min_leaf) continue;
+        const double score = ls * ls / static_cast<double>(nl) +
+                             (total - ls) * (total - ls) / static_cast<double>(nr);
+        if (score > best + 1e-15) {
+          best = score;
+          best_f = static_cast<int>(f);
+          best_th = th;
+        }
+      }
+    }
+  }
+};
+
+RegressorData fit_forest(const Rows& x, const std::vector<double>& y, const ForestConfig& cfg) {
+  require(!x.empty() && x.size() == y.size(), "forest train: empty or mismatched data");
+  RegressorData f;
+  f.type = "forest";
+  f.num_features = x.front().size();
+  f.y_lo = *std::min_element(y.begin(), y.end());
+  f.y_hi = *std::max_element(y.begin(), y.end());
+  const double pad = 0.1 * (f.y_hi - f.y_lo);
+  f.y_lo -= pad;
+  f.y_hi += pad;
+  std::size_t min_leaf = cfg.min_samples_leaf > 0 ? static_cast<std::size_t>(cfg.min_samples_leaf)
+                         : f.num_features <= 1    ? 2
+                                                  : f.num_features + 2;
+  ForestBuilder fb{x, y, cfg, f.num_features, min_leaf};
+  std::vector<std::size_t> all(x.size());
+  for (std::size_t i = 0; i < all.size(); ++i) all[i] = i;
+  for (int t = 0; t < cfg.num_trees; ++t) {
+    std::mt19937_64 rng(cfg.seed * 0x9e3779b97f4a7c15ULL + static_cast<std::uint64_t>(t) + 1);
+    ForestTree tree;
+    fb.grow(tree, all, 0, rng);
+    f.trees.push_back(std::move(tree));
+  }
+  return f;
+}
+
+RegressorData fit(const std::string& kind, const Rows& x, const std::vector<double>& y,
+                  const ForestConfig& fc) {
+  if (kind == "forest") return fit_forest(x, y, fc);
+  if (kind == "interp") return fit_interp(x, y);
+  throw Error("train: unknown regressor kind '" + kind + "'");
+}
+
+// Host evaluation used only for the training-time hold-out score (estimator.hpp:261-270);
+// every runtime query goes through the device kernels.
+double host_regress(const RegressorData& r, const std::vector<double>& x) {
+  double sum = 0.0;
+  for (const auto& t : r.trees) {
+    int node = 0;
+    while (t.feature[node] >= 0) node = x[t.feature[node]] <= t.threshold[node] ? t.left[node] : t.right[node];
+    const auto& w = t.leaf_weights[-t.feature[node] - 1];
+    double v = w[0];
+    for (std::size_t f = 0; f < r.num_features; ++f) v += w[f + 1] * x[f];
+    sum += std::clamp(v, r.y_lo, r.y_hi);
+  }
+  return sum / static_cast<double>(r.trees.size());
+}
+
+}  // namespace
+
+EstimatorModel train(const std::vector<ProfileRecord>& records, const TrainConfig& cfg) {
+  std::map<OpModelKey, std::vector<const ProfileRecord*>> groups;
+  for (const auto& r : records) {
+    auto it = r.features.find(kFeatTpDegree);
+    require(it != r.features.end(), "train: record missing tp_degree feature");
+    groups[{r.op, static_cast<std::int64_t>(it->second)}].push_back(&r);
+  }
+  require(!groups.empty(), "train: no records");
+  EstimatorModel model;
+  std::uint64_t group_index = 0;
+  for (const auto& [key, recs] : groups) {
+    require(recs.size() >= cfg.min_points_per_op,
+            "train: op " + to_string(key) + " has only " + std::to_string(recs.size()) +
+                " points (need " + std::to_string(cfg.min_points_per_op) + ")");
+    EstimatorModel::PerOpModel m;
+    m.schema = feature_schema(triage(key.op));
+    m.n_points = recs.size();
+    const std::size_t nf = m.schema.size();
+    m.levels.assign(nf, {});
+    m.bbox_lo.assign(nf, 0.0);
+    m.bbox_hi.assign(nf, 0.0);
+    Rows x;
+    std::vector<double> y;
+    for (const auto* r : recs) {
+      std::vector<double> row(nf);
+      for (std::size_t f = 0; f < nf; ++f) {
+        auto it = r->features.find(m.schema[f]);
+        require(it != r->features.end(),
+                "train: op " + to_string(key) + " record missing feature " + m.schema[f]);
+        row[f] = std::log1p(it->second);
+        m.levels[f].push_back(it->second);
+      }
+      x.push_back(std::move(row));
+      y.push_back(std::log(r->runtime));
+    }
+    for (std::size_t f = 0; f < nf; ++f) {
+      auto& lv = m.levels[f];
+      std::sort(lv.begin(), lv.end());
+      lv.erase(std::unique(lv.begin(), lv.end()), lv.end());
+      m.bbox_lo[f] = lv.front();
+      m.bbox_hi[f] = lv.back();
+    }
+    ForestConfig fc = cfg.forest;
+    fc.seed = cfg.seed * 1000003ULL + group_index++;
+    Rows xt;
+    std::vector<double> yt;
+    std::vector<std::size_t> held;
+    const bool can_hold = x.size() >= 2 * cfg.min_points_per_op;
+    for (std::size_t i = 0; i < x.size(); ++i) {
+      if (can_hold && i % 5 == 2) {
+        held.push_back(i);
+      } else {
+        xt.push_back(x[i]);
+        yt.push_back(y[i]);
+      }
+    }
+    if (!held.empty() && cfg.regressor == "forest") {
+      RegressorData probe = fit(cfg.regressor, xt, yt, fc);
+      double ape = 0.0;
+      for (auto i : held) {
+        const double pred = std::exp(host_regress(probe, x[i]));
+        const double truth = std::exp(y[i]);
+        ape += std::fabs(pred - truth) / truth;
+      }
+      m.holdout_mape = ape / static_cast<double>(held.size());
+    }
+    m.regressor = fit(cfg.regressor, x, y, fc);
+    model.insert(key, std::move(m));
+  }
+  return model;
+}
+
+// ------------------------------------------------------------------ JSON
+namespace {
+
+json regressor_json(const RegressorData& r) {
+  json j;
+  j["type"] = r.type;
+  if (r.type == "forest") {
+    j["num_features"] = r.num_features;
+    j["y_lo"] = r.y_lo;
+    j["y_hi"] = r.y_hi;
+    json trees = json::array();
+    for (const auto& t : r.trees) {
+      json tj;
+      tj["feature"] = t.feature;
+      tj["threshold"] = t.threshold;
+      tj["left"] = t.left;
+      tj["right"] = t.right;
+      tj["leaf_weights"] = t.leaf_weights;
+      trees.push_back(std::move(tj));
+    }
+    j["trees"] = std::move(trees);
+  } else {
+    j["axes"] = r.axes;
+    j["values"] = r.values;
+  }
+  return j;
+}
+
+RegressorData regressor_from(const json& j) {
+  RegressorData r;
+  r.type = j.at("type").get<std::string>();
+  if (r.type == "forest") {
+    r.num_features = j.at("num_features").get<std::size_t>();
+    r.y_lo = j.at("y_lo").get<double>();
+    r.y_hi = j.at("y_hi").get<double>();
+    for (const auto& tj : j.at("trees")) {
+      ForestTree t;
+      t.feature = tj.at("feature").get<std::vector<int>>();
+      t.threshold = tj.at("threshold").get<std::vector<double>>();
+      t.left = tj.at("left").get<std::vector<int>>();
+      t.right = tj.at("right").get<std::vector<int>>();
+      t.leaf_weights = tj.at("leaf_weights").get<std::vector<std::vector<double>>>();
+      r.trees.push_back(std::move(t));
+    }
+    require(!r.trees.empty(), "forest model: no trees");
+    return r;
+  }
+  if (r.type == "interp") {
+    r.axes = j.at("axes").get<std::vector<std::vector<double>>>();
+    r.values = j.at("values").get<std::vector<double>>();
+    std::size_t cells = 1;
+    for (auto& ax : r.axes) cells *= ax.size();
+    require(cells == r.values.size(), "interp model: axes/value size mismatch");
+    return r;
+  }
+  throw Error("unknown regressor type '" + r.type + "'");
+}
+
+}  // namespace
+
+std::string EstimatorModel::to_json() const {
+  json j;
+  j["schema_version"] = 1;
+  j["kind"] = "estimator";
+  json ops = json::object();
+  for (const auto& [key, m] : models_) {
+    json mj;
+    mj["op"] = servesim::to_string(key.op);
+    mj["tp_degree"] = key.tp_degree;
+    mj["schema"] = m.schema;
+    mj["bbox_lo"] = m.bbox_lo;
+    mj["bbox_hi"] = m.bbox_hi;
+    mj["levels"] = m.levels;
+    mj["holdout_mape"] = m.holdout_mape;
+    mj["n_points"] = m.n_points;
+    mj["regressor"] = regressor_json(m.regressor);
+    ops[servesim::to_string(key)] = std::move(mj);
+  }
+  j["ops"] = std::move(ops);
+  return j.dump();
+}
+
+EstimatorModel EstimatorModel::from_json(const std::string& text) {
+  json j;
+  try {
+    j = json::parse(text);
+  } catch (const json::exception& e) {
+    throw Error(std::string("estimator file: invalid JSON: ") + e.what());
+  }
+  try {
+    require(j.value("kind", "") == "estimator", "estimator file: wrong kind");
+    require(j.at("schema_version").get<int>() == 1, "estimator file: unsupported schema_version");
+    EstimatorModel e;
+    for (const auto& [unused, mj] : j.at("ops").items()) {
+      OpModelKey key{op_name_from_string(mj.at("op").get<std::string>()),
+                     mj.at("tp_degree").get<std::int64_t>()};
+      PerOpModel m;
+      m.schema = mj.at("schema").get<std::vector<std::string>>();
+      m.bbox_lo = mj.at("bbox_lo").get<std::vector<double>>();
+      m.bbox_hi = mj.at("bbox_hi").get<std::vector<double>>();
+      m.levels = mj.at("levels").get<std::vector<std::vector<double>>>();
+      m.holdout_mape = mj.at("holdout_mape").get<double>();
+      m.n_points = mj.at("n_points").get<std::size_t>();
+      m.regressor = regressor_from(mj.at("regressor"));
+      e.models_[key] = std::move(m);
+    }
+    return e;
+  } catch (const json::exception& ex) {
+    throw Error(std::string("estimator file: malformed: ") + ex.what());
+  }
+}
+
+}  // namespace servesim

@@ -1,0 +1,250 @@
+// predictor.cu -- K1/K2: batched operator-runtime prediction on sm_100a.
+//
+// Upload: each (op, tp) model of an EstimatorModel is flattened once into HBM
+//   * interp axes + values  -> dpool (fp64)
+//   * forest trees          -> nodes[] 16 B records in preorder (left = i + 1,
+//                              leaves carry their plane weights inline) and
+//                              roots[] per tree
+// A whole SKU's estimator (all ops x tp degrees) is ~60 KB (interp) or a few MB
+// (forest), so it stays resident in L2 across every kernel of a sweep.
+//
+// Kernel: one thread per query, grid-stride over 148 SMs x resident blocks.
+// Queries are SoA (model slot, feature 0, feature 1) for coalesced loads.
+//
+// reference: estimator.hpp:105-131 (predict/find), regressor.hpp:103-108,
+//            256-264, 308-341
+#include <algorithm>
+#include <cstring>
+
+#include "predictor.cuh"
+#include "runtime.h"
+
+namespace servesim {
+
+namespace {
+
+// Re-layout one reference tree (arbitrary node numbering) into preorder
+// 16-byte records appended to `out`; returns the root's absolute index.
+int32_t append_tree(const ForestTree& t, std::size_t nf, std::vector<SsgNode>& out) {
+  const int32_t root = static_cast<int32_t>(out.size());
+  // explicit stack of (reference node, slot whose `right` must be patched)
+  std::vector<std::pair<int, int32_t>> stack;
+  stack.push_back({0, -1});
+  while (!stack.empty()) {
+    auto [ref, patch] = stack.back();
+    stack.pop_back();
+    const int32_t here = static_cast<int32_t>(out.size());
+    if (patch >= 0) out[patch].right = here;
+    internal_check(ref >= 0 && ref < static_cast<int>(t.feature.size()), "forest: bad child index");
+    if (t.feature[ref] >= 0) {
+      SsgNode n{};
+      n.a = t.threshold[ref];
+      n.feat = t.feature[ref];
+      n.right = -1;
+      out.push_back(n);
+      // preorder: left subtree immediately follows, right is patched later
+      stack.push_back({t.right[ref], here});
+      stack.push_back({t.left[ref], -1});
+    } else {
+      const auto& w = t.leaf_weights.at(static_cast<std::size_t>(-t.feature[ref] - 1));
+      internal_check(w.size() == nf + 1, "forest: leaf weight count mismatch");
+      SsgNode n{};
+      n.a = w[0];
+      n.feat = -1;
+      n.right = static_cast<int32_t>(nf);
+      out.push_back(n);
+      SsgNode tail{};
+      double w12[2] = {nf > 0 ? w[1] : 0.0, nf > 1 ? w[2] : 0.0};
+      std::memcpy(&tail, w12, sizeof w12);
+      out.push_back(tail);
+    }
+  }
+  return root;
+}
+
+__global__ void k_predict(SsgEstView E, int64_t n, const int32_t* __restrict__ slot,
+                          int32_t uniform_slot, const double* __restrict__ f0,
+                          const double* __restrict__ f1, double* __restrict__ out,
+                          unsigned long long* __restrict__ first_error) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int32_t m = slot ? __ldg(slot + i) : uniform_slot;
+    const double v0 = __ldg(f0 + i);
+    const double v1 = f1 ? __ldg(f1 + i) : 0.0;
+    double r = 0.0;
+    int bad = 0;
+    const int code = ssg_predict_one(E, m, v0, v1, &r, &bad);
+    out[i] = r;
+    if (code != SSG_OK) atomicMin(first_error, ((unsigned long long)i << 8) | (unsigned)code);
+  }
+}
+
+}  // namespace
+
+std::string bbox_error_message(const EstimatorModel::PerOpModel& m, const OpModelKey& key,
+                               int f, double v) {
+  const double extent = m.bbox_hi[f] - m.bbox_lo[f];
+  const double margin = EstimatorModel::kExtrapolationMargin * extent;
+  return "estimator: feature " + m.schema[f] + "=" + std::to_string(v) + " for " +
+         to_string(key) + " outside extrapolation margin [" +
+         std::to_string(m.bbox_lo[f] - margin) + ", " + std::to_string(m.bbox_hi[f] + margin) + "]";
+}
+
+// ------------------------------------------------------------------ model
+EstimatorModel::EstimatorModel() = default;
+EstimatorModel::~EstimatorModel() = default;
+EstimatorModel::EstimatorModel(EstimatorModel&&) noexcept = default;
+EstimatorModel& EstimatorModel::operator=(EstimatorModel&&) noexcept = default;
+
+const EstimatorModel::PerOpModel& EstimatorModel::find(OpName op, std::int64_t tp) const {
+  auto it = models_.find({op, tp});
+  require(it != models_.end(), "estimator: no trained model for op " + to_string(OpModelKey{op, tp}) +
+                                   " (profile and train must cover the config's operators)");
+  return it->second;
+}
+
+void EstimatorModel::insert(const OpModelKey& k, PerOpModel m) {
+  models_[k] = std::move(m);
+  dev_.reset();
+}
+
+const DeviceEstimator& EstimatorModel::device() const {
+  if (dev_) return *dev_;
+  auto& ctx = ssg::context();
+  auto d = std::make_unique<DeviceEstimator>();
+  std::vector<double> dpool;
+  std::vector<SsgNode> nodes;
+  std::vector<int32_t> roots;
+  for (const auto& [key, m] : models_) {
+    SsgModelDesc desc{};
+    desc.op = static_cast<int32_t>(key.op);
+    desc.tp = static_cast<int32_t>(key.tp_degree);
+    desc.nf = static_cast<int32_t>(m.schema.size());
+    internal_check(desc.nf >= 1 && desc.nf <= 2, "estimator upload: models take 1 or 2 features");
+    for (int f = 0; f < desc.nf; ++f) {
+      const double extent = m.bbox_hi[f] - m.bbox_lo[f];
+      const double margin = kExtrapolationMargin * extent;
+      desc.lower[f] = m.bbox_lo[f] - margin;
+      desc.upper[f] = m.bbox_hi[f] + margin;
+    }
+    const RegressorData& r = m.regressor;
+    if (r.type == "interp") {
+      desc.kind = SSG_KIND_INTERP;
+      internal_check(r.axes.size() == static_cast<std::size_t>(desc.nf),
+                     "interp predict: feature count mismatch");
+      for (int f = 0; f < desc.nf; ++f) {
+        desc.axis_len[f] = static_cast<int32_t>(r.axes[f].size());
+        desc.axis_off[f] = static_cast<int64_t>(dpool.size());
+        dpool.insert(dpool.end(), r.axes[f].begin(), r.axes[f].end());
+      }
+      desc.values_off = static_cast<int64_t>(dpool.size());
+      dpool.insert(dpool.end(), r.values.begin(), r.values.end());
+    } else {
+      desc.kind = SSG_KIND_FOREST;
+      internal_check(r.num_features == static_cast<std::size_t>(desc.nf),
+                     "forest predict: feature count mismatch");
+      desc.ntrees = static_cast<int32_t>(r.trees.size());
+      desc.roots_off = static_cast<int64_t>(roots.size());
+      desc.y_lo = r.y_lo;
+      desc.y_hi = r.y_hi;
+      for (const auto& t : r.trees) roots.push_back(append_tree(t, r.num_features, nodes));
+    }
+    d->index[key] = static_cast<int32_t>(d->host_models.size());
+    d->host_models.push_back(desc);
+  }
+  internal_check(nodes.size() < (1u << 31), "forest: node pool exceeds int32 addressing");
+  // keep every pool non-empty so the view never carries null pointers
+  if (dpool.empty()) dpool.push_back(0.0);
+  if (nodes.empty()) nodes.push_back(SsgNode{});
+  if (roots.empty()) roots.push_back(0);
+  d->models.upload(d->host_models, ctx.stream);
+  d->dpool.upload(dpool, ctx.stream);
+  d->nodes.upload(nodes, ctx.stream);
+  d->roots.upload(roots, ctx.stream);
+  ssg::cuda_check(cudaStreamSynchronize(ctx.stream), "estimator upload");
+  d->bytes = d->host_models.size() * sizeof(SsgModelDesc) + dpool.size() * 8 +
+             nodes.size() * sizeof(SsgNode) + roots.size() * 4;
+  d->view.models = d->models.ptr;
+  d->view.dpool = d->dpool.ptr;
+  d->view.nodes = d->nodes.ptr;
+  d->view.roots = d->roots.ptr;
+  d->view.nmodels = static_cast<int32_t>(d->host_models.size());
+  d->view.math_fma = ctx.math_fma;
+  dev_ = std::move(d);
+  return *dev_;
+}
+
+}  // namespace servesim
+
+namespace ssg {
+
+using namespace servesim;
+
+// Launch on device pointers (no synchronisation).  `first_error` must hold
+// SSG_NO_ERROR on entry.
+void launch_predict(const DeviceEstimator& de, int64_t n, const int32_t* slots, int32_t uniform,
+                    const double* f0, const double* f1, double* out,
+                    unsigned long long* first_error, cudaStream_t s) {
+  if (n <= 0) return;
+  auto& ctx = context();
+  const int threads = 256;
+  int64_t blocks = (n + threads - 1) / threads;
+  const int64_t cap = static_cast<int64_t>(ctx.num_sms) * 8;  // 8 x 256 threads resident per SM
+  if (blocks > cap) blocks = cap;
+  k_predict<<<static_cast<unsigned>(blocks), threads, 0, s>>>(de.view, n, slots, uniform, f0, f1,
+                                                              out, first_error);
+  cuda_check(cudaGetLastError(), "k_predict launch");
+}
+
+// Turns the packed first-error word into the reference's exception.
+[[noreturn]] void raise_predict_error(const EstimatorModel& est, unsigned long long word,
+                                      const int32_t* slots_host, int32_t uniform,
+                                      const double* f0_host, const double* f1_host) {
+  const auto& de = est.device();
+  const int64_t i = static_cast<int64_t>(word >> 8);
+  const int code = static_cast<int>(word & 0xff);
+  const int32_t slot = slots_host ? slots_host[i] : uniform;
+  const SsgModelDesc& d = de.host_models.at(slot);
+  const OpModelKey key{static_cast<OpName>(d.op), d.tp};
+  if (code == SSG_ERR_BBOX) {
+    const auto& m = est.find(key.op, key.tp_degree);
+    const double v0 = f0_host[i];
+    const bool first_bad = !(v0 >= d.lower[0] && v0 <= d.upper[0]);
+    const int f = first_bad ? 0 : 1;
+    throw Error(bbox_error_message(m, key, f, f == 0 ? v0 : f1_host[i]));
+  }
+  throw InternalError("predict: regressor output outside exp range for " + to_string(key));
+}
+
+}  // namespace ssg
+
+namespace servesim {
+
+double EstimatorModel::predict(OpName op, std::int64_t tp, const FeatureMap& features) const {
+  const PerOpModel& m = find(op, tp);
+  double v[2] = {0.0, 0.0};
+  for (std::size_t f = 0; f < m.schema.size(); ++f) {
+    auto it = features.find(m.schema[f]);
+    require(it != features.end(), "estimator: query for " + to_string(OpModelKey{op, tp}) +
+                                      " missing feature " + m.schema[f]);
+    v[f] = it->second;
+  }
+  const auto& de = device();
+  auto& ctx = ssg::context();
+  const int32_t slot = de.slot(op, tp);
+  ssg::DeviceBuffer<double> buf(4);
+  ssg::DeviceBuffer<unsigned long long> err(1);
+  unsigned long long none = SSG_NO_ERROR;
+  err.upload(&none, 1, ctx.stream);
+  buf.upload(v, 2, ctx.stream);
+  ssg::launch_predict(de, 1, nullptr, slot, buf.ptr, buf.ptr + 1, buf.ptr + 2, err.ptr, ctx.stream);
+  double out = 0.0;
+  unsigned long long word = 0;
+  cudaMemcpyAsync(&out, buf.ptr + 2, 8, cudaMemcpyDeviceToHost, ctx.stream);
+  cudaMemcpyAsync(&word, err.ptr, 8, cudaMemcpyDeviceToHost, ctx.stream);
+  ssg::cuda_check(cudaStreamSynchronize(ctx.stream), "predict");
+  if (word != SSG_NO_ERROR) ssg::raise_predict_error(*this, word, nullptr, slot, v, v + 1);
+  return out;
+}
+
+}  // namespace servesim

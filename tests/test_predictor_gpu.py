@@ -1,0 +1,94 @@
+"""K1/K2 parity: GPU EstimatorModel::predict vs the compiled reference, bit for bit.
+
+Reference: estimator.hpp:105-123, regressor.hpp:103-108,256-264,308-341.
+The oracle is the reference library itself (oracle/_ref), trained with the
+reference's own train(); the GPU path loads that same JSON.
+"""
+import numpy as np
+import pytest
+
+from paper_2405_05465_b200 import catalog, OPS
+
+pytestmark = pytest.mark.gpu
+
+
+def queries(op, kvb, n, rng):
+    """Feature draws shaped like the BASELINE cfg #3 microbench plus grid/edge points."""
+    u = rng.random(n)
+    f0 = np.floor(4096.0 ** u)
+    f1 = None
+    if op in ("attn_prefill", "attn_decode"):
+        f1 = np.floor((512.0 * 4096.0) ** rng.random(n)) * kvb
+        f1[:5] = [0.0, kvb, 512 * 4096 * kvb, 2 * kvb, 1.0]
+    elif op in ("allreduce", "allgather", "send_recv"):
+        f0 = np.floor(1024.0 * 1048576.0 ** u)
+        f0[:3] = [1024.0, 2.0 ** 30, 3.0 * 2 ** 20]
+    f0[:2] = [1.0, 4096.0] if op not in ("allreduce", "allgather", "send_recv") else f0[:2]
+    return f0, f1
+
+
+@pytest.mark.parametrize("model,dev,tps,reg", [
+    ("llama2_70b", "h100_80g", [1, 2, 4], "interp"),
+    ("llama2_70b", "h100_80g", [4], "forest"),
+    ("llama2_7b", "a100_80g", [1, 2], "forest"),
+    ("internlm_20b", "a100_80g", [1, 2, 4], "interp"),
+])
+def test_predict_bit_exact(ssg, ref, model, dev, tps, reg):
+    est_json = ref.train(catalog.MODELS[model], catalog.DEVICES[dev], tps, reg, 11)
+    mine = ssg.Estimator.from_json(est_json)
+    theirs = ref.Estimator(est_json)
+    rng = np.random.default_rng(5)
+    spec = catalog.MODELS[model]
+    for tp in tps:
+        kvb = 2 * (spec["num_kv_heads"] // tp) * spec["head_dim"] * spec["param_bytes_per_element"]
+        for op in OPS:
+            if mine.slot(op, tp) < 0:
+                continue
+            f0, f1 = queries(op, kvb, 4000, rng)
+            got = mine.predict(op, tp, f0, f1)
+            want, bad, msg = theirs.predict(OPS.index(op), tp, f0, f1)
+            assert bad == -1, msg
+            assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), (op, tp)
+
+
+def test_predict_mixed_and_errors(ssg, ref):
+    spec, dev = catalog.MODELS["llama2_70b"], catalog.DEVICES["h100_80g"]
+    est_json = ref.train(spec, dev, [4], "forest", 3)
+    mine = ssg.Estimator.from_json(est_json)
+    theirs = ref.Estimator(est_json)
+    rng = np.random.default_rng(9)
+    kvb = 2 * 2 * 128 * 2
+    n = 30000
+    ops = rng.choice([OPS.index("attn_prefill"), OPS.index("attn_decode"), OPS.index("mlp_up_proj")], n)
+    f0 = np.floor(4096.0 ** rng.random(n))
+    f1 = np.floor((512.0 * 4096.0) ** rng.random(n)) * kvb
+    slots = np.array([mine.slot(OPS[o], 4) for o in ops], dtype=np.int32)
+    got = mine.predict_mixed(slots, f0, f1)
+    want, bad, msg = theirs.predict(ops, 4, f0, f1)
+    assert bad == -1
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+    # guard violations: the lowest failing index wins, message verbatim
+    f0b = f0.copy()
+    f0b[[17, 400]] = [5000.0, 1e9]
+    with pytest.raises(ssg.InputError) as ei:
+        mine.predict_mixed(slots, f0b, f1)
+    _, bad, msg = theirs.predict(ops, 4, f0b, f1)
+    assert bad == 17
+    assert str(ei.value) == msg
+    f1b = f1.copy()
+    i = int(np.nonzero(ops == OPS.index("attn_decode"))[0][3])
+    f1b[i] = -1e12
+    with pytest.raises(ssg.InputError) as ei:
+        mine.predict_mixed(slots, f0, f1b)
+    _, bad, msg = theirs.predict(ops, 4, f0, f1b)
+    assert bad == i and str(ei.value) == msg
+
+
+def test_untrained_op_message(ssg, ref):
+    est_json = ref.train(catalog.MODELS["llama2_7b"], catalog.DEVICES["a100_80g"], [1], "interp", 0)
+    mine = ssg.Estimator.from_json(est_json)
+    with pytest.raises(ssg.InputError) as ei:
+        mine.predict("allreduce", 2, np.array([4096.0]))
+    assert str(ei.value) == ("estimator: no trained model for op allreduce@tp2 "
+                             "(profile and train must cover the config's operators)")
