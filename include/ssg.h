@@ -93,6 +93,47 @@ int ssg_predict_batch(const ssg_estimator* e, const char* model_spec_json, int64
                       const int64_t* d_off, const int64_t* d_ctx, double* seconds,
                       double* flops, ssg_status* st);
 
+/* ---- engine ------------------------------------------------------------ */
+/* run_simulation + build_report (sim.hpp:135-320, metrics.hpp:106-126) of one
+ * cluster over one trace (arrays in trace order).  cluster_json is a cluster
+ * document with the model spec and device embedded:
+ *   {"model_spec": {...}, "device": {...}, "parallelism": {...},
+ *    "scheduler": {...}, "routing": {"policy": ...}, "cpu_overhead_per_iter": x}
+ * abort_delay > 0 turns on the capacity-probe abort (SimOptions, sim.hpp:99-107).
+ * *out receives a JSON document (requests, replicas, iterations, report, and
+ * the per-batch log when record_batches); free with ssg_free. */
+int ssg_simulate(const char* cluster_json, const ssg_estimator* e, size_t n, const int64_t* ids,
+                 const double* arrivals, const int64_t* prefill, const int64_t* decode,
+                 int record_batches, double abort_delay, size_t abort_max_late, int static_mode,
+                 char** out, ssg_status* st);
+
+/* ---- search (Vidur-Search) --------------------------------------------- */
+/* One evaluated candidate, fixed-size so shards can be all-gathered as bytes.
+ * Fields as ConfigResult (search.hpp:182-194); `index` is the enumeration
+ * position (enumerate_configs order, search.hpp:76-129). */
+typedef struct ssg_config_record {
+  int64_t index;
+  double capacity_qps, qps_per_dollar, ttft_p90, tbt_p99, delay_p99, makespan;
+  int32_t slo_pass;
+  int32_t reserved;
+  char error[960];
+} ssg_config_record;
+
+size_t ssg_search_record_size(void);
+/* load_search_config + run_search + writers (config.hpp:111, search.hpp:369-486)
+ * over the configs i % num_shards == shard (1 shard = the whole search).
+ * *out: JSON {results_csv, frontier_ttft_csv, frontier_tbt_csv, summary,
+ * configs, best}; free with ssg_free.  With num_shards > 1 the other configs
+ * appear with default fields -- use _shard/_finalize to combine shards. */
+int ssg_search(const char* config_path, int shard, int num_shards, char** out, ssg_status* st);
+/* Evaluates this shard's configs into `records` (capacity >= ceil(N/num_shards)). */
+int ssg_search_shard(const char* config_path, int shard, int num_shards, ssg_config_record* records,
+                     size_t capacity, size_t* count, ssg_status* st);
+/* Ranking, Pareto frontiers and writers over the gathered records of every
+ * shard (search.hpp:395-486); byte-identical to the single-GPU outcome. */
+int ssg_search_finalize(const char* config_path, const ssg_config_record* records, size_t n,
+                        char** out, ssg_status* st);
+
 #ifdef __cplusplus
 }
 #endif

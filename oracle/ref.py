@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB = os.path.join(HERE, "_ref", "libservesim_ref.so")
+LIB = os.environ.get("SSG_REF_LIB", os.path.join(HERE, "_ref", "libservesim_ref.so"))
 
 _lib = None
 
@@ -60,10 +60,14 @@ class RefError(RuntimeError):
         self.kind = kind
 
 
-def _text(ptr) -> dict:
+def _raw(ptr) -> str:
     s = C.string_at(ptr).decode()
     lib().ref_free(ptr)
-    j = json.loads(s)
+    return s
+
+
+def _text(ptr) -> dict:
+    j = json.loads(_raw(ptr))
     if isinstance(j, dict) and "error" in j and "kind" in j:
         raise RefError(j["kind"], j["error"])
     return j
@@ -77,7 +81,11 @@ def train(model_spec: dict, device: dict, tps, regressor="interp", seed=0) -> st
     arr = np.asarray(tps, dtype=np.int64)
     ptr = lib().ref_train(json.dumps(model_spec).encode(), json.dumps(device).encode(), _p(arr),
                           len(arr), regressor.encode(), seed)
-    return json.dumps(_text(ptr))
+    text = _raw(ptr)  # the reference's own nlohmann dump, byte for byte
+    j = json.loads(text)
+    if "error" in j and "kind" in j:
+        raise RefError(j["kind"], j["error"])
+    return text
 
 
 class Estimator:

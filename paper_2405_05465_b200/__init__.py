@@ -147,3 +147,30 @@ def search(config_path: str, shard: int = 0, num_shards: int = 1) -> dict:
     out = C.c_void_p()
     _ffi.call("ssg_search", config_path.encode(), shard, num_shards, C.byref(out))
     return json.loads(_ffi.take_text(out))
+
+
+def record_size() -> int:
+    return _ffi.lib().ssg_search_record_size()
+
+
+def search_shard(config_path: str, shard: int, num_shards: int) -> bytes:
+    """This shard's ConfigResults as fixed-size records (ssg_config_record), for all-gather."""
+    import math
+
+    # capacity: every config could land in one shard; the header counts them
+    cap = 1 << 16
+    size = record_size()
+    buf = (C.c_char * (cap * size))()
+    n = C.c_size_t()
+    _ffi.call("ssg_search_shard", config_path.encode(), shard, num_shards, buf, cap, C.byref(n))
+    return bytes(buf[: n.value * size])
+
+
+def search_finalize(config_path: str, records: bytes) -> dict:
+    """Ranking + Pareto + writers over all shards' records."""
+    size = record_size()
+    assert len(records) % size == 0
+    out = C.c_void_p()
+    buf = C.create_string_buffer(records, len(records))
+    _ffi.call("ssg_search_finalize", config_path.encode(), buf, len(records) // size, C.byref(out))
+    return json.loads(_ffi.take_text(out))

@@ -72,7 +72,7 @@ _SIGNATURES = {
                                C.c_size_t, C.c_int, C.POINTER(C.c_void_p), C.POINTER(Status)]),
     "ssg_search": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.POINTER(C.c_void_p),
                              C.POINTER(Status)]),
-    "ssg_search_shard": (C.c_int, [C.c_char_p, C.c_int, C.c_int, P, C.c_size_t,
+    "ssg_search_shard": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_void_p, C.c_size_t,
                                    C.POINTER(C.c_size_t), C.POINTER(Status)]),
     "ssg_search_finalize": (C.c_int, [C.c_char_p, P, C.c_size_t, C.POINTER(C.c_void_p),
                                       C.POINTER(Status)]),

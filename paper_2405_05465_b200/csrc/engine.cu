@@ -1,0 +1,600 @@
+// engine.cu -- K3 kernel: the discrete-event loop over a unit's replicas.
+//
+// reference: sim.hpp:135-320 (run_simulation), sim.hpp:42-47 (event order),
+//            scheduler.hpp:146-233 (enqueue, complete_iteration),
+//            scheduler.hpp:492-561 (Router)
+//
+// Event order.  The reference pushes every arrival first (seq 0..N-1) and then
+// BatchStart/BatchComplete events with increasing seq; ties on time break on
+// seq.  Each replica has at most one pending BatchStart/BatchComplete, so the
+// device queue is "next arrival" plus one slot per replica, and the next event
+// is a warp-wide (time, seq) argmin over those slots.  RequestComplete events
+// are pure bookkeeping in the reference and are not materialised; seq stays
+// monotone in push order, which is all the ordering depends on.
+#include "engine.cuh"
+#include "runtime.h"
+#include "sim_engine.h"
+#include "sim_host.h"
+
+namespace ssgk {
+
+// ---------------------------------------------------------------- helpers
+__device__ __forceinline__ RepState load_rep(Unit& U, int r) {
+  __syncwarp();
+  RepState s = U.reps[r];
+  __syncwarp();
+  return s;
+}
+__device__ __forceinline__ void store_rep(Unit& U, int r, const RepState& s) {
+  __syncwarp();
+  if (U.lane == 0) U.reps[r] = s;
+  __syncwarp();
+}
+
+// ReplicaScheduler::enqueue (scheduler.hpp:146-155)
+__device__ bool enqueue(Unit& U, RepState& S, int r, int32_t j) {
+  const SimConfig& c = *U.cfg;
+  const ReqHot h = U.hot[j];
+  const int64_t need = units_for(c, (int64_t)h.prefill + h.decode);
+  if (need > c.total_units) {
+    set_error(U, SSG_ERR_ENQUEUE, r, U.ids[j], need, (double)c.total_units);
+    return false;
+  }
+  wput(U, &U.hot[j].target, h.prefill + h.emitted);
+  wait_insert(U, S, r, j);
+  S.outstanding += 1;
+  return true;
+}
+
+// start_if_idle (sim.hpp:191-195): has_work() == outstanding() > 0
+__device__ __forceinline__ void start_if_idle(Unit& U, RepState& S) {
+  if (S.busy || S.outstanding == 0) return;
+  S.ev_kind = 1;
+  S.ev_time = U.clock;
+  S.ev_seq = U.seq++;
+  S.busy = 1;
+}
+
+// Router::drain for the deferred policy (scheduler.hpp:532-551) followed by the
+// engine's enqueue + start_if_idle per assignment (sim.hpp:197-202).
+__device__ void drain_pool(Unit& U) {
+  const SimConfig& c = *U.cfg;
+  if (c.routing != SSG_ROUTE_DEFERRED) return;
+  int32_t* pool = POOL(U);
+  int32_t* ph = POOL_HEAD(U);  // [0] head, [1] size
+  int32_t head = ph[0], size = ph[1];
+  if (size == 0) return;
+  const int R = U.u->R;
+  // counts snapshot, one lane per replica
+  int64_t cnt = INT64_MAX;
+  if (U.lane < R) cnt = U.reps[U.lane].outstanding;
+  const int mask = U.WC - 1;
+  // assignments are decided first, then applied in order
+  int32_t assigned = 0;
+  while (size > 0) {
+    // best = lowest index among counts < threshold with the smallest count
+    int64_t key = (U.lane < R && cnt < c.defer_threshold) ? ((cnt << 8) | U.lane) : INT64_MAX;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      int64_t t = __shfl_xor_sync(SSG_FULL, key, o);
+      key = t < key ? t : key;
+    }
+    if (key == INT64_MAX) break;
+    const int best = (int)(key & 0xff);
+    const int32_t j = pool[head & mask];
+    head = (head + 1) & mask;
+    size -= 1;
+    if (U.lane == best) cnt += 1;
+    // stash the decision in the drained slot: pool[(head-1)] = j | best<<24 is
+    // not needed -- apply immediately, outstanding counts were snapshotted
+    RepState S = load_rep(U, best);
+    const bool ok = enqueue(U, S, best, j);
+    if (ok) start_if_idle(U, S);
+    store_rep(U, best, S);
+    if (!ok) break;
+    ++assigned;
+  }
+  wput(U, &ph[0], head);
+  wput(U, &ph[1], size);
+}
+
+// complete_iteration (scheduler.hpp:197-233), warp-parallel over the batch.
+__device__ void complete_batch(Unit& U, RepState& S, int r) {
+  const int32_t np = S.np, nd = S.nd;
+  const bool emit_times = (U.u->flags & SSG_UF_EMISSIONS) != 0;
+  int newly_finished = 0;
+  bool bad = false;
+  for (int32_t k = U.lane; k < np + nd; k += 32) {
+    int32_t j;
+    bool emit;
+    if (k < np) {
+      j = P_IDX(U, r)[k];
+      ReqHot& h = U.hot[j];
+      const int32_t done = h.done + P_CHUNK(U, r)[k];
+      h.done = done;
+      h.kv = done;
+      if (done > h.target) bad = true;  // "prefill progressed past its target"
+      emit = done >= h.target;
+    } else {
+      j = D_IDX(U, r)[k - np];
+      U.hot[j].kv = D_CTX(U, r)[k - np];
+      emit = true;
+    }
+    if (emit) {
+      ReqHot& h = U.hot[j];
+      if (h.emitted >= h.decode) bad = true;  // "emit_token on finished request"
+      const int32_t e = h.emitted + 1;
+      h.emitted = e;
+      if (emit_times) U.emissions[U.emit_base[j] + e - 1] = U.clock;
+      ReqTimes& t = U.tm[j];
+      if (t.first_tok < 0) t.first_tok = U.clock;
+      if (e >= h.decode) {
+        t.completion = U.clock;
+        ++newly_finished;
+      }
+    }
+  }
+  __syncwarp();
+  if (__any_sync(SSG_FULL, bad)) {
+    set_error(U, SSG_ERR_INTERNAL, 4, 0, 0, 0.0);
+    return;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) newly_finished += __shfl_xor_sync(SSG_FULL, newly_finished, o);
+  S.outstanding -= newly_finished;
+  // release finished runners; drop them from running unless FT froze membership
+  int32_t* a = RUN(U, r);
+  int32_t write = 0;
+  int64_t freed = 0;
+  bool any_unfinished = false;
+  for (int32_t base = 0; base < S.run_n; base += 32) {
+    const int32_t p = base + U.lane;
+    int32_t j = -1;
+    bool fin = false;
+    if (p < S.run_n) {
+      j = a[p];
+      ReqHot& h = U.hot[j];
+      fin = h.emitted >= h.decode;
+      if (fin) {
+        freed += h.held;
+        h.held = 0;
+      } else {
+        any_unfinished = true;
+      }
+    }
+    if (!S.ft_inflight) {
+      const unsigned keep = __ballot_sync(SSG_FULL, p < S.run_n && !fin);
+      const int dst = write + __popc(keep & ((1u << U.lane) - 1u));
+      __syncwarp();
+      if (p < S.run_n && !fin) a[dst] = j;
+      write += __popc(keep);
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) freed += __shfl_xor_sync(SSG_FULL, freed, o);
+  S.allocated -= freed;
+  if (!S.ft_inflight) {
+    S.run_n = write;
+  } else if (!__any_sync(SSG_FULL, any_unfinished)) {
+    S.run_n = 0;
+    S.ft_inflight = 0;
+  }
+  __syncwarp();
+}
+
+// One BatchStart event (sim.hpp:221-283).  Returns false when the unit must
+// stop (error or probe abort).
+__device__ bool batch_start(Unit& U, RepState& S, int r) {
+  const SimConfig& c = *U.cfg;
+  U.serial += 1;
+  S.np = 0;
+  S.nd = 0;
+  switch (c.policy) {
+    case SSG_POL_FT: schedule_ft(U, S, r); break;
+    case SSG_POL_VLLM: schedule_vllm(U, S, r); break;
+    case SSG_POL_ORCA:
+    case SSG_POL_LIGHTLLM: schedule_orca(U, S, r); break;
+    case SSG_POL_SARATHI: schedule_sarathi(U, S, r); break;
+  }
+  if (failed(U)) return false;
+  if (S.np + S.nd == 0) {
+    S.busy = 0;
+    S.ev_kind = 0;
+    return true;
+  }
+  int32_t tokens = S.nd;
+  for (int32_t k = 0; k < S.np; ++k) tokens += P_CHUNK(U, r)[k];
+  if (c.policy == SSG_POL_SARATHI && tokens > c.chunk) {
+    set_error(U, SSG_ERR_INTERNAL, 5, tokens, 0, 0.0);  // sarathi: token budget exceeded
+    return false;
+  }
+  // batch log (SimObserver::on_batch payload, before the abort check)
+  int64_t log_hdr = -1;
+  if (U.u->flags & SSG_UF_BATCH_LOG) {
+    const int64_t need = 6 + 3LL * S.np + 2LL * S.nd;
+    const int64_t used = U.out->log_used;
+    if (used >= 0 && used + need <= U.u->log_cap) {
+      int64_t* L = U.log + used;
+      if (U.lane == 0) {
+        L[0] = r;
+        L[1] = __double_as_longlong(U.clock);
+        L[2] = S.allocated;
+        L[3] = S.np;
+        L[4] = S.nd;
+        L[5] = 0;
+      }
+      for (int32_t k = U.lane; k < S.np; k += 32) {
+        L[6 + 3 * k] = U.ids[P_IDX(U, r)[k]];
+        L[7 + 3 * k] = P_CHUNK(U, r)[k];
+        L[8 + 3 * k] = P_PRIOR(U, r)[k];
+      }
+      for (int32_t k = U.lane; k < S.nd; k += 32) {
+        L[6 + 3 * S.np + 2 * k] = U.ids[D_IDX(U, r)[k]];
+        L[7 + 3 * S.np + 2 * k] = D_CTX(U, r)[k];
+      }
+      log_hdr = used;
+      wput(U, &U.out->log_used, used + need);
+    } else {
+      wput(U, &U.out->log_used, (int64_t)-1);  // overflow: log incomplete
+    }
+  }
+  // capacity-probe abort (sim.hpp:231-240)
+  if (U.u->flags & SSG_UF_ABORT) {
+    int late = 0;
+    for (int32_t k = U.lane; k < S.np + S.nd; k += 32) {
+      const int32_t j = k < S.np ? P_IDX(U, r)[k] : D_IDX(U, r)[k - S.np];
+      const ReqTimes t = U.tm[j];
+      if (t.first_sched == U.clock && U.clock - t.arrival > U.u->abort_thr) ++late;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) late += __shfl_xor_sync(SSG_FULL, late, o);
+    if (late) {
+      const int total = U.out->late + late;
+      wput(U, &U.out->late, total);
+      if (total > U.u->abort_max_late) {
+        wput(U, &U.out->aborted, 1);
+        return false;
+      }
+    }
+  }
+  double lat = 0.0, flops = 0.0;
+  if (batch_latency(U, S, r, &lat, &flops) != SSG_OK) return false;
+  if (log_hdr >= 0) wput(U, &U.log[log_hdr + 5], (int64_t)__double_as_longlong(lat));
+  S.busy_time = __dadd_rn(S.busy_time, lat);
+  S.iterations += 1;
+  S.tokens += tokens;
+  const double util = (double)S.allocated / (double)c.total_units;
+  S.peak_kv = S.peak_kv < util ? util : S.peak_kv;
+  wput(U, &U.out->flops, __dadd_rn(U.out->flops, flops));
+  S.ev_kind = 2;
+  S.ev_time = __dadd_rn(U.clock, lat);
+  S.ev_seq = U.seq++;
+  return true;
+}
+
+__device__ void run_unit(Unit& U) {
+  const SimUnit& u = *U.u;
+  const SimConfig& c = *U.cfg;
+  const int R = u.R;
+  // ---- reset per-request state and replicas
+  for (int32_t j = U.lane; j < u.n; j += 32) {
+    ReqHot& h = U.hot[j];
+    h.target = 0;
+    h.done = 0;
+    h.emitted = 0;
+    h.kv = 0;
+    h.held = 0;
+    h.planned = 0;
+    ReqTimes& t = U.tm[j];
+    t.first_sched = -1.0;
+    t.first_tok = -1.0;
+    t.completion = -1.0;
+    U.restarts[j] = 0;
+  }
+  for (int r = U.lane; r < R; r += 32) {
+    RepState s;
+    memset(&s, 0, sizeof s);
+    U.reps[r] = s;
+  }
+  if (U.lane == 0) {
+    POOL_HEAD(U)[0] = 0;
+    POOL_HEAD(U)[1] = 0;
+    SimUnitOut o;
+    memset(&o, 0, sizeof o);
+    *U.out = o;
+  }
+  __syncwarp();
+  U.clock = 0.0;
+  U.seq = (uint64_t)u.n;
+  U.serial = 0;
+  int32_t next_arrival = 0;
+  int32_t rr_next = 0;
+  int64_t events = 0;
+  while (true) {
+    // ---- next event: (time, seq) argmin over the arrival head and replica slots
+    double bt = INFINITY;
+    uint64_t bs = ~0ull;
+    int bw = -2;  // -1 arrival, r >= 0 replica
+    if (next_arrival < u.n) {
+      const int32_t j = U.arr_order ? U.arr_order[next_arrival] : next_arrival;
+      bt = U.tm[j].arrival;
+      bs = (uint64_t)next_arrival;
+      bw = -1;
+    }
+    for (int r0 = 0; r0 < R; r0 += 32) {
+      const int r = r0 + U.lane;
+      double t = INFINITY;
+      uint64_t q = ~0ull;
+      if (r < R && U.reps[r].ev_kind != 0) {
+        t = U.reps[r].ev_time;
+        q = U.reps[r].ev_seq;
+      }
+      int w = r;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double t2 = __shfl_xor_sync(SSG_FULL, t, o);
+        const uint64_t q2 = __shfl_xor_sync(SSG_FULL, q, o);
+        const int w2 = __shfl_xor_sync(SSG_FULL, w, o);
+        if (t2 < t || (t2 == t && q2 < q)) {
+          t = t2;
+          q = q2;
+          w = w2;
+        }
+      }
+      if (q != ~0ull && (t < bt || (t == bt && q < bs))) {
+        bt = t;
+        bs = q;
+        bw = w;
+      }
+    }
+    if (bw == -2) break;
+    if (bt < U.clock) {
+      set_error(U, SSG_ERR_INTERNAL, 6, 0, 0, bt);  // event time regression
+      break;
+    }
+    U.clock = bt;
+    ++events;
+    if (bw == -1) {
+      // ---- Arrival: route, enqueue, start_if_idle (sim.hpp:211-220)
+      const int32_t j = U.arr_order ? U.arr_order[next_arrival] : next_arrival;
+      ++next_arrival;
+      int dest = 0;
+      if (c.routing == SSG_ROUTE_RR) {
+        dest = rr_next;
+        rr_next = (rr_next + 1) % R;
+      } else if (c.routing == SSG_ROUTE_LO) {
+        // argmin outstanding, ties to the lowest index
+        int64_t key = INT64_MAX;
+        for (int r0 = 0; r0 < R; r0 += 32) {
+          const int r = r0 + U.lane;
+          int64_t k2 = r < R ? (((int64_t)U.reps[r].outstanding) << 16 | r) : INT64_MAX;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const int64_t t2 = __shfl_xor_sync(SSG_FULL, k2, o);
+            k2 = t2 < k2 ? t2 : k2;
+          }
+          key = k2 < key ? k2 : key;
+        }
+        dest = (int)(key & 0xffff);
+      } else {
+        // deferred: pool the request, then drain
+        int32_t* ph = POOL_HEAD(U);
+        const int32_t head = ph[0], size = ph[1];
+        wput(U, &POOL(U)[(head + size) & (U.WC - 1)], j);
+        wput(U, &ph[1], size + 1);
+        drain_pool(U);
+        if (failed(U)) break;
+        continue;
+      }
+      RepState S = load_rep(U, dest);
+      const bool ok = enqueue(U, S, dest, j);
+      if (ok) start_if_idle(U, S);
+      store_rep(U, dest, S);
+      if (!ok) break;
+      continue;
+    }
+    const int r = bw;
+    RepState S = load_rep(U, r);
+    if (S.ev_kind == 1) {
+      S.ev_kind = 0;
+      const bool ok = batch_start(U, S, r);
+      store_rep(U, r, S);
+      if (!ok) break;
+    } else {
+      // ---- BatchComplete (sim.hpp:284-293)
+      S.ev_kind = 0;
+      complete_batch(U, S, r);
+      S.np = 0;
+      S.nd = 0;
+      S.busy = 0;
+      if (failed(U)) {
+        store_rep(U, r, S);
+        break;
+      }
+      start_if_idle(U, S);
+      store_rep(U, r, S);
+      drain_pool(U);
+      if (failed(U)) break;
+    }
+  }
+  if (U.lane == 0) {
+    U.out->span = U.clock;
+    U.out->events = events;
+  }
+  __syncwarp();
+  if (!failed(U) && !U.out->aborted) {
+    // "simulation drained with unfinished request" (sim.hpp:305-306)
+    int32_t first_bad = INT32_MAX;
+    for (int32_t j = U.lane; j < u.n; j += 32) {
+      const ReqHot h = U.hot[j];
+      if (h.emitted < h.decode && j < first_bad) first_bad = j;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const int32_t t = __shfl_xor_sync(SSG_FULL, first_bad, o);
+      first_bad = t < first_bad ? t : first_bad;
+    }
+    if (first_bad != INT32_MAX) set_error(U, SSG_ERR_INTERNAL, 7, U.ids[first_bad], 0, 0.0);
+  }
+}
+
+__global__ void __launch_bounds__(SSG_SIM_WARPS * 32)
+    k_simulate(SimLaunch L) {
+  __shared__ int64_t stats[SSG_SIM_WARPS][SSG_MAX_PP * 6];
+  __shared__ double part[SSG_SIM_WARPS][4 * SSG_MAX_PP];
+  const int wib = threadIdx.x >> 5;
+  const int64_t w = (int64_t)blockIdx.x * SSG_SIM_WARPS + wib;
+  if (w >= L.nunits) return;
+  const int32_t uid = L.order ? L.order[w] : (int32_t)w;
+  Unit U;
+  U.u = L.units + uid;
+  U.cfg = L.configs + U.u->config;
+  U.E = L.ests[U.cfg->est];
+  U.hot = L.hot + U.u->req_off;
+  U.tm = L.tm + U.u->req_off;
+  U.ids = L.ids + U.u->req_off;
+  U.restarts = L.restarts + U.u->req_off;
+  U.emit_base = L.emit_base ? L.emit_base + U.u->req_off : nullptr;
+  U.emissions = L.emissions;
+  U.arr_order = L.arr_order ? L.arr_order + U.u->req_off : nullptr;
+  U.reps = L.reps + U.u->rep_off;
+  U.ws = L.ws + U.u->ws_off;
+  U.log = L.log ? L.log + U.u->log_off : nullptr;
+  U.out = L.out + uid;
+  U.smem_stats = stats[wib];
+  U.smem_part = part[wib];
+  U.group_late = nullptr;
+  U.lane = threadIdx.x & 31;
+  U.MB = U.cfg->max_batch;
+  U.WC = U.u->wait_cap;
+  U.rep_stride = 6LL * U.MB + U.WC;
+  run_unit(U);
+}
+
+// predict_batch / batch_device_flops for standalone compositions (the
+// estimator.hpp:294-380 API): one warp per composition, same device code path
+// as the engine's per-iteration latency.
+__global__ void __launch_bounds__(SSG_SIM_WARPS * 32)
+    k_predict_batch(const SimConfig* cfg, SsgEstView E, int64_t n, int32_t MB, int32_t* ws,
+                    const int32_t* np_nd, double* seconds, double* flops, SimUnitOut* out) {
+  __shared__ int64_t stats[SSG_SIM_WARPS][SSG_MAX_PP * 6];
+  __shared__ double part[SSG_SIM_WARPS][4 * SSG_MAX_PP];
+  const int wib = threadIdx.x >> 5;
+  const int64_t c = (int64_t)blockIdx.x * SSG_SIM_WARPS + wib;
+  if (c >= n) return;
+  Unit U;
+  SimUnit dummy;
+  memset(&dummy, 0, sizeof dummy);
+  dummy.R = 1;
+  U.u = &dummy;
+  U.cfg = cfg;
+  U.E = E;
+  U.MB = MB;
+  U.WC = 2;
+  U.rep_stride = 6LL * MB + 2;
+  U.ws = ws + c * (U.rep_stride + 4);
+  U.out = out + c;
+  U.smem_stats = stats[wib];
+  U.smem_part = part[wib];
+  U.lane = threadIdx.x & 31;
+  U.clock = 0.0;
+  if (U.lane == 0) {
+    SimUnitOut o;
+    memset(&o, 0, sizeof o);
+    *U.out = o;
+  }
+  __syncwarp();
+  RepState S;
+  memset(&S, 0, sizeof S);
+  S.np = np_nd[2 * c];
+  S.nd = np_nd[2 * c + 1];
+  double lat = 0.0, fl = 0.0;
+  if (batch_latency(U, S, 0, &lat, &fl) == SSG_OK && U.lane == 0) {
+    seconds[c] = lat;
+    flops[c] = fl;
+  }
+}
+
+}  // namespace ssgk
+
+namespace ssg {
+
+void launch_simulate(const SimLaunch& L, cudaStream_t s) {
+  if (L.nunits <= 0) return;
+  const int64_t blocks = (L.nunits + SSG_SIM_WARPS - 1) / SSG_SIM_WARPS;
+  ssgk::k_simulate<<<(unsigned)blocks, SSG_SIM_WARPS * 32, 0, s>>>(L);
+  cuda_check(cudaGetLastError(), "k_simulate launch");
+}
+
+}  // namespace ssg
+
+namespace ssg {
+
+void predict_batches(const servesim::EstimatorModel& est, const SimConfig& cfg_in, int64_t n,
+                     const int64_t* p_off, const int64_t* p_len, const int64_t* p_prior,
+                     const int64_t* d_off, const int64_t* d_ctx, double* seconds, double* flops) {
+  using namespace servesim;
+  if (n <= 0) return;
+  auto& ctx = context();
+  cudaStream_t s = ctx.stream;
+  const auto& de = est.device();
+  SimConfig cfg = cfg_in;
+  cfg.pp = 1;
+  cfg.tp = 1;
+  cfg.cpu_overhead = 0.0;
+  int64_t MB = 1;
+  for (int64_t c = 0; c < n; ++c) {
+    const int64_t np = p_off[c + 1] - p_off[c], nd = d_off[c + 1] - d_off[c];
+    require(np + nd > 0, "predict_batch: empty batch");
+    for (int64_t k = p_off[c]; k < p_off[c + 1]; ++k)
+      require(p_len[k] > 0, "equivalent_prefill_length: lengths must be positive");
+    MB = std::max<int64_t>(MB, std::max(np, nd));
+  }
+  internal_check(MB < (1 << 24), "predict_batch: composition too large");
+  const int64_t stride = 6 * MB + 2 + 4;
+  std::vector<int32_t> ws(static_cast<std::size_t>(stride * n), 0), np_nd(2 * n);
+  for (int64_t c = 0; c < n; ++c) {
+    int32_t* w = ws.data() + c * stride;
+    const int64_t np = p_off[c + 1] - p_off[c], nd = d_off[c + 1] - d_off[c];
+    np_nd[2 * c] = static_cast<int32_t>(np);
+    np_nd[2 * c + 1] = static_cast<int32_t>(nd);
+    int32_t* pc = w + MB + 2 + MB;  // P_CHUNK = P_IDX + MB, P_IDX = MB + WC
+    for (int64_t k = 0; k < np; ++k) {
+      require(p_len[p_off[c] + k] < INT32_MAX && p_prior[p_off[c] + k] < INT32_MAX &&
+                  p_prior[p_off[c] + k] >= 0,
+              "ssg: prefill entry outside the device engine range");
+      pc[k] = static_cast<int32_t>(p_len[p_off[c] + k]);
+      pc[MB + k] = static_cast<int32_t>(p_prior[p_off[c] + k]);
+    }
+    int32_t* dc = w + MB + 2 + 4 * MB;  // D_CTX = P_IDX + 4 MB
+    for (int64_t k = 0; k < nd; ++k) {
+      require(d_ctx[d_off[c] + k] >= 0 && d_ctx[d_off[c] + k] < INT32_MAX,
+              "ssg: decode context outside the device engine range");
+      dc[k] = static_cast<int32_t>(d_ctx[d_off[c] + k]);
+    }
+  }
+  DeviceBuffer<SimConfig> d_cfg;
+  DeviceBuffer<int32_t> d_ws, d_npnd;
+  DeviceBuffer<double> d_sec, d_fl;
+  DeviceBuffer<SimUnitOut> d_out;
+  d_cfg.upload(&cfg, 1, s);
+  d_ws.upload(ws, s);
+  d_npnd.upload(np_nd, s);
+  d_sec.resize(n);
+  d_fl.resize(n);
+  d_out.resize(n);
+  const int64_t blocks = (n + SSG_SIM_WARPS - 1) / SSG_SIM_WARPS;
+  ssgk::k_predict_batch<<<(unsigned)blocks, SSG_SIM_WARPS * 32, 0, s>>>(
+      d_cfg.ptr, de.view, n, static_cast<int32_t>(MB), d_ws.ptr, d_npnd.ptr, d_sec.ptr, d_fl.ptr, d_out.ptr);
+  cuda_check(cudaGetLastError(), "k_predict_batch launch");
+  std::vector<SimUnitOut> out(n);
+  d_out.download(out.data(), n, s);
+  d_sec.download(seconds, n, s);
+  d_fl.download(flops, n, s);
+  cuda_check(cudaStreamSynchronize(s), "predict_batch");
+  for (int64_t c = 0; c < n; ++c)
+    if (out[c].code != SSG_OK) raise_unit_error(out[c], cfg, est);
+}
+
+}  // namespace ssg

@@ -1,0 +1,681 @@
+// engine.cuh -- K3: one warp simulates one unit (a replica, or a routed group
+// of replicas) event by event, exactly as the reference's engine and
+// schedulers do.
+//
+// reference: sim.hpp:135-320 (event loop), scheduler.hpp:136-561 (policies,
+//            preemption, routing), memory.hpp:51-104 (block accounting),
+//            estimator.hpp:294-380 (batch latency and flops),
+//            scheduler.hpp:566-579 (pipeline makespan)
+//
+// Execution model.  All 32 lanes run the scheduler's control flow together on
+// identical (warp-uniform) scalars held in registers.  Every store of shared
+// sequential state goes through wput(): a warp barrier (all lanes finished
+// reading the old value), one store from lane 0, a second barrier (the value is
+// visible to every lane) -- so no lane ever depends on implicit lockstep.
+// The data-parallel pieces -- decode admission over the running queue,
+// completion of a batch, queue shifts, per-entry reductions and the per-
+// operator predictor evaluations -- spread over lanes and end in __syncwarp().
+// Sequential semantics that matter for parity (admission order, preemption of
+// the latest unplanned runner, operator-order fp64 sums, tree-order forest
+// sums) are kept exactly; parallel fast paths are taken only where they are
+// provably equivalent (e.g. a decode window whose cumulative block shortfall
+// fits in free memory cannot preempt).
+#pragma once
+#include "predictor.cuh"
+#include "sim_device.h"
+
+#define SSG_FULL 0xffffffffu
+
+namespace ssgk {
+
+struct Unit {
+  const SimConfig* cfg;
+  const SimUnit* u;
+  SsgEstView E;
+  ReqHot* hot;
+  ReqTimes* tm;
+  const int64_t* ids;
+  int32_t* restarts;
+  const int64_t* emit_base;
+  double* emissions;
+  const int32_t* arr_order;
+  RepState* reps;
+  int32_t* ws;
+  int64_t* log;
+  SimUnitOut* out;
+  int64_t* smem_stats;  // per-warp shared scratch [SSG_MAX_PP * 6]
+  double* smem_part;    // per-warp shared scratch [4 * SSG_MAX_PP]
+  int* group_late;  // shared by the probe's units (may be null)
+  int lane;
+  int64_t rep_stride;  // int32 words per replica in ws
+  int32_t MB, WC;
+  int32_t serial;      // schedule_iteration counter (planned_ stamp)
+  double clock;
+  uint64_t seq;
+};
+
+// ---------------------------------------------------------------- workspace
+__device__ __forceinline__ int32_t* rep_ws(Unit& U, int r) { return U.ws + r * U.rep_stride; }
+__device__ __forceinline__ int32_t* RUN(Unit& U, int r) { return rep_ws(U, r); }
+__device__ __forceinline__ int32_t* WAIT(Unit& U, int r) { return rep_ws(U, r) + U.MB; }
+__device__ __forceinline__ int32_t* P_IDX(Unit& U, int r) { return rep_ws(U, r) + U.MB + U.WC; }
+__device__ __forceinline__ int32_t* P_CHUNK(Unit& U, int r) { return P_IDX(U, r) + U.MB; }
+__device__ __forceinline__ int32_t* P_PRIOR(Unit& U, int r) { return P_IDX(U, r) + 2 * U.MB; }
+__device__ __forceinline__ int32_t* D_IDX(Unit& U, int r) { return P_IDX(U, r) + 3 * U.MB; }
+__device__ __forceinline__ int32_t* D_CTX(Unit& U, int r) { return P_IDX(U, r) + 4 * U.MB; }
+__device__ __forceinline__ int32_t* POOL(Unit& U) { return U.ws + U.u->R * U.rep_stride; }
+// pool ring state lives after the pool itself
+__device__ __forceinline__ int32_t* POOL_HEAD(Unit& U) { return POOL(U) + U.WC; }
+
+__host__ __device__ inline int64_t unit_ws_words(int R, int MB, int WC) {
+  return (int64_t)R * (6LL * MB + WC) + WC + 2;
+}
+
+// ---------------------------------------------------------------- stores
+template <typename T>
+__device__ __forceinline__ void wput(const Unit& U, T* p, T v) {
+  __syncwarp();
+  if (U.lane == 0) *p = v;
+  __syncwarp();
+}
+
+// ---------------------------------------------------------------- errors
+__device__ __forceinline__ void set_error(Unit& U, int code, int32_t i32, int64_t a, int64_t b,
+                                          double f) {
+  __syncwarp();
+  if (U.lane == 0 && U.out->code == SSG_OK) {
+    U.out->code = code;
+    U.out->err_i32 = i32;
+    U.out->err_i64[0] = a;
+    U.out->err_i64[1] = b;
+    U.out->err_f64 = f;
+    U.out->err_time = U.clock;
+  }
+  __syncwarp();
+}
+__device__ __forceinline__ bool failed(Unit& U) { return U.out->code != SSG_OK; }
+
+// ---------------------------------------------------------------- blocks
+__device__ __forceinline__ int64_t units_for(const SimConfig& c, int64_t tokens) {
+  return c.token_granular ? tokens : (tokens + c.block_size - 1) / c.block_size;
+}
+__device__ __forceinline__ int64_t shortfall(const SimConfig& c, const ReqHot& h, int64_t tokens) {
+  int64_t s = units_for(c, tokens) - (int64_t)h.held;
+  return s > 0 ? s : 0;
+}
+// BlockManager::try_reserve (memory.hpp:82-89)
+__device__ __forceinline__ bool try_reserve(Unit& U, RepState& S, int32_t j, int64_t tokens) {
+  const SimConfig& c = *U.cfg;
+  const int64_t need = shortfall(c, U.hot[j], tokens);
+  if (need > c.total_units - S.allocated) return false;
+  wput(U, &U.hot[j].held, U.hot[j].held + (int32_t)need);
+  S.allocated += need;
+  return true;
+}
+// BlockManager::release (memory.hpp:91-97)
+__device__ __forceinline__ void release(Unit& U, RepState& S, int32_t j) {
+  S.allocated -= U.hot[j].held;
+  wput(U, &U.hot[j].held, 0);
+}
+
+// ---------------------------------------------------------------- queues
+// Shift a[lo, hi) by `delta` (+1 or -1) positions, warp-cooperatively; the
+// ring variant maps logical positions through (base + p) & mask.
+__device__ __forceinline__ void ring_shift(Unit& U, int32_t* a, int32_t mask, int32_t base,
+                                           int32_t lo, int32_t hi, int delta) {
+  const int n = hi - lo;
+  if (n <= 0) return;
+  if (delta < 0) {
+    for (int c = 0; c < n; c += 32) {
+      const int p = lo + c + U.lane;
+      int32_t v = 0;
+      if (p < hi) v = a[(base + p) & mask];
+      __syncwarp();
+      if (p < hi) a[(base + p - 1) & mask] = v;
+      __syncwarp();
+    }
+  } else {
+    for (int c = n; c > 0; c -= 32) {
+      const int p = lo + c - 1 - U.lane;
+      int32_t v = 0;
+      if (p >= lo) v = a[(base + p) & mask];
+      __syncwarp();
+      if (p >= lo) a[(base + p + 1) & mask] = v;
+      __syncwarp();
+    }
+  }
+}
+
+// first logical position whose value is > x (upper_bound) in a sorted ring
+__device__ __forceinline__ int32_t ring_upper(const int32_t* a, int32_t mask, int32_t base,
+                                              int32_t n, int32_t x) {
+  int32_t first = 0, count = n;
+  while (count > 0) {
+    int32_t step = count >> 1;
+    if (!(x < a[(base + first + step) & mask])) {
+      first += step + 1;
+      count -= step + 1;
+    } else {
+      count = step;
+    }
+  }
+  return first;
+}
+
+// insert_sorted(waiting_, r) (scheduler.hpp:243-247)
+__device__ void wait_insert(Unit& U, RepState& S, int r, int32_t j) {
+  int32_t* w = WAIT(U, r);
+  const int32_t mask = U.WC - 1;
+  int32_t pos;
+  if (S.wait_n == 0 || w[(S.wait_head + S.wait_n - 1) & mask] < j)
+    pos = S.wait_n;
+  else
+    pos = ring_upper(w, mask, S.wait_head, S.wait_n, j);
+  if (pos < S.wait_n - pos) {  // shift the front part left by one
+    ring_shift(U, w, mask, S.wait_head, 0, pos, -1);
+    S.wait_head = (S.wait_head - 1) & mask;
+  } else {
+    ring_shift(U, w, mask, S.wait_head, pos, S.wait_n, +1);
+  }
+  wput(U, &w[(S.wait_head + pos) & mask], j);
+  S.wait_n += 1;
+}
+
+// erase_from_waiting (scheduler.hpp:474-478); the queue is sorted, so the
+// element's position is its lower bound.
+__device__ void wait_erase(Unit& U, RepState& S, int r, int32_t j) {
+  int32_t* w = WAIT(U, r);
+  const int32_t mask = U.WC - 1;
+  int32_t pos = ring_upper(w, mask, S.wait_head, S.wait_n, j - 1);
+  if (pos >= S.wait_n || w[(S.wait_head + pos) & mask] != j) {
+    set_error(U, SSG_ERR_INTERNAL, 1, j, 0, 0.0);  // "request not in waiting queue"
+    return;
+  }
+  if (pos < S.wait_n - 1 - pos) {
+    ring_shift(U, w, mask, S.wait_head, 0, pos, +1);
+    S.wait_head = (S.wait_head + 1) & mask;
+  } else {
+    ring_shift(U, w, mask, S.wait_head, pos + 1, S.wait_n, -1);
+  }
+  S.wait_n -= 1;
+  __syncwarp();
+}
+
+__device__ __forceinline__ int32_t wait_front(Unit& U, const RepState& S, int r) {
+  return WAIT(U, r)[S.wait_head & (U.WC - 1)];
+}
+
+// insert_sorted_running (scheduler.hpp:249-252)
+__device__ void run_insert(Unit& U, RepState& S, int r, int32_t j) {
+  int32_t* a = RUN(U, r);
+  int32_t pos;
+  if (S.run_n == 0 || a[S.run_n - 1] < j)
+    pos = S.run_n;
+  else
+    pos = ring_upper(a, 0x7fffffff, 0, S.run_n, j);
+  ring_shift(U, a, 0x7fffffff, 0, pos, S.run_n, +1);
+  wput(U, &a[pos], j);
+  S.run_n += 1;
+}
+
+__device__ void run_erase_at(Unit& U, RepState& S, int r, int32_t pos) {
+  int32_t* a = RUN(U, r);
+  ring_shift(U, a, 0x7fffffff, 0, pos + 1, S.run_n, -1);
+  S.run_n -= 1;
+  __syncwarp();
+}
+
+// ---------------------------------------------------------------- scheduler
+__device__ __forceinline__ bool finished(const ReqHot& h) { return h.emitted >= h.decode; }
+__device__ __forceinline__ bool prefill_complete(const ReqHot& h) { return h.done >= h.target; }
+
+// mark_scheduled (scheduler.hpp:262-265)
+__device__ __forceinline__ void mark_scheduled(Unit& U, int32_t j) {
+  if (U.tm[j].first_sched < 0) wput(U, &U.tm[j].first_sched, U.clock);
+  wput(U, &U.hot[j].planned, U.serial);
+}
+
+// preempt_latest (scheduler.hpp:269-285): returns the victim or -1.
+__device__ int32_t preempt_latest(Unit& U, RepState& S, int r) {
+  int32_t* a = RUN(U, r);
+  for (int32_t p = S.run_n - 1; p >= 0; --p) {
+    const int32_t v = a[p];
+    if (U.hot[v].planned == U.serial) continue;
+    run_erase_at(U, S, r, p);
+    release(U, S, v);
+    ReqHot& h = U.hot[v];
+    wput(U, &h.kv, 0);
+    wput(U, &h.done, 0);
+    wput(U, &h.target, h.prefill + h.emitted);
+    wput(U, &U.restarts[v], U.restarts[v] + 1);
+    S.preemptions += 1;
+    wait_insert(U, S, r, v);  // victim was unfinished: outstanding unchanged
+    return v;
+  }
+  return -1;
+}
+
+// ensure_decode_memory (scheduler.hpp:290-296)
+__device__ bool ensure_decode_memory(Unit& U, RepState& S, int r, int32_t j) {
+  while (!try_reserve(U, S, j, (int64_t)U.hot[j].kv + 1)) {
+    const int32_t victim = preempt_latest(U, S, r);
+    if (victim < 0 || victim == j) return false;
+  }
+  return true;
+}
+
+// admit_reserve (scheduler.hpp:302-316)
+__device__ bool admit_reserve(Unit& U, RepState& S, int r, int32_t j, int64_t target,
+                              bool allow_preempt, bool use_watermark) {
+  const SimConfig& c = *U.cfg;
+  while (true) {
+    const int64_t need = shortfall(c, U.hot[j], target);
+    const int64_t floor = (use_watermark && S.run_n > 0) ? c.watermark_units : 0;
+    if ((c.total_units - S.allocated) - need >= floor) break;
+    if (!allow_preempt) return false;
+    const int32_t victim = preempt_latest(U, S, r);
+    if (victim < 0 || victim == j) return false;
+  }
+  return try_reserve(U, S, j, target);
+}
+
+__device__ __forceinline__ void push_prefill(Unit& U, RepState& S, int r, int32_t j, int32_t chunk,
+                                             int32_t prior) {
+  wput(U, &P_IDX(U, r)[S.np], j);
+  wput(U, &P_CHUNK(U, r)[S.np], chunk);
+  wput(U, &P_PRIOR(U, r)[S.np], prior);
+  S.np += 1;
+}
+
+// schedule_decodes (scheduler.hpp:449-472).  Fast path: a 32-entry window of
+// the running queue is judged at once -- eligibility, batch cap / token budget
+// and the cumulative block shortfall against free units.  Entries up to the
+// first one that would not fit are admitted together (no preemption can occur
+// for them); that entry, if any, replays the sequential ensure_decode_memory
+// path, after which the window scan resumes.
+__device__ void schedule_decodes(Unit& U, RepState& S, int r, int32_t max_entries,
+                                 int32_t* budget) {
+  const SimConfig& c = *U.cfg;
+  int32_t i = 0;
+  while (i < S.run_n) {
+    const int32_t* a = RUN(U, r);
+    const int p = i + U.lane;
+    int32_t j = -1;
+    bool elig = false;
+    int64_t need = 0;
+    if (p < S.run_n) {
+      j = a[p];
+      const ReqHot h = U.hot[j];
+      elig = !finished(h) && prefill_complete(h) && h.planned != U.serial;
+      if (elig) need = shortfall(c, h, (int64_t)h.kv + 1);
+    }
+    const unsigned em = __ballot_sync(SSG_FULL, elig);
+    if (em == 0) {
+      i += 32;
+      continue;
+    }
+    // exclusive count of eligible entries before this lane; inclusive need sum
+    const int before = __popc(em & ((1u << U.lane) - 1u));
+    int64_t incl = need;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t t = __shfl_up_sync(SSG_FULL, incl, o);
+      if (U.lane >= o) incl += t;
+    }
+    const int32_t batch0 = S.np + S.nd;
+    const int64_t free0 = c.total_units - S.allocated;
+    const bool cap_ok = (batch0 + before < max_entries) && (!budget || *budget - before >= 1);
+    const bool mem_ok = incl <= free0;
+    const unsigned stop = __ballot_sync(SSG_FULL, elig && !(cap_ok && mem_ok));
+    const int first_stop = stop ? __ffs(stop) - 1 : 32;
+    // admit the eligible entries before first_stop
+    const bool take = elig && U.lane < first_stop;
+    const unsigned tm = __ballot_sync(SSG_FULL, take);
+    const int ntake = __popc(tm);
+    if (take) {
+      ReqHot& h = U.hot[j];
+      h.held += (int32_t)need;  // distinct requests per lane
+      if (U.tm[j].first_sched < 0) U.tm[j].first_sched = U.clock;
+      h.planned = U.serial;
+      D_IDX(U, r)[S.nd + before] = j;
+      D_CTX(U, r)[S.nd + before] = h.kv + 1;
+    }
+    __syncwarp();
+    int64_t taken_need = __shfl_sync(SSG_FULL, incl, first_stop == 0 ? 0 : first_stop - 1);
+    // inclusive prefix at the last taken lane (non-eligible lanes add 0)
+    if (ntake == 0) taken_need = 0;
+    __syncwarp();
+    S.allocated += taken_need;
+    S.nd += ntake;
+    if (budget) *budget -= ntake;
+    if (first_stop == 32) {
+      i += 32;
+      continue;
+    }
+    // the stopping entry: cap/budget -> the reference breaks out of the loop
+    const int32_t js = __shfl_sync(SSG_FULL, j, first_stop);
+    if (S.np + S.nd >= max_entries) return;
+    if (budget && *budget < 1) return;
+    // memory shortfall: sequential ensure_decode_memory with preemption
+    i = i + first_stop;
+    if (!ensure_decode_memory(U, S, r, js)) {
+      if (i < S.run_n && RUN(U, r)[i] == js) ++i;
+      continue;
+    }
+    mark_scheduled(U, js);
+    wput(U, &D_IDX(U, r)[S.nd], js);
+    wput(U, &D_CTX(U, r)[S.nd], U.hot[js].kv + 1);
+    S.nd += 1;
+    if (budget) *budget -= 1;
+    int32_t pos = 0;
+    const int32_t* a2 = RUN(U, r);
+    while (pos < S.run_n && a2[pos] != js) ++pos;
+    i = pos + 1;
+  }
+}
+
+__device__ void schedule_vllm(Unit& U, RepState& S, int r) {
+  const SimConfig& c = *U.cfg;
+  int32_t budget = c.max_tokens;
+  while (S.wait_n > 0 && S.run_n < c.max_batch) {
+    const int32_t head = wait_front(U, S, r);
+    const int32_t prompt = U.hot[head].target;
+    const bool alone = prompt > c.max_tokens;
+    if (alone && S.np > 0) break;
+    if (!alone && prompt > budget) break;
+    if (!admit_reserve(U, S, r, head, prompt, true, true)) break;
+    wait_erase(U, S, r, head);
+    run_insert(U, S, r, head);
+    mark_scheduled(U, head);
+    push_prefill(U, S, r, head, prompt, 0);
+    budget -= (prompt < budget ? prompt : budget);
+    if (alone || budget == 0) break;
+  }
+  __syncwarp();
+  if (S.np > 0) return;
+  schedule_decodes(U, S, r, c.max_batch, nullptr);
+}
+
+__device__ void schedule_orca(Unit& U, RepState& S, int r) {
+  const SimConfig& c = *U.cfg;
+  int32_t budget = c.max_tokens;
+  while (S.wait_n > 0 && S.run_n < c.max_batch) {
+    const int32_t head = wait_front(U, S, r);
+    const int32_t prompt = U.hot[head].target;
+    const bool alone = prompt > c.max_tokens;
+    if (alone && S.np > 0) break;
+    if (!alone && prompt > budget) break;
+    if (!admit_reserve(U, S, r, head, prompt, false, true)) break;
+    wait_erase(U, S, r, head);
+    run_insert(U, S, r, head);
+    mark_scheduled(U, head);
+    push_prefill(U, S, r, head, prompt, 0);
+    budget -= (prompt < budget ? prompt : budget);
+    if (alone) return;
+    if (budget == 0) break;
+  }
+  __syncwarp();
+  schedule_decodes(U, S, r, c.max_batch, &budget);
+}
+
+__device__ void schedule_sarathi(Unit& U, RepState& S, int r) {
+  const SimConfig& c = *U.cfg;
+  int32_t budget = c.chunk;
+  schedule_decodes(U, S, r, c.max_batch, &budget);
+  for (int32_t i = 0; i < S.run_n; ++i) {
+    if (budget < 1 || S.np + S.nd >= c.max_batch) break;
+    const int32_t j = RUN(U, r)[i];
+    const ReqHot h = U.hot[j];
+    if (finished(h) || prefill_complete(h)) continue;
+    const int32_t rem = h.target - h.done;
+    const int32_t chunk = budget < rem ? budget : rem;
+    if (!admit_reserve(U, S, r, j, (int64_t)h.done + chunk, false, false)) break;
+    mark_scheduled(U, j);
+    push_prefill(U, S, r, j, chunk, h.done);
+    budget -= chunk;
+  }
+  while (budget > 0 && S.wait_n > 0 && S.run_n < c.max_batch && S.np + S.nd < c.max_batch) {
+    const int32_t head = wait_front(U, S, r);
+    const int32_t t = U.hot[head].target;
+    const int32_t chunk = budget < t ? budget : t;
+    if (!admit_reserve(U, S, r, head, chunk, false, true)) break;
+    wait_erase(U, S, r, head);
+    run_insert(U, S, r, head);
+    mark_scheduled(U, head);
+    push_prefill(U, S, r, head, chunk, 0);
+    budget -= chunk;
+  }
+  __syncwarp();
+}
+
+__device__ void schedule_ft(Unit& U, RepState& S, int r) {
+  const SimConfig& c = *U.cfg;
+  if (!S.ft_inflight) {
+    while (S.wait_n > 0 && S.run_n < c.max_batch) {
+      const int32_t head = wait_front(U, S, r);
+      const ReqHot h = U.hot[head];
+      const int64_t final_ctx = (int64_t)h.target + (h.decode - h.emitted);
+      if (!try_reserve(U, S, head, final_ctx)) break;
+      S.wait_head = (S.wait_head + 1) & (U.WC - 1);
+      S.wait_n -= 1;
+      run_insert(U, S, r, head);
+    }
+    __syncwarp();
+    if (S.run_n == 0) return;
+    S.ft_inflight = 1;
+  }
+  const int32_t* a = RUN(U, r);
+  for (int32_t i = 0; i < S.run_n; ++i) {
+    const int32_t j = a[i];
+    const ReqHot h = U.hot[j];
+    if (!finished(h) && !prefill_complete(h)) {
+      mark_scheduled(U, j);
+      push_prefill(U, S, r, j, h.target - h.done, h.done);
+      __syncwarp();
+      return;
+    }
+  }
+  for (int32_t i = 0; i < S.run_n; ++i) {
+    const int32_t j = a[i];
+    const ReqHot h = U.hot[j];
+    if (finished(h)) continue;
+    mark_scheduled(U, j);
+    wput(U, &D_IDX(U, r)[S.nd], j);
+    wput(U, &D_CTX(U, r)[S.nd], h.kv + 1);
+    S.nd += 1;
+  }
+}
+
+// ---------------------------------------------------------------- latency
+// predict_batch / batch_device_flops per microbatch (estimator.hpp:294-380),
+// split_microbatches (sim.hpp:118-130) and pipeline_makespan
+// (scheduler.hpp:566-579).  Per-entry sums are integer (exact in any order);
+// the per-operator predictions run one per lane and are then added strictly
+// in operator order, microbatch by microbatch, as the reference does.
+__device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, double* flops_out) {
+  const SimConfig& c = *U.cfg;
+  const int pp = c.pp;
+  int64_t* st = U.smem_stats;  // [pp][6]: prefills, tokens, sum p^2, sum prior, decodes, sum ctx
+  const int32_t total = S.np + S.nd;
+  for (int m = 0; m < pp; ++m) {
+    int64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0;
+    for (int32_t k = U.lane; k < total; k += 32) {
+      if (k % pp != m) continue;
+      if (k < S.np) {
+        const int64_t ch = P_CHUNK(U, r)[k];
+        a0 += 1;
+        a1 += ch;
+        a2 += ch * ch;
+        a3 += P_PRIOR(U, r)[k];
+      } else {
+        a1 += 1;
+        a4 += 1;
+        a5 += D_CTX(U, r)[k - S.np];
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a0 += __shfl_xor_sync(SSG_FULL, a0, o);
+      a1 += __shfl_xor_sync(SSG_FULL, a1, o);
+      a2 += __shfl_xor_sync(SSG_FULL, a2, o);
+      a3 += __shfl_xor_sync(SSG_FULL, a3, o);
+      a4 += __shfl_xor_sync(SSG_FULL, a4, o);
+      a5 += __shfl_xor_sync(SSG_FULL, a5, o);
+    }
+    if (U.lane == 0) {
+      st[m * 6 + 0] = a0;
+      st[m * 6 + 1] = a1;
+      st[m * 6 + 2] = a2;
+      st[m * 6 + 3] = a3;
+      st[m * 6 + 4] = a4;
+      st[m * 6 + 5] = a5;
+    }
+  }
+  __syncwarp();
+  const int nops = c.nops;
+  const int work = pp * nops;
+  double* secs_part = U.smem_part;       // [pp]
+  double* flop_part = U.smem_part + SSG_MAX_PP;
+  double acc_s = 0.0, acc_f = 0.0;
+  int cur_m = 0;
+  int err = SSG_OK, err_task = 0, err_feat = 0;
+  double err_val = 0.0;
+  for (int base = 0; base < work; base += 32) {
+    const int t = base + U.lane;
+    double pred = 0.0, fl = 0.0, v0 = 0.0, v1 = 0.0;
+    bool active = false;
+    int code = SSG_OK, bad = 0;
+    if (t < work) {
+      const int m = t / nops;
+      const SimOp& o = c.ops[t - m * nops];
+      const int64_t* s = st + m * 6;
+      const double tokens = (double)s[1];
+      if (s[1] > 0) {
+        if (o.cls == SSG_CLS_TOKEN) {
+          active = true;
+          v0 = tokens;
+          if (o.flop_kind == 0)
+            fl = __dmul_rn(__dmul_rn(__dmul_rn(2.0, tokens), o.fa), o.fb);
+          else if (o.flop_kind == 1)
+            fl = __dmul_rn(tokens, o.fa);
+          else
+            fl = __dmul_rn(__dmul_rn(8.0, tokens), o.fa);
+        } else if (o.cls == SSG_CLS_SEQ) {
+          if (o.flop_kind == 3 && s[0] > 0) {
+            active = true;
+            const double n_eq = (double)ssg_llround_nonneg(sqrt((double)s[2]));
+            v0 = n_eq;
+            v1 = __dmul_rn((double)s[3], o.kvb);
+            const double ctx_tokens = v1 / o.kvb;
+            fl = __dmul_rn(__dmul_rn(__dmul_rn(4.0, n_eq), __dadd_rn(n_eq, ctx_tokens)), o.fa);
+          } else if (o.flop_kind == 4 && s[4] > 0) {
+            active = true;
+            v0 = (double)s[4];
+            v1 = __dmul_rn((double)s[5], o.kvb);
+            const double ctx_tokens = v1 / o.kvb;
+            fl = __dmul_rn(__dmul_rn(4.0, ctx_tokens), o.fa);
+          }
+        } else {
+          active = true;
+          v0 = __dmul_rn(tokens, o.payload);
+        }
+      }
+      if (active) {
+        code = ssg_predict_one(U.E, o.slot, v0, v1, &pred, &bad);
+        pred = __dmul_rn(o.count, pred);
+        fl = (o.cls == SSG_CLS_COMM) ? 0.0 : __dmul_rn(o.count, fl);
+      }
+    }
+    const unsigned em = __ballot_sync(SSG_FULL, code != SSG_OK);
+    if (em && err == SSG_OK) {
+      const int src = __ffs(em) - 1;
+      err = __shfl_sync(SSG_FULL, code, src);
+      err_task = base + src;
+      err_feat = __shfl_sync(SSG_FULL, bad, src);
+      err_val = __shfl_sync(SSG_FULL, bad ? v1 : v0, src);
+    }
+    const int kmax = (work - base) < 32 ? (work - base) : 32;
+    for (int k = 0; k < kmax; ++k) {
+      const double pk = __shfl_sync(SSG_FULL, pred, k);
+      const double fk = __shfl_sync(SSG_FULL, fl, k);
+      const int ak = __shfl_sync(SSG_FULL, (int)active, k);
+      const int m = (base + k) / nops;
+      if (m != cur_m) {
+        if (U.lane == 0) {
+          secs_part[cur_m] = acc_s;
+          flop_part[cur_m] = acc_f;
+        }
+        acc_s = 0.0;
+        acc_f = 0.0;
+        cur_m = m;
+      }
+      if (ak) {
+        acc_s = __dadd_rn(acc_s, pk);
+        if (c.ops[(base + k) - m * nops].cls != SSG_CLS_COMM) acc_f = __dadd_rn(acc_f, fk);
+      }
+    }
+  }
+  if (U.lane == 0) {
+    secs_part[cur_m] = acc_s;
+    flop_part[cur_m] = acc_f;
+  }
+  __syncwarp();
+  if (err != SSG_OK) {
+    const SimOp& o = c.ops[err_task % nops];
+    set_error(U, err, o.slot, err_feat, 0, err_val);
+    return err;
+  }
+  double lat = 0.0, flops = 0.0;
+  if (pp == 1) {
+    lat = secs_part[0];
+    if (!(lat > 0.0)) {
+      set_error(U, SSG_ERR_INTERNAL, 2, 0, 0, lat);  // predict_batch: non-positive prediction
+      return SSG_ERR_INTERNAL;
+    }
+    flops = __dmul_rn(flop_part[0], (double)c.tp);
+  } else {
+    // compact the non-empty microbatches' times into part[2*MAX..]; makespan
+    double* times = U.smem_part + 2 * SSG_MAX_PP;
+    double* finish = U.smem_part + 3 * SSG_MAX_PP;
+    int nt = 0;
+    for (int m = 0; m < pp; ++m) {
+      if (st[m * 6 + 1] == 0) continue;
+      if (!(secs_part[m] > 0.0)) {
+        set_error(U, SSG_ERR_INTERNAL, 2, 0, 0, secs_part[m]);
+        return SSG_ERR_INTERNAL;
+      }
+      flops = __dadd_rn(flops, __dmul_rn(flop_part[m], (double)(c.tp * c.pp)));
+      if (U.lane == 0) {
+        times[nt] = secs_part[m];
+        finish[nt] = 0.0;
+      }
+      ++nt;
+    }
+    __syncwarp();
+    // every lane runs the makespan on its own registers-through-smem copy;
+    // lane 0 owns the stores
+    for (int s = 0; s < pp; ++s) {
+      double prev = 0.0;
+      for (int m = 0; m < nt; ++m) {
+        const double f = finish[m];
+        const double start = f < prev ? prev : f;
+        prev = __dadd_rn(start, times[m]);
+        __syncwarp();
+        if (U.lane == 0) finish[m] = prev;
+        __syncwarp();
+      }
+    }
+    lat = nt ? finish[nt - 1] : 0.0;
+    __syncwarp();
+  }
+  lat = __dadd_rn(lat, c.cpu_overhead);
+  if (!(lat > 0.0)) {
+    set_error(U, SSG_ERR_INTERNAL, 3, 0, 0, lat);  // non-positive iteration latency
+    return SSG_ERR_INTERNAL;
+  }
+  *latency = lat;
+  *flops_out = flops;
+  return SSG_OK;
+}
+
+}  // namespace ssgk

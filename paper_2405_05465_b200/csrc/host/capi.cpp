@@ -8,10 +8,16 @@
 #include <cstring>
 #include <functional>
 
+#include "json.hpp"
 #include "runtime.h"
 #include "servesim_b200.hpp"
+#include "sim_host.h"
 
 using namespace servesim;
+
+namespace servesim {
+ClusterConfig parse_cluster_inline(const std::string& text);  // config.cpp
+}
 
 struct ssg_estimator {
   EstimatorModel model;
@@ -195,6 +201,185 @@ int ssg_predict_device(const ssg_estimator* e, size_t n, const int32_t* d_slots,
             "predict: invalid model slot");
     ssg::launch_predict(de, static_cast<int64_t>(n), d_slots, uniform_slot, d_f0, d_f1, d_out,
                         d_first_error, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int ssg_predict_batch(const ssg_estimator* e, const char* model_spec_json, int64_t tp, size_t n,
+                      const int64_t* p_off, const int64_t* p_len, const int64_t* p_prior,
+                      const int64_t* d_off, const int64_t* d_ctx, double* seconds, double* flops,
+                      ssg_status* st) {
+  return guarded(st, [&] {
+    ModelSpec spec = parse_model_spec(model_spec_json);
+    auto ops = derive_operators(spec, ParallelismConfig{tp, 1, 1});
+    for (const auto& d : ops) e->model.find(d.op, d.tp_degree);
+    SimConfig cfg{};
+    ssg::fill_sim_ops(cfg, ops, e->model.device());
+    std::vector<double> fl(n);
+    ssg::predict_batches(e->model, cfg, static_cast<int64_t>(n), p_off, p_len, p_prior, d_off, d_ctx,
+                         seconds, flops ? flops : fl.data());
+  });
+}
+
+int ssg_simulate(const char* cluster_json, const ssg_estimator* e, size_t n, const int64_t* ids,
+                 const double* arrivals, const int64_t* prefill, const int64_t* decode,
+                 int record_batches, double abort_delay, size_t abort_max_late, int static_mode,
+                 char** out, ssg_status* st) {
+  return guarded(st, [&] {
+    ClusterConfig cluster = parse_cluster_inline(cluster_json);
+    std::vector<Request> trace(n);
+    for (size_t i = 0; i < n; ++i) trace[i] = Request{ids[i], arrivals[i], prefill[i], decode[i]};
+    SimOptions o;
+    o.record_iterations = true;
+    o.record_batches = record_batches != 0;
+    o.abort_delay_threshold = abort_delay;
+    o.abort_max_late = abort_max_late;
+    nlohmann::json j;
+    SimulationOutput so;
+    try {
+      so = run_simulation_logged(cluster, trace, e->model, o);
+    } catch (const ProbeInfeasible&) {
+      j["probe_infeasible"] = true;
+      *out = dup_text(j.dump(), nullptr);
+      return;
+    }
+    const SimulationResult& r = so.result;
+    nlohmann::json reqs = nlohmann::json::array();
+    for (const auto& q : r.requests)
+      reqs.push_back({{"id", q.id},
+                      {"arrival", q.arrival},
+                      {"first_scheduled", q.first_scheduled},
+                      {"first_token", q.first_token},
+                      {"completion", q.completion},
+                      {"restarts", q.restarts},
+                      {"emissions", q.emission_times}});
+    nlohmann::json reps = nlohmann::json::array();
+    for (const auto& a : r.replicas)
+      reps.push_back({{"busy_time", a.busy_time},
+                      {"iterations", a.iterations},
+                      {"tokens_processed", a.tokens_processed},
+                      {"peak_kv_utilization", a.peak_kv_utilization},
+                      {"preemptions", a.preemptions}});
+    nlohmann::json iters = nlohmann::json::array();
+    for (const auto& it : r.iterations)
+      iters.push_back({it.start, it.latency, it.replica, it.batch_requests, it.current_tokens,
+                       it.prefill_entries, it.decode_entries, it.kv_utilization});
+    auto rep = build_report(r, static_mode != 0);
+    auto summ = [](const MetricSummary& s) {
+      return nlohmann::json{{"mean", s.mean}, {"p50", s.p50}, {"p90", s.p90}, {"p95", s.p95}, {"p99", s.p99}};
+    };
+    j["requests"] = std::move(reqs);
+    j["replicas"] = std::move(reps);
+    j["iterations"] = std::move(iters);
+    j["simulated_span"] = r.simulated_span;
+    j["total_model_flops"] = r.total_model_flops;
+    j["num_devices"] = r.num_devices;
+    j["report"] = {{"scheduling_delay", summ(rep.scheduling_delay)},
+                   {"ttft", summ(rep.ttft)},
+                   {"tbt", summ(rep.tbt)},
+                   {"e2e", summ(rep.e2e)},
+                   {"normalized", summ(rep.normalized)},
+                   {"mfu", rep.cluster.mfu},
+                   {"kv_utilization_peak", rep.cluster.kv_utilization_peak},
+                   {"busy_fraction", rep.cluster.busy_fraction},
+                   {"preemptions", rep.cluster.preemptions}};
+    j["requests_csv"] = request_metrics_to_csv(rep);
+    if (record_batches) {
+      nlohmann::json log = nlohmann::json::array();
+      for (const auto& b : so.batches) {
+        nlohmann::json ent = nlohmann::json::array();
+        for (const auto& en : b.entries) ent.push_back({en.prefill ? 1 : 0, en.request_id, en.tokens, en.context});
+        log.push_back({{"replica", b.replica}, {"now", b.now}, {"kv", b.kv_allocated_units}, {"entries", ent}});
+      }
+      j["batches"] = std::move(log);
+    }
+    *out = dup_text(j.dump(), nullptr);
+  });
+}
+
+size_t ssg_search_record_size(void) { return sizeof(ssg_config_record); }
+
+namespace {
+
+nlohmann::json outcome_json(const SearchOutcome& o, const std::string& objective) {
+  nlohmann::json j;
+  j["results_csv"] = search_results_to_csv(o);
+  j["frontier_ttft_csv"] = frontier_to_csv(o, o.frontier_ttft, true);
+  j["frontier_tbt_csv"] = frontier_to_csv(o, o.frontier_tbt, false);
+  j["summary"] = search_summary_text(o, objective);
+  j["configs"] = o.results.size();
+  if (o.best) j["best"] = o.results[*o.best].config.id;
+  return j;
+}
+
+}  // namespace
+
+int ssg_search(const char* config_path, int shard, int num_shards, char** out, ssg_status* st) {
+  return guarded(st, [&] {
+    require(num_shards >= 1 && shard >= 0 && shard < num_shards, "ssg_search: bad shard");
+    auto cfg = load_search_config(config_path);
+    auto results = evaluate_configs_shard(cfg.spec, cfg.workload, cfg.options, shard, num_shards);
+    auto o = finalize_search(cfg.spec, cfg.options, std::move(results));
+    *out = dup_text(outcome_json(o, cfg.options.objective).dump(), nullptr);
+  });
+}
+
+int ssg_search_shard(const char* config_path, int shard, int num_shards, ssg_config_record* records,
+                     size_t capacity, size_t* count, ssg_status* st) {
+  return guarded(st, [&] {
+    require(num_shards >= 1 && shard >= 0 && shard < num_shards, "ssg_search_shard: bad shard");
+    auto cfg = load_search_config(config_path);
+    auto results = evaluate_configs_shard(cfg.spec, cfg.workload, cfg.options, shard, num_shards);
+    size_t k = 0;
+    for (size_t i = 0; i < results.size(); ++i) {
+      if (static_cast<int>(i % static_cast<size_t>(num_shards)) != shard) continue;
+      require(k < capacity, "ssg_search_shard: record buffer too small");
+      const ConfigResult& r = results[i];
+      ssg_config_record& rec = records[k++];
+      std::memset(&rec, 0, sizeof rec);
+      rec.index = static_cast<int64_t>(i);
+      rec.capacity_qps = r.capacity_qps;
+      rec.qps_per_dollar = r.qps_per_dollar;
+      rec.ttft_p90 = r.ttft_p90;
+      rec.tbt_p99 = r.tbt_p99;
+      rec.delay_p99 = r.delay_p99;
+      rec.makespan = r.makespan;
+      rec.slo_pass = r.slo_pass ? 1 : 0;
+      internal_check(r.error.size() < sizeof(rec.error), "error message longer than a record");
+      std::memcpy(rec.error, r.error.data(), r.error.size());
+    }
+    *count = k;
+  });
+}
+
+int ssg_search_finalize(const char* config_path, const ssg_config_record* records, size_t n,
+                        char** out, ssg_status* st) {
+  return guarded(st, [&] {
+    auto cfg = load_search_config(config_path);
+    PolicyConfig base;
+    auto configs = enumerate_configs(cfg.spec, cfg.options.space, base);
+    std::vector<ConfigResult> results(configs.size());
+    std::vector<char> seen(configs.size(), 0);
+    for (size_t k = 0; k < n; ++k) {
+      const ssg_config_record& rec = records[k];
+      require(rec.index >= 0 && static_cast<size_t>(rec.index) < configs.size(),
+              "ssg_search_finalize: record index out of range");
+      ConfigResult& r = results[rec.index];
+      seen[rec.index] = 1;
+      r.config = configs[rec.index];
+      r.sku_name = cfg.options.space.skus[r.config.sku_index].sku_name;
+      r.capacity_qps = rec.capacity_qps;
+      r.qps_per_dollar = rec.qps_per_dollar;
+      r.ttft_p90 = rec.ttft_p90;
+      r.tbt_p99 = rec.tbt_p99;
+      r.delay_p99 = rec.delay_p99;
+      r.makespan = rec.makespan;
+      r.slo_pass = rec.slo_pass != 0;
+      r.error.assign(rec.error, strnlen(rec.error, sizeof(rec.error)));
+    }
+    for (size_t i = 0; i < seen.size(); ++i)
+      require(seen[i], "ssg_search_finalize: missing result for config " + configs[i].id);
+    auto o = finalize_search(cfg.spec, cfg.options, std::move(results));
+    *out = dup_text(outcome_json(o, cfg.options.objective).dump(), nullptr);
   });
 }
 

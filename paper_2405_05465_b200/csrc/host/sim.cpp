@@ -1,0 +1,468 @@
+// sim.cpp -- run_simulation on the GPU: config flattening, unit decomposition,
+// launch, and reassembly of the reference's SimulationResult.
+//
+// reference: sim.hpp:135-320, scheduler.hpp:146-155 (enqueue capacity error),
+//            model_spec.hpp:203-266 (operators), memory.hpp:21-46
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+
+#include "sim_host.h"
+#include "engine_limits.h"
+
+namespace ssg {
+
+using namespace servesim;
+
+void fill_sim_ops(SimConfig& c, const std::vector<OperatorDescriptor>& ops, const DeviceEstimator& de) {
+  internal_check(ops.size() <= SSG_MAX_OPS, "operator set larger than the device table");
+  c.nops = static_cast<int32_t>(ops.size());
+  for (std::size_t i = 0; i < ops.size(); ++i) {
+    const auto& d = ops[i];
+    SimOp& o = c.ops[i];
+    o.slot = de.slot(d.op, d.tp_degree);
+    o.cls = static_cast<int32_t>(d.op_class);
+    o.op = static_cast<int32_t>(d.op);
+    o.count = static_cast<double>(d.count);
+    o.kvb = 2.0 * static_cast<double>(d.elem_bytes) *
+            static_cast<double>(d.kv_heads_per_device * d.head_dim);
+    o.payload = static_cast<double>(d.payload_bytes_per_token);
+    switch (d.op) {
+      case OpName::QkvProj:
+      case OpName::AttnOutProj:
+      case OpName::MlpUpProj:
+      case OpName::MlpDownProj:
+        o.flop_kind = 0;
+        o.fa = static_cast<double>(d.in_dim);
+        o.fb = static_cast<double>(d.out_dim);
+        break;
+      case OpName::ActFn:
+        o.flop_kind = 1;
+        o.fa = static_cast<double>(d.in_dim);
+        break;
+      case OpName::AddNorm:
+        o.flop_kind = 2;
+        o.fa = static_cast<double>(d.in_dim);
+        break;
+      case OpName::AttnPrefill:
+      case OpName::AttnDecode:
+        o.flop_kind = d.op == OpName::AttnPrefill ? 3 : 4;
+        o.fa = static_cast<double>(d.q_heads_per_device * d.head_dim);
+        break;
+      default:
+        o.flop_kind = 5;
+        break;
+    }
+  }
+}
+
+SimConfig make_sim_config(const ClusterConfig& cl, const EstimatorModel& est, int32_t est_index,
+                          MemoryPlan* plan_out) {
+  validate(cl.spec);
+  validate(cl.spec, cl.par);
+  validate(cl.dev);
+  validate(cl.policy);
+  auto ops = derive_operators(cl.spec, cl.par);
+  for (const auto& d : ops) est.find(d.op, d.tp_degree);  // throws the reference's message
+  MemoryPlan plan = plan_memory(cl.spec, cl.par, cl.dev, cl.policy.block_size,
+                                cl.policy.watermark_fraction, cl.policy.activation_reserve_fraction);
+  if (plan_out) *plan_out = plan;
+  const std::int64_t threshold =
+      cl.deferred_threshold > 0 ? cl.deferred_threshold : cl.policy.max_batch_size;
+  require(cl.par.num_replicas >= 1, "router: need at least one replica");
+  require(threshold >= 1, "router: deferred threshold must be >= 1");
+
+  const auto& de = est.device();
+  SimConfig c{};
+  c.policy = static_cast<int32_t>(cl.policy.policy);
+  require(cl.policy.max_batch_size <= kMaxBatchEntries,
+          "ssg: max_batch_size above the device engine limit (" + std::to_string(kMaxBatchEntries) + ")");
+  require(cl.par.pp_degree <= SSG_MAX_PP,
+          "ssg: pp_degree above the device engine limit (" + std::to_string(SSG_MAX_PP) + ")");
+  c.max_batch = static_cast<int32_t>(cl.policy.max_batch_size);
+  c.max_tokens = static_cast<int32_t>(std::min<std::int64_t>(cl.policy.max_tokens_per_iter, INT32_MAX));
+  c.chunk = static_cast<int32_t>(std::min<std::int64_t>(cl.policy.chunk_size, INT32_MAX));
+  c.token_granular = cl.policy.policy == SchedulerPolicy::LightLLM ? 1 : 0;
+  c.pp = static_cast<int32_t>(cl.par.pp_degree);
+  c.tp = static_cast<int32_t>(cl.par.tp_degree);
+  c.est = est_index;
+  c.block_size = plan.block_size;
+  c.total_units = c.token_granular ? plan.kv_capacity_tokens : plan.num_blocks;
+  c.watermark_units = c.token_granular ? plan.watermark_blocks * plan.block_size : plan.watermark_blocks;
+  c.cpu_overhead = cl.cpu_overhead_per_iter;
+  c.nops = static_cast<int32_t>(ops.size());
+  c.routing = static_cast<int32_t>(cl.routing);
+  c.defer_threshold = static_cast<int32_t>(std::min<std::int64_t>(threshold, INT32_MAX));
+  fill_sim_ops(c, ops, de);
+  return c;
+}
+
+static int32_t pow2_above(int64_t n) {
+  int64_t c = 2;
+  while (c <= n) c <<= 1;
+  internal_check(c <= (int64_t(1) << 30), "unit too large for the device queue");
+  return static_cast<int32_t>(c);
+}
+
+int32_t SimJobs::add_unit(const UnitSpec& spec, const std::vector<Request>& reqs,
+                          const std::vector<int32_t>& event_order) {
+  const SimConfig& cfg = configs.at(spec.config);
+  SimUnit u{};
+  u.config = spec.config;
+  u.n = static_cast<int32_t>(reqs.size());
+  u.R = spec.R;
+  u.flags = spec.flags;
+  u.req_off = static_cast<int64_t>(hot.size());
+  u.wait_cap = pow2_above(u.n);
+  u.ws_off = ws_words;
+  ws_words += static_cast<int64_t>(u.R) * (6LL * cfg.max_batch + u.wait_cap) + u.wait_cap + 2;
+  u.rep_off = nreps;
+  nreps += u.R;
+  u.abort_thr = spec.abort_thr;
+  u.abort_max_late = spec.abort_max_late;
+  u.log_off = log_words;
+  u.log_cap = spec.log_cap;
+  log_words += spec.log_cap;
+  for (std::size_t j = 0; j < reqs.size(); ++j) {
+    const Request& r = reqs[j];
+    require(r.prefill_tokens < INT32_MAX / 2 && r.decode_tokens < INT32_MAX / 2,
+            "ssg: request lengths above the device engine limit");
+    ReqHot h{};
+    h.prefill = static_cast<int32_t>(r.prefill_tokens);
+    h.decode = static_cast<int32_t>(r.decode_tokens);
+    hot.push_back(h);
+    ReqTimes t{};
+    t.arrival = r.arrival_time;
+    tm.push_back(t);
+    ids.push_back(r.id);
+    if (spec.flags & SSG_UF_EMISSIONS) {
+      emit_base.push_back(emissions);
+      emissions += r.decode_tokens;
+    } else {
+      emit_base.push_back(-1);
+    }
+  }
+  if (!event_order.empty()) {
+    any_order = true;
+    for (auto k : event_order) arr_order.push_back(k);
+  } else {
+    for (int32_t k = 0; k < u.n; ++k) arr_order.push_back(k);
+  }
+  units.push_back(u);
+  return static_cast<int32_t>(units.size() - 1);
+}
+
+void run_jobs(const SimJobs& J, SimResults& R, bool want_requests) {
+  auto& ctx = context();
+  cudaStream_t s = ctx.stream;
+  DeviceBuffer<SimConfig> d_cfg;
+  DeviceBuffer<SsgEstView> d_est;
+  DeviceBuffer<SimUnit> d_units;
+  DeviceBuffer<ReqHot> d_hot;
+  DeviceBuffer<ReqTimes> d_tm;
+  DeviceBuffer<int64_t> d_ids, d_emit_base, d_log;
+  DeviceBuffer<int32_t> d_restarts, d_order, d_ws, d_launch;
+  DeviceBuffer<double> d_emis;
+  DeviceBuffer<RepState> d_reps;
+  DeviceBuffer<SimUnitOut> d_out;
+  d_cfg.upload(J.configs, s);
+  d_est.upload(J.ests, s);
+  d_units.upload(J.units, s);
+  d_hot.upload(J.hot, s);
+  d_tm.upload(J.tm, s);
+  d_ids.upload(J.ids, s);
+  d_restarts.resize(std::max<std::size_t>(1, J.hot.size()));
+  if (J.emissions > 0) {
+    d_emit_base.upload(J.emit_base, s);
+    d_emis.resize(static_cast<std::size_t>(J.emissions));
+  }
+  if (J.any_order) d_order.upload(J.arr_order, s);
+  d_ws.resize(static_cast<std::size_t>(std::max<int64_t>(1, J.ws_words)));
+  d_reps.resize(static_cast<std::size_t>(std::max<int64_t>(1, J.nreps)));
+  if (J.log_words > 0) d_log.resize(static_cast<std::size_t>(J.log_words));
+  d_out.resize(J.units.size());
+  // longest units first: requests x decode length is a fair proxy
+  std::vector<int32_t> order(J.units.size());
+  std::iota(order.begin(), order.end(), 0);
+  std::vector<int64_t> work(J.units.size(), 0);
+  for (std::size_t u = 0; u < J.units.size(); ++u)
+    for (int32_t j = 0; j < J.units[u].n; ++j) work[u] += J.hot[J.units[u].req_off + j].decode;
+  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return work[a] > work[b]; });
+  d_launch.upload(order, s);
+
+  SimLaunch L{};
+  L.configs = d_cfg.ptr;
+  L.units = d_units.ptr;
+  L.order = d_launch.ptr;
+  L.nunits = static_cast<int64_t>(J.units.size());
+  L.ests = d_est.ptr;
+  L.hot = d_hot.ptr;
+  L.tm = d_tm.ptr;
+  L.ids = d_ids.ptr;
+  L.restarts = d_restarts.ptr;
+  L.emit_base = J.emissions > 0 ? d_emit_base.ptr : nullptr;
+  L.emissions = J.emissions > 0 ? d_emis.ptr : nullptr;
+  L.arr_order = J.any_order ? d_order.ptr : nullptr;
+  L.reps = d_reps.ptr;
+  L.ws = d_ws.ptr;
+  L.log = J.log_words > 0 ? d_log.ptr : nullptr;
+  L.out = d_out.ptr;
+  launch_simulate(L, s);
+
+  R.out.resize(J.units.size());
+  d_out.download(R.out.data(), R.out.size(), s);
+  R.reps.resize(static_cast<std::size_t>(J.nreps));
+  d_reps.download(R.reps.data(), R.reps.size(), s);
+  if (want_requests) {
+    R.tm.resize(J.tm.size());
+    d_tm.download(R.tm.data(), R.tm.size(), s);
+    R.restarts.resize(J.hot.size());
+    d_restarts.download(R.restarts.data(), R.restarts.size(), s);
+  }
+  if (J.emissions > 0) {
+    R.emissions.resize(static_cast<std::size_t>(J.emissions));
+    d_emis.download(R.emissions.data(), R.emissions.size(), s);
+  }
+  if (J.log_words > 0) {
+    R.log.resize(static_cast<std::size_t>(J.log_words));
+    d_log.download(R.log.data(), R.log.size(), s);
+  }
+  cuda_check(cudaStreamSynchronize(s), "simulate");
+}
+
+[[noreturn]] void raise_unit_error(const SimUnitOut& o, const SimConfig& cfg,
+                                   const EstimatorModel& est) {
+  switch (o.code) {
+    case SSG_ERR_ENQUEUE:
+      throw Error("request " + std::to_string(o.err_i64[0]) + " needs " +
+                  std::to_string(o.err_i64[1]) + " KV units but replica capacity is " +
+                  std::to_string(cfg.total_units) + " (model/config cannot serve this request)");
+    case SSG_ERR_BBOX: {
+      const auto& de = est.device();
+      const SsgModelDesc& d = de.host_models.at(o.err_i32);
+      const OpModelKey key{static_cast<OpName>(d.op), d.tp};
+      throw Error(bbox_error_message(est.find(key.op, key.tp_degree), key,
+                                     static_cast<int>(o.err_i64[0]), o.err_f64));
+    }
+    case SSG_ERR_EXP_RANGE:
+      throw InternalError("predict: regressor output outside exp fast path");
+    default:
+      break;
+  }
+  static const char* kInternal[] = {"?",
+                                    "request not in waiting queue",
+                                    "predict_batch: non-positive prediction",
+                                    "non-positive iteration latency",
+                                    "prefill progressed past its target",
+                                    "sarathi: token budget exceeded",
+                                    "event time regression",
+                                    "simulation drained with unfinished request"};
+  const int k = (o.err_i32 >= 1 && o.err_i32 <= 7) ? o.err_i32 : 0;
+  std::string msg = kInternal[k];
+  if (k == 7) msg += " " + std::to_string(o.err_i64[0]);
+  throw InternalError(msg);
+}
+
+}  // namespace ssg
+
+namespace servesim {
+
+using namespace ssg;
+
+namespace {
+
+struct Placement {
+  SimJobs jobs;
+  std::vector<std::pair<int32_t, int32_t>> where;  // trace index -> (unit, local)
+  bool coupled = false;
+};
+
+// Units for one run_simulation call.  Round-robin replicas are independent
+// (each owns the arrivals at event positions r, r+R, ...) and become one unit
+// each; otherwise -- or when exact cross-replica event order matters -- all
+// replicas share one coupled unit.
+Placement place(const ClusterConfig& cluster, const std::vector<Request>& trace,
+                const EstimatorModel& estimator, const SimOptions& opts, bool coupled) {
+  Placement P;
+  P.coupled = coupled;
+  SimJobs& J = P.jobs;
+  J.configs.push_back(make_sim_config(cluster, estimator, 0));
+  J.ests.push_back(estimator.device().view);
+  const int R = static_cast<int>(cluster.par.num_replicas);
+  const std::size_t n = trace.size();
+  std::vector<int32_t> ev(n);
+  std::iota(ev.begin(), ev.end(), 0);
+  std::stable_sort(ev.begin(), ev.end(), [&](int32_t a, int32_t b) {
+    return trace[a].arrival_time < trace[b].arrival_time;
+  });
+  const bool want_log = opts.record_batches || opts.record_iterations;
+  UnitSpec us;
+  us.config = 0;
+  us.flags = SSG_UF_EMISSIONS | (want_log ? SSG_UF_BATCH_LOG : 0) |
+             (opts.abort_delay_threshold > 0.0 ? SSG_UF_ABORT : 0);
+  us.abort_thr = opts.abort_delay_threshold;
+  us.abort_max_late = static_cast<int32_t>(std::min<std::size_t>(opts.abort_max_late, INT32_MAX));
+  std::vector<std::vector<int32_t>> members;
+  if (!coupled) {
+    members.resize(R);
+    for (std::size_t p = 0; p < n; ++p) members[p % R].push_back(ev[p]);
+    us.R = 1;
+  } else {
+    require(R <= kMaxCoupledReplicas, "ssg: least_outstanding/deferred routing supports up to " +
+                                          std::to_string(kMaxCoupledReplicas) + " replicas");
+    members.push_back(ev);
+    us.R = R;
+  }
+  P.where.assign(n, {0, 0});
+  for (std::size_t u = 0; u < members.size(); ++u) {
+    const auto& m = members[u];
+    std::vector<int32_t> rank(m);
+    std::stable_sort(rank.begin(), rank.end(), [&](int32_t a, int32_t b) {
+      if (trace[a].arrival_time != trace[b].arrival_time)
+        return trace[a].arrival_time < trace[b].arrival_time;
+      return trace[a].id < trace[b].id;
+    });
+    std::vector<Request> reqs;
+    reqs.reserve(rank.size());
+    int64_t tokens = 0;
+    for (std::size_t k = 0; k < rank.size(); ++k) {
+      P.where[rank[k]] = {static_cast<int32_t>(u), static_cast<int32_t>(k)};
+      reqs.push_back(trace[rank[k]]);
+      tokens += trace[rank[k]].prefill_tokens + trace[rank[k]].decode_tokens;
+    }
+    std::vector<int32_t> order;
+    bool identity = true;
+    for (std::size_t k = 0; k < m.size(); ++k) {
+      order.push_back(P.where[m[k]].second);
+      if (order.back() != static_cast<int32_t>(k)) identity = false;
+    }
+    if (identity) order.clear();
+    UnitSpec s2 = us;
+    if (want_log) s2.log_cap = 1024 + 16 * tokens;
+    J.add_unit(s2, reqs, order);
+  }
+  return P;
+}
+
+}  // namespace
+
+SimulationOutput run_simulation_logged(const ClusterConfig& cluster,
+                                       const std::vector<Request>& trace,
+                                       const EstimatorModel& estimator, const SimOptions& opts) {
+  for (const auto& r : trace)
+    require(r.has_arrival(), "trace request " + std::to_string(r.id) +
+                                 " has no arrival time; assign arrivals before simulating");
+  const int R = static_cast<int>(cluster.par.num_replicas);
+  // probes with an abort bound need the global event order of late schedules
+  bool coupled = cluster.routing != RoutingPolicy::RoundRobin ||
+                 (opts.abort_delay_threshold > 0.0 && R > 1);
+  Placement P = place(cluster, trace, estimator, opts, coupled);
+  SimResults res;
+  run_jobs(P.jobs, res, true);
+  int errors = 0;
+  for (const auto& o : res.out) errors += o.code != SSG_OK;
+  if (errors > 1 && !coupled && R <= kMaxCoupledReplicas) {
+    // several independent replicas failed: replay coupled for the exact first one
+    P = place(cluster, trace, estimator, opts, true);
+    run_jobs(P.jobs, res, true);
+  }
+  const SimJobs& J = P.jobs;
+  const SimConfig& cfg = J.configs[0];
+  const SimUnitOut* first_err = nullptr;
+  bool aborted = false;
+  for (const auto& o : res.out) {
+    if (o.code != SSG_OK && (!first_err || o.err_time < first_err->err_time)) first_err = &o;
+    if (o.aborted) aborted = true;
+  }
+  if (first_err) raise_unit_error(*first_err, cfg, estimator);
+  if (aborted) throw ProbeInfeasible();
+
+  const std::size_t n = trace.size();
+  const bool want_log = opts.record_batches || opts.record_iterations;
+  SimulationOutput out;
+  SimulationResult& r = out.result;
+  r.num_devices = cluster.gpus_used();
+  r.peak_device_flops = cluster.dev.peak_flops;
+  r.replicas.resize(R);
+  double span = 0.0, flops = 0.0;
+  for (std::size_t u = 0; u < J.units.size(); ++u) {
+    span = std::max(span, res.out[u].span);
+    flops += res.out[u].flops;
+  }
+  r.simulated_span = span;
+  r.total_model_flops = flops;
+  for (int rep = 0; rep < R; ++rep) {
+    const RepState& s = !P.coupled ? res.reps[J.units[rep].rep_off] : res.reps[J.units[0].rep_off + rep];
+    ReplicaAggregate& a = r.replicas[rep];
+    a.busy_time = s.busy_time;
+    a.iterations = s.iterations;
+    a.tokens_processed = s.tokens;
+    a.peak_kv_utilization = s.peak_kv;
+    a.preemptions = static_cast<std::size_t>(s.preemptions);
+  }
+  r.requests.resize(n);
+  for (std::size_t i = 0; i < n; ++i) {
+    const SimUnit& u = J.units[P.where[i].first];
+    const int64_t g = u.req_off + P.where[i].second;
+    RequestRecord& rec = r.requests[i];
+    rec.id = trace[i].id;
+    rec.arrival = trace[i].arrival_time;
+    rec.first_scheduled = res.tm[g].first_sched;
+    rec.first_token = res.tm[g].first_tok;
+    rec.completion = res.tm[g].completion;
+    rec.prefill_tokens = trace[i].prefill_tokens;
+    rec.decode_tokens = trace[i].decode_tokens;
+    rec.restarts = res.restarts[g];
+    const int64_t b = J.emit_base[g];
+    rec.emission_times.assign(res.emissions.begin() + b,
+                              res.emissions.begin() + b + trace[i].decode_tokens);
+  }
+  if (want_log) {
+    for (std::size_t u = 0; u < J.units.size(); ++u) {
+      const SimUnit& su = J.units[u];
+      const int64_t used = res.out[u].log_used;
+      internal_check(used >= 0, "batch log overflow");
+      for (int64_t p = 0; p < used;) {
+        const int64_t* L = res.log.data() + su.log_off + p;
+        BatchLog b;
+        b.replica = !P.coupled ? u : static_cast<std::size_t>(L[0]);
+        b.now = __builtin_bit_cast(double, L[1]);
+        b.kv_allocated_units = L[2];
+        const int64_t np = L[3], nd = L[4];
+        const double lat = __builtin_bit_cast(double, L[5]);
+        for (int64_t k = 0; k < np; ++k)
+          b.entries.push_back(BatchEntryLog{true, L[6 + 3 * k], L[7 + 3 * k], L[8 + 3 * k]});
+        for (int64_t k = 0; k < nd; ++k)
+          b.entries.push_back(BatchEntryLog{false, L[6 + 3 * np + 2 * k], 1, L[7 + 3 * np + 2 * k]});
+        if (opts.record_iterations) {
+          IterationRecord it;
+          it.start = b.now;
+          it.latency = lat;
+          it.replica = b.replica;
+          it.batch_requests = np + nd;
+          int64_t tok = nd;
+          for (int64_t k = 0; k < np; ++k) tok += L[7 + 3 * k];
+          it.current_tokens = tok;
+          it.prefill_entries = np;
+          it.decode_entries = nd;
+          it.kv_utilization =
+              static_cast<double>(b.kv_allocated_units) / static_cast<double>(cfg.total_units);
+          r.iterations.push_back(it);
+        }
+        if (opts.record_batches) out.batches.push_back(std::move(b));
+        p += 6 + 3 * np + 2 * nd;
+      }
+    }
+    std::stable_sort(r.iterations.begin(), r.iterations.end(), [](const auto& a, const auto& b) {
+      return a.start != b.start ? a.start < b.start : a.replica < b.replica;
+    });
+  }
+  return out;
+}
+
+SimulationResult run_simulation(const ClusterConfig& cluster, const std::vector<Request>& trace,
+                                const EstimatorModel& estimator, const SimOptions& opts) {
+  return run_simulation_logged(cluster, trace, estimator, opts).result;
+}
+
+}  // namespace servesim

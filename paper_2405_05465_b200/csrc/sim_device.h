@@ -1,0 +1,118 @@
+// sim_device.h -- POD layouts of the replica-simulation engine (engine.cu).
+//
+// A "unit" is what one warp simulates: R_u replicas of one cluster config over
+// a request stream.  Round-robin clusters are split into R independent
+// single-replica units (replica r owns arrivals r, r+R, ... -- the reference's
+// RR router hands them out in exactly that order, scheduler.hpp:506-510);
+// least-outstanding / deferred routing couple replicas and run as one unit.
+#pragma once
+#include <stdint.h>
+
+// SchedulerPolicy order (scheduler.hpp:20)
+#define SSG_POL_FT 0
+#define SSG_POL_ORCA 1
+#define SSG_POL_VLLM 2
+#define SSG_POL_SARATHI 3
+#define SSG_POL_LIGHTLLM 4
+// RoutingPolicy order (scheduler.hpp:21)
+#define SSG_ROUTE_RR 0
+#define SSG_ROUTE_LO 1
+#define SSG_ROUTE_DEFERRED 2
+// OpClass order (model_spec.hpp:49)
+#define SSG_CLS_TOKEN 0
+#define SSG_CLS_SEQ 1
+#define SSG_CLS_COMM 2
+
+#define SSG_MAX_OPS 11
+#define SSG_MAX_PP 8
+
+// Unit flags
+#define SSG_UF_EMISSIONS 1  // write per-token emission times (CSR)
+#define SSG_UF_BATCH_LOG 2  // record every scheduled batch (SimObserver payload)
+#define SSG_UF_ABORT 4      // capacity probe: stop once late schedules exceed the bound
+
+// One operator of the per-stage operator set, with everything predict_batch /
+// batch_device_flops need (estimator.hpp:294-380, op_cost.hpp:21-73).
+struct SimOp {
+  int32_t slot;   // estimator model slot
+  int32_t cls;    // SSG_CLS_*
+  int32_t op;     // OpName
+  int32_t flop_kind;  // 0 matmul, 1 act_fn, 2 add_norm, 3 attn prefill, 4 attn decode, 5 none
+  double count;   // double(d.count)
+  double kvb;     // 2.0 * e * double(kv_heads_per_device * head_dim)
+  double payload; // double(payload_bytes_per_token)
+  double fa, fb;  // flop operands: matmul in/out, act/add_norm in, attention hq
+};
+
+struct SimConfig {
+  int32_t policy, max_batch, max_tokens, chunk;
+  int32_t token_granular, pp, tp, est;
+  int64_t block_size;
+  int64_t total_units, watermark_units;
+  double cpu_overhead;
+  int32_t nops, routing, defer_threshold, pad;
+  SimOp ops[SSG_MAX_OPS];
+};
+
+// Per-request hot state (32 B, one sector).  Indices are unit-local and
+// ordered by (arrival, id), so "sorted by arrival then id" (scheduler.hpp:236)
+// is plain integer order on the device.
+struct __attribute__((aligned(16))) ReqHot {
+  int32_t target;   // prefill_target
+  int32_t done;     // prefill_done
+  int32_t emitted;
+  int32_t kv;       // kv_context
+  int32_t held;     // KV units held (BlockManager::held_)
+  int32_t planned;  // schedule serial that last planned it (planned_ set)
+  int32_t decode;   // req.decode_tokens
+  int32_t prefill;  // req.prefill_tokens
+};
+
+struct __attribute__((aligned(16))) ReqTimes {
+  double arrival, first_sched, first_tok, completion;
+};
+
+struct SimUnit {
+  int32_t config;
+  int32_t n;          // requests in this unit
+  int32_t R;          // replicas simulated together
+  int32_t flags;
+  int64_t req_off;    // into the request arena (ReqHot/ReqTimes/ids/...)
+  int64_t ws_off;     // into the int32 workspace
+  int64_t rep_off;    // into the RepState / RepOut arrays
+  int32_t wait_cap;   // ring capacity, power of two > n
+  int32_t abort_max_late;
+  double abort_thr;
+  int64_t log_off;    // into the batch-log arena (int64 words)
+  int64_t log_cap;
+  int32_t group;      // late-schedule counter shared by the units of one probe
+  int32_t pad;
+};
+
+struct RepState {
+  int32_t run_n, wait_head, wait_n, busy;
+  int32_t ft_inflight, np, nd, outstanding;
+  int64_t allocated;
+  int64_t preemptions;
+  double ev_time;
+  uint64_t ev_seq;
+  int32_t ev_kind;  // 0 none, 1 BatchStart, 2 BatchComplete
+  int32_t pad;
+  double busy_time;
+  int64_t iterations, tokens;
+  double peak_kv;
+};
+
+struct SimUnitOut {
+  int32_t code;       // SSG_OK / SSG_ERR_*
+  int32_t aborted;    // probe stopped: late schedules exceeded the bound
+  int32_t late;       // late first-schedules counted (probe units)
+  int32_t err_i32;    // error operand: op slot / replica
+  int64_t err_i64[2]; // error operands: request id, needed units / feature index
+  double err_f64;     // error operand: feature value
+  double err_time;    // sim clock of the error
+  double span;        // clock of the last event
+  double flops;       // total_model_flops
+  int64_t log_used;   // batch-log words written
+  int64_t events;
+};

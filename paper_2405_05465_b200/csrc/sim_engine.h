@@ -1,0 +1,32 @@
+// sim_engine.h -- launch descriptor of the simulation kernel (host <-> device).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sim_device.h"
+#include "ssg_device.h"
+
+#define SSG_SIM_WARPS 2  // warps per block: units differ wildly in length, keep blocks small
+
+struct SimLaunch {
+  const SimConfig* configs;
+  const SimUnit* units;
+  const int32_t* order;  // unit launch order (longest first), may be null
+  int64_t nunits;
+  const SsgEstView* ests;
+  ReqHot* hot;
+  ReqTimes* tm;
+  const int64_t* ids;
+  int32_t* restarts;
+  const int64_t* emit_base;  // may be null
+  double* emissions;         // may be null
+  const int32_t* arr_order;  // may be null (identity)
+  RepState* reps;
+  int32_t* ws;
+  int64_t* log;              // may be null
+  SimUnitOut* out;
+};
+
+namespace ssg {
+void launch_simulate(const SimLaunch& L, cudaStream_t s);
+}

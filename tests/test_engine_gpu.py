@@ -1,0 +1,175 @@
+"""K3 parity: GPU replica simulation vs the compiled reference run_simulation.
+
+Checks, on identical inputs: every scheduled batch (replica, clock, KV units
+allocated, entries with chunk/prior/context) -- the reference SimObserver
+payload, sim.hpp:230 -- per-request records incl. every emission time,
+replica aggregates, span, and the metrics report.  Bit-exact except total
+model flops / MFU (summed across independent replicas in a different order;
+north_star tolerance 1e-6 relative).
+"""
+import json
+
+import numpy as np
+import pytest
+
+from paper_2405_05465_b200 import catalog
+
+pytestmark = pytest.mark.gpu
+
+_EST = {}
+
+
+def estimators(ssg, ref, model, dev, tps, reg="interp", seed=3):
+    key = (model, dev, tuple(tps), reg, seed)
+    if key not in _EST:
+        text = ref.train(catalog.MODELS[model], catalog.DEVICES[dev], tps, reg, seed)
+        _EST[key] = (ssg.Estimator.from_json(text), ref.Estimator(text))
+    return _EST[key]
+
+
+def trace_fixture(n, qps, seed, scale_decode=1.0):
+    lengths = catalog.fixture_chat_1k()
+    idx = np.arange(n) % len(lengths)
+    pre = lengths[idx, 0].astype(np.int64)
+    dec = np.maximum(1, (lengths[idx, 1] * scale_decode).astype(np.int64))
+    rng = np.random.default_rng(seed)
+    arr = np.cumsum(rng.exponential(1.0 / qps, n))
+    return np.arange(n, dtype=np.int64), arr, pre, dec
+
+
+def by_replica(batches):
+    out = {}
+    for b in batches:
+        out.setdefault(b["replica"], []).append(b)
+    return out
+
+
+def assert_same(mine, theirs, flops_rtol=1e-9):
+    assert "probe_infeasible" not in mine and "probe_infeasible" not in theirs
+    # batch logs, per replica in order
+    bm, bt = by_replica(mine["batches"]), by_replica(theirs["batches"])
+    assert sorted(bm) == sorted(bt)
+    for r in bt:
+        assert len(bm[r]) == len(bt[r]), ("batches", r)
+        for k, (a, b) in enumerate(zip(bm[r], bt[r])):
+            assert a["now"] == b["now"] and a["kv"] == b["kv"] and a["entries"] == b["entries"], (r, k, a, b)
+    for a, b in zip(mine["requests"], theirs["requests"]):
+        assert a == b, (a["id"], {k: (a[k], b[k]) for k in a if a[k] != b[k]})
+    assert mine["replicas"] == theirs["replicas"]
+    assert mine["simulated_span"] == theirs["simulated_span"]
+    assert mine["total_model_flops"] == pytest.approx(theirs["total_model_flops"], rel=flops_rtol)
+    rm, rt = mine["report"], theirs["report"]
+    for k in ("scheduling_delay", "ttft", "tbt", "e2e", "normalized"):
+        for q in ("p50", "p90", "p95", "p99"):
+            assert rm[k][q] == rt[k][q], (k, q)
+        assert rm[k]["mean"] == pytest.approx(rt[k]["mean"], rel=1e-12, abs=0)
+    for k in ("kv_utilization_peak", "busy_fraction", "preemptions"):
+        assert rm[k] == pytest.approx(rt[k], rel=1e-12), k
+    assert rm["mfu"] == pytest.approx(rt["mfu"], rel=flops_rtol)
+    assert mine["requests_csv"] == theirs["requests_csv"]
+
+
+def run_both(ssg, mine_est, ref_est, cluster, trace, **kw):
+    ids, arr, pre, dec = trace
+    mine = ssg.simulate(cluster, mine_est, ids, arr, pre, dec, record_batches=True, **kw)
+    theirs = ref_est.simulate(cluster, ids, arr, pre, dec, record_batches=True, **kw)
+    return mine, theirs
+
+
+@pytest.mark.parametrize("qps", [5.0, 10.0])
+def test_cfg1_vllm_7b(ssg, ref, qps):
+    """BASELINE cfg #1: LLaMA2-7B TP1, one replica, vLLM bs128, the 1K fixture."""
+    m, t = estimators(ssg, ref, "llama2_7b", "a100_80g", [1])
+    cluster = catalog.cluster_doc("llama2_7b", "a100_80g", policy="vllm", max_batch_size=128)
+    mine, theirs = run_both(ssg, m, t, cluster, trace_fixture(1000, qps, 5))
+    assert_same(mine, theirs)
+
+
+TIGHT = dict(catalog.DEVICES["a100_80g"], device_mem=30e9)
+
+
+@pytest.mark.parametrize("policy,extra", [
+    ("vllm", {}), ("orca_plus", {}), ("lightllm", {}),
+    ("sarathi_serve", {"chunk_size": 512}), ("faster_transformer", {}),
+])
+def test_policies_under_memory_pressure(ssg, ref, policy, extra):
+    """Acceptance #4 shape: a tight device forces watermark stalls and preemptions."""
+    m, t = estimators(ssg, ref, "llama2_7b", "a100_80g", [1])
+    cluster = catalog.cluster_doc("llama2_7b", TIGHT, policy=policy, max_batch_size=64, **extra)
+    mine, theirs = run_both(ssg, m, t, cluster, trace_fixture(600, 8.0, 11))
+    assert_same(mine, theirs)
+    if policy == "vllm":
+        assert theirs["report"]["preemptions"] > 0
+
+
+@pytest.mark.parametrize("routing,replicas", [("round_robin", 3), ("least_outstanding", 3),
+                                              ("deferred", 4)])
+def test_routing(ssg, ref, routing, replicas):
+    m, t = estimators(ssg, ref, "llama2_7b", "a100_80g", [1])
+    cluster = catalog.cluster_doc("llama2_7b", "a100_80g", replicas=replicas, routing=routing,
+                                  policy="vllm", max_batch_size=32)
+    mine, theirs = run_both(ssg, m, t, cluster, trace_fixture(900, 14.0, 2))
+    assert_same(mine, theirs)
+
+
+@pytest.mark.parametrize("tp,pp,policy", [(4, 1, "sarathi_serve"), (2, 2, "vllm"), (1, 4, "orca_plus")])
+def test_70b_parallelism(ssg, ref, tp, pp, policy):
+    """cfg #2 shape (70B, Sarathi cs512) plus pipeline microbatching."""
+    m, t = estimators(ssg, ref, "llama2_70b", "h100_80g", [1, 2, 4])
+    cluster = catalog.cluster_doc("llama2_70b", "h100_80g", tp=tp, pp=pp, policy=policy,
+                                  max_batch_size=128, chunk_size=512, cpu_overhead=1e-4)
+    mine, theirs = run_both(ssg, m, t, cluster, trace_fixture(700, 6.0, 4))
+    assert_same(mine, theirs)
+
+
+def test_forest_regressor_sim(ssg, ref):
+    m, t = estimators(ssg, ref, "llama2_7b", "a100_80g", [1], reg="forest")
+    cluster = catalog.cluster_doc("llama2_7b", "a100_80g", policy="sarathi_serve", chunk_size=1024)
+    mine, theirs = run_both(ssg, m, t, cluster, trace_fixture(400, 4.0, 8))
+    assert_same(mine, theirs)
+
+
+def test_probe_abort_matches(ssg, ref):
+    """SimOptions abort (sim.hpp:231-240): same verdict as the reference."""
+    m, t = estimators(ssg, ref, "llama2_7b", "a100_80g", [1])
+    cluster = catalog.cluster_doc("llama2_7b", "a100_80g", replicas=2, policy="vllm")
+    for qps, expect in [(60.0, True), (2.0, False)]:
+        mine, theirs = run_both(ssg, m, t, cluster, trace_fixture(500, qps, 1),
+                                abort_delay=5.0, abort_max_late=5)
+        assert bool(mine.get("probe_infeasible")) == bool(theirs.get("probe_infeasible")) == expect
+
+
+def test_enqueue_capacity_error(ssg, ref):
+    m, t = estimators(ssg, ref, "llama2_7b", "a100_80g", [1])
+    tiny = dict(catalog.DEVICES["a100_80g"], device_mem=15.2e9)
+    cluster = catalog.cluster_doc("llama2_7b", tiny, policy="vllm")
+    ids, arr, pre, dec = trace_fixture(50, 1.0, 0)
+    pre[7] = 9000  # > the 369 blocks x 16 tokens this device leaves for KV
+    with pytest.raises(ssg.InputError) as ei:
+        ssg.simulate(cluster, m, ids, arr, pre, dec)
+    from oracle.ref import RefError
+    with pytest.raises(RefError) as er:
+        t.simulate(cluster, ids, arr, pre, dec)
+    assert str(ei.value) == str(er.value)
+
+
+def test_predict_batch_parity(ssg, ref):
+    m, t = estimators(ssg, ref, "llama2_70b", "h100_80g", [1, 2, 4])
+    rng = np.random.default_rng(3)
+    batches = []
+    for _ in range(300):
+        npf = int(rng.integers(0, 5))
+        nd = int(rng.integers(0 if npf else 1, 200))
+        pl = rng.integers(1, 1024, npf).tolist()
+        pp = rng.integers(0, 3000, npf).tolist()
+        dc = rng.integers(1, 4096, nd).tolist()
+        batches.append((pl, pp, dc))
+    batches.append(([3, 4], [0, 0], []))       # sqrt(3^2+4^2) = 5 (test_estimator.cpp:85-90)
+    batches.append(([100] * 4, [0] * 4, []))   # -> 200
+    spec = catalog.MODELS["llama2_70b"]
+    for tp in (1, 2, 4):
+        s_m, f_m = m.predict_batch(spec, tp, batches)
+        s_t, f_t, res = t.predict_batch(spec, tp, batches)
+        assert res == {}
+        assert np.array_equal(s_m.view(np.uint64), s_t.view(np.uint64))
+        assert np.array_equal(f_m.view(np.uint64), f_t.view(np.uint64))
