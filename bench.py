@@ -1,0 +1,417 @@
+#!/usr/bin/env python3
+"""Benchmark: the Vidur-Search sweep (BASELINE cfg #4) on B200, plus the
+predictor microbench (cfg #3), printed as ONE JSON line by rank 0.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl ssg|reference]
+
+* metric   simulated configs/sec of the LLaMA2-70B capacity sweep (450 configs:
+           {A100,H100} x tp,pp in {1,2,4} x {vLLM, Orca+, Sarathi-Serve} x bs x cs,
+           chat_like workload, 2000 probe requests, tol 0.02, interp estimator).
+* value    configs / device time of the sweep with the prepared session's inputs
+           resident in HBM (estimators, probe workload); CUDA events on the
+           library stream bracket each step, max over ranks.
+* e2e      the same metric through the reference-facing C ABI call
+           (ssg_search_shard from the search-config file: load, train, upload,
+           simulate, download) + the NCCL all-gather + finalize.
+* roofline k_simulate: algorithmic bytes (predictor bytes of
+           every query + 48 B per batch entry, counted by the kernel) / its
+           CUDA-event time, against the measured HBM copy bandwidth.
+* cpu_baseline  the compiled reference (oracle/_ref) evaluating a bounded sample
+           of the same configs on all host threads (rank 0, N=1 only).
+Multi-GPU: configs i % N == rank per rank (strong scaling of the fixed grid),
+one NCCL all_gather of fixed-size result records, ranking/Pareto on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "simulated configs/sec (Vidur-Search sweep)"
+UNIT = "configs/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ssg", choices=["ssg", "reference"])
+    ap.add_argument("--predictor-queries", type=int, default=10_000_000)
+    ap.add_argument("--cpu-sample", type=int, default=0, help="configs in the CPU baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="small grid (smoke of the bench itself)")
+    return ap.parse_args()
+
+
+def search_config(directory: str, quick: bool) -> str:
+    from paper_2405_05465_b200 import catalog
+
+    if quick:
+        return catalog.write_search_config(directory, model="llama2_70b", tp=(4,), pp=(1,),
+                                           batch_sizes=(64, 256), chunk_sizes=(512,),
+                                           probe_requests=500, num_requests=500)
+    return catalog.write_search_config(directory)  # cfg #4 defaults
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md recipe)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.Q,
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def flush_l2(torch, dev):
+    # 512 MB write: larger than the 126 MB L2, between timed steps
+    buf = getattr(flush_l2, "buf", None)
+    if buf is None:
+        buf = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device=dev)
+        flush_l2.buf = buf
+    buf.fill_(1.0)
+    torch.cuda.synchronize()
+
+
+def measured_peak():
+    try:
+        j = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(j["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def cpu_baseline(cfg_path: str, n_configs: int, sample: int) -> dict:
+    """The compiled reference evaluating a strided sample of the grid on all host threads."""
+    from oracle import ref
+
+    threads = os.cpu_count() or 1
+    k = sample or threads
+    stride = max(1, n_configs // k)
+    idx = list(range(0, n_configs, stride))[:k]
+    res = ref.evaluate_sample(cfg_path, idx, threads)
+    secs = res["seconds"]
+    return {"value": len(idx) / secs, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": "%d of %d configs (every %dth in enumeration order), evaluate_config on %d "
+                      "threads, %.1f s" % (len(idx), n_configs, stride, threads, secs)}
+
+
+def predictor_bench(torch, dev, nq: int, steps: int, warmup: int) -> dict:
+    """cfg #3: 10M forest queries (1/3 attn_prefill, attn_decode, mlp_up_proj) on the
+    LLaMA2-70B/H100 tp4 estimator, inputs resident in HBM; plus the e2e host-buffer call."""
+    import numpy as np
+
+    import paper_2405_05465_b200 as ssg
+    from paper_2405_05465_b200 import catalog
+
+    est = ssg.Estimator.train(catalog.MODELS["llama2_70b"], catalog.DEVICES["h100_80g"], [4],
+                              "forest", seed=3)
+    rng = np.random.default_rng(0)
+    ops = ("attn_prefill", "attn_decode", "mlp_up_proj")
+    which = rng.integers(0, 3, nq)
+    slots = np.array([est.slot(o, 4) for o in ops], dtype=np.int32)[which]
+    f0 = np.floor(4096.0 ** rng.random(nq))
+    f1 = np.floor((512.0 * 4096.0) ** rng.random(nq)) * 1024.0  # kv_bytes_per_token_per_block, 70B tp4
+    f1[which == 2] = 0.0
+    d_slots = torch.from_numpy(slots).to(dev)
+    d_f0 = torch.from_numpy(f0).to(dev)
+    d_f1 = torch.from_numpy(f1).to(dev)
+    d_out = torch.empty(nq, dtype=torch.float64, device=dev)
+    d_err = torch.full((1,), -1, dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    times = []
+    for i in range(warmup + steps):
+        flush_l2(torch, dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        est.predict_device(nq, d_slots.data_ptr(), 0, d_f0.data_ptr(), d_f1.data_ptr(),
+                           d_out.data_ptr(), d_err.data_ptr(), stream)
+        e1.record()
+        torch.cuda.synchronize()
+        if i >= warmup:
+            times.append(e0.elapsed_time(e1) / 1e3)
+    assert int(d_err.item()) == -1, "predictor error"
+    t = sum(times) / len(times)
+    # e2e: host (pinned) buffers through ssg_predict_mixed
+    hp = [torch.from_numpy(a).pin_memory() for a in (slots, f0, f1)]
+    out = torch.empty(nq, dtype=torch.float64).pin_memory()
+    e2e = []
+    for i in range(max(1, steps)):
+        t0 = time.perf_counter()
+        est.predict_mixed(hp[0].numpy(), hp[1].numpy(), hp[2].numpy(), out=out.numpy())
+        e2e.append(time.perf_counter() - t0)
+    # algorithmic bytes per query from the trained trees' mean depths
+    doc = json.loads(est.to_json())
+    qb = {}
+    for o in ops:
+        m = doc["ops"]["%s@tp4" % o]
+        nf = len(m["schema"])
+        b = 8 * nf + 8
+        for tr in m["regressor"]["trees"]:
+            feat, left, right = tr["feature"], tr["left"], tr["right"]
+            st, tot, leaves = [(0, 0)], 0, 0
+            while st:
+                node, d = st.pop()
+                if feat[node] >= 0:
+                    st += [(left[node], d + 1), (right[node], d + 1)]
+                else:
+                    tot, leaves = tot + d, leaves + 1
+            b += 20.0 * tot / leaves + 8 * (nf + 1)
+        qb[o] = b
+    mean_b = sum(qb[o] for o in ops) / 3.0
+    peak, kind = measured_peak()
+    achieved = mean_b * nq / t / 1e9
+    # CPU baseline sample of the same queries through the reference (all host threads)
+    base = None
+    try:
+        from oracle import ref
+
+        r = ref.Estimator(est.to_json())
+        threads = os.cpu_count() or 1
+        ns = min(nq, 2_000_000)
+        opi = np.array([ssg.OP_INDEX[o] for o in ops], dtype=np.int32)[which[:ns]]
+        _, secs = r.predict_timed(opi, np.full(ns, 4), f0[:ns], f1[:ns], threads)
+        base = {"value": ns / secs, "unit": "queries/s", "cores": threads, "kind": "reference",
+                "sample": "%d queries, EstimatorModel::predict on %d threads" % (ns, threads)}
+    except Exception as e:  # noqa: BLE001
+        base = {"unavailable": str(e)}
+    return {"workload": "cfg #3: %d forest queries, LLaMA2-70B H100 tp4, attn_prefill/attn_decode/"
+                        "mlp_up_proj mix" % nq,
+            "value": nq / t, "unit": "queries/s", "ms_per_step": t * 1e3,
+            "e2e": {"value": nq / min(e2e), "unit": "queries/s",
+                    "h2d_bytes_per_step": nq * (4 + 8 + 8), "d2h_bytes_per_step": nq * 8},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_kind": kind,
+                         "bytes_per_query": mean_b},
+            "cpu_baseline": base}
+
+
+def main():
+    a = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        return reference_arm(a, world, rank)
+    import torch
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2405_05465_b200 as ssg
+
+    ssg.init(local)
+    tmp = tempfile.mkdtemp(prefix="ssg_bench_")
+    cfg_path = search_config(tmp, a.quick)
+    session = ssg.SearchSession(cfg_path)  # untimed setup: load, train, upload
+    n_configs = session.num_configs
+    rec_size = ssg.record_size()
+    per_rank = -(-n_configs // world)
+
+    def gather(records: bytes) -> bytes:
+        if world == 1:
+            return records
+        buf = torch.zeros(per_rank * rec_size, dtype=torch.uint8, device=dev)
+        if records:
+            buf[: len(records)] = torch.frombuffer(bytearray(records), dtype=torch.uint8).to(dev)
+        out = torch.empty(world * per_rank * rec_size, dtype=torch.uint8, device=dev)
+        dist.all_gather_into_tensor(out, buf)  # one NCCL all-gather over NVLink
+        host = out.cpu().numpy().tobytes()
+        parts = []
+        for r in range(world):
+            n_r = len(range(r, n_configs, world))
+            base = r * per_rank * rec_size
+            parts.append(host[base: base + n_r * rec_size])
+        return b"".join(parts)
+
+    def step(e2e: bool):
+        if e2e:
+            recs = ssg.search_shard(cfg_path, rank, world)
+        else:
+            recs = session.run(rank, world)
+        allrecs = gather(recs)
+        out = ssg.search_finalize(cfg_path, allrecs) if rank == 0 else None
+        return out
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(e2e: bool, steps: int):
+        times, out = [], None
+        for _ in range(steps):
+            flush_l2(torch, dev)
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            out = step(e2e)
+            e1.record()
+            barrier()
+            t = e0.elapsed_time(e1) / 1e3
+            if dist is not None:
+                tt = torch.tensor([t], dtype=torch.float64, device=dev)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                t = float(tt.item())
+            times.append(t)
+        return times, out
+
+    for _ in range(a.warmup):
+        step(False)
+    clocks = Clocks(local)
+    clocks.start()
+    ssg.stats_reset()
+    times, outcome = timed(False, a.steps)
+    st = ssg.stats()
+    clk = clocks.stop()
+    t_step = sum(times) / len(times)
+    # e2e through the C ABI from the config file (includes load/train/H2D/D2H)
+    ssg.stats_reset()
+    e2e_times, _ = timed(True, max(1, a.steps))
+    st_e2e = ssg.stats()
+    e2e_steps = max(1, a.steps)
+
+    peak, peak_kind = measured_peak()
+    sim_s = st["simulate_ms"] / 1e3
+    alg_bytes = st["predictor_bytes"] + st["entry_bytes"]
+    achieved = alg_bytes / sim_s / 1e9 if sim_s > 0 else 0.0
+    launches = (st["launches_simulate"] + st["launches_select"] + st["launches_predict"]
+                + st["launches_batch"])
+    result = {
+        "metric": METRIC, "value": n_configs / t_step, "unit": UNIT, "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": t_step * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (chat_like lognormal lengths, synth seed 7; Poisson probes seed 1)",
+        "config": {"workload": "cfg #4: LLaMA2-70B Vidur-Search capacity sweep, %d configs "
+                               "(A100/H100 x tp,pp in {1,2,4} x vLLM/Orca+/Sarathi x bs x cs), "
+                               "2000 probe requests, tol 0.02, interp estimator" % n_configs,
+                   "configs": n_configs, "parallelism": "config shards x%d + 1 NCCL all_gather" % world,
+                   "l2": "flushed (512 MB write) before every timed step"},
+        "e2e": {"value": n_configs / (sum(e2e_times) / len(e2e_times)), "unit": UNIT,
+                "h2d_bytes_per_step": st_e2e["h2d_bytes"] // e2e_steps,
+                "d2h_bytes_per_step": st_e2e["d2h_bytes"] // e2e_steps},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak if peak else None, "traffic": None,
+                     "kernel": "k_simulate", "peak_kind": peak_kind,
+                     "alg_bytes_per_step": alg_bytes / a.steps,
+                     "kernel_ms_per_step": st["simulate_ms"] / a.steps,
+                     "kernel_share_of_step": (st["simulate_ms"] / a.steps) / (t_step * 1e3)},
+        "gpu_launches": launches,
+        "work": {k: st[k] // a.steps for k in ("units", "iterations", "entries", "events")},
+        "clocks": clk,
+    }
+    if rank == 0 and outcome is not None:
+        result["optimum"] = outcome.get("best")
+    if rank == 0 and world == 1 and not a.quick:
+        try:
+            result["predictor"] = predictor_bench(torch, dev, a.predictor_queries, a.steps, a.warmup)
+        except Exception as e:  # noqa: BLE001
+            result["predictor"] = {"error": str(e)}
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        try:
+            result["cpu_baseline"] = cpu_baseline(cfg_path, n_configs, a.cpu_sample)
+        except Exception as e:  # noqa: BLE001
+            result["cpu_baseline"] = {"unavailable": str(e)}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    session.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def reference_arm(a, world: int, rank: int):
+    """--impl reference: the compiled reference (oracle/_ref) on the host cores, on
+    bounded samples of the same sweep (each step = a strided sample of configs)."""
+    if rank != 0:
+        return
+    try:
+        from oracle import ref
+
+        if not ref.available():
+            raise ImportError("oracle/_ref not built")
+        tmp = tempfile.mkdtemp(prefix="ssg_ref_")
+        cfg_path = search_config(tmp, a.quick)
+        threads = os.cpu_count() or 1
+        n_configs = int(ref.evaluate_sample(cfg_path, [], 1)["num_configs_total"])
+        k = a.cpu_sample or threads
+        times = []
+        for i in range(a.warmup + a.steps):
+            stride = max(1, n_configs // k)
+            idx = [(j + i) % n_configs for j in range(0, n_configs, stride)][:k]
+            res = ref.evaluate_sample(cfg_path, idx, threads)
+            if i >= a.warmup:
+                times.append((len(idx), res["seconds"]))
+        v = sum(n for n, _ in times) / sum(s for _, s in times)
+        print(json.dumps({
+            "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": 1e3 * sum(s for _, s in times) / len(times),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": "cfg #4 sample, %d configs/step" % k},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
+                             "sample": "%d strided configs per step, evaluate_config" % k},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+            flush=True)
+    except Exception as e:  # noqa: BLE001
+        print(json.dumps({"impl": "reference", "unavailable": str(e)[:200]}), flush=True)
+
+
+if __name__ == "__main__":
+    main()

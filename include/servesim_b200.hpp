@@ -476,6 +476,22 @@ std::vector<ConfigResult> evaluate_configs_shard(const ModelSpec& spec,
 SearchOutcome finalize_search(const ModelSpec& spec, const SearchOptions& opts,
                               std::vector<ConfigResult> results);
 
+// A prepared sweep: configs enumerated, estimators trained and resident in
+// HBM, probe workload and arrival exponentials built.  evaluate() is the hot
+// path (repeatable; what the bench times).
+class SearchSession {
+ public:
+  SearchSession(const ModelSpec& spec, const std::vector<Request>& workload,
+                const SearchOptions& opts);
+  ~SearchSession();
+  std::vector<ConfigResult> evaluate(int shard = 0, int num_shards = 1);
+  std::size_t num_configs() const;
+
+ private:
+  struct State;
+  std::unique_ptr<State> st_;
+};
+
 std::string search_results_to_csv(const SearchOutcome& outcome);
 std::string frontier_to_csv(const SearchOutcome& outcome, const std::vector<std::size_t>& frontier,
                             bool use_ttft);

@@ -134,6 +134,29 @@ int ssg_search_shard(const char* config_path, int shard, int num_shards, ssg_con
 int ssg_search_finalize(const char* config_path, const ssg_config_record* records, size_t n,
                         char** out, ssg_status* st);
 
+/* A prepared sweep (SearchSession): config loaded, estimators trained and
+ * resident in HBM, probe workload built.  ssg_search_run evaluates this
+ * shard's configs (the timed hot path) and may be called repeatedly. */
+typedef struct ssg_search_session ssg_search_session;
+int ssg_search_open(const char* config_path, ssg_search_session** out, ssg_status* st);
+int ssg_search_run(ssg_search_session* s, int shard, int num_shards, ssg_config_record* records,
+                   size_t capacity, size_t* count, ssg_status* st);
+int64_t ssg_search_num_configs(const ssg_search_session* s);
+void ssg_search_close(ssg_search_session* s);
+
+/* ---- counters over the library's kernels (bench / roofline evidence) ----- */
+typedef struct ssg_run_stats {
+  int64_t launches_simulate, launches_select, launches_predict, launches_batch;
+  int64_t units, iterations, entries, events;
+  int64_t predictor_bytes; /* algorithmic predictor bytes */
+  int64_t entry_bytes;     /* 48 B per batch entry (request progress r/w) */
+  int64_t queries;         /* k_predict queries */
+  double simulate_ms;      /* k_simulate device time (CUDA events, library stream) */
+  int64_t h2d_bytes, d2h_bytes; /* host<->device copies issued by the library */
+} ssg_run_stats;
+void ssg_stats_reset(void);
+void ssg_stats_get(ssg_run_stats* out);
+
 #ifdef __cplusplus
 }
 #endif

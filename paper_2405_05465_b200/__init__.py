@@ -174,3 +174,58 @@ def search_finalize(config_path: str, records: bytes) -> dict:
     buf = C.create_string_buffer(records, len(records))
     _ffi.call("ssg_search_finalize", config_path.encode(), buf, len(records) // size, C.byref(out))
     return json.loads(_ffi.take_text(out))
+
+
+class SearchSession:
+    """A prepared sweep (ssg_search_open): estimators resident in HBM; run() is the hot path."""
+
+    def __init__(self, config_path: str):
+        self._h = C.c_void_p()
+        self.path = config_path
+        _ffi.call("ssg_search_open", config_path.encode(), C.byref(self._h))
+        self.num_configs = _ffi.lib().ssg_search_num_configs(self._h)
+
+    def run(self, shard: int = 0, num_shards: int = 1) -> bytes:
+        size = record_size()
+        cap = self.num_configs
+        buf = (C.c_char * (cap * size))()
+        n = C.c_size_t()
+        _ffi.call("ssg_search_run", self._h, shard, num_shards, buf, cap, C.byref(n))
+        return bytes(buf[: n.value * size])
+
+    def close(self):
+        if self._h:
+            _ffi.lib().ssg_search_close(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def stats_reset() -> None:
+    _ffi.lib().ssg_stats_reset()
+
+
+def stats() -> dict:
+    s = _ffi.RunStats()
+    _ffi.lib().ssg_stats_get(C.byref(s))
+    return {name: getattr(s, name) for name, _ in s._fields_}
+
+
+def decode_records(records: bytes) -> list:
+    """Fixed-size ssg_config_record bytes -> dicts (for inspection / tests)."""
+    size = record_size()
+    out = []
+    for k in range(0, len(records), size):
+        r = records[k:k + size]
+        idx = int.from_bytes(r[0:8], "little", signed=True)
+        vals = np.frombuffer(r[8:56], dtype=np.float64)
+        slo = int.from_bytes(r[56:60], "little", signed=True)
+        err = r[64:].split(b"\0", 1)[0].decode()
+        out.append(dict(index=idx, capacity_qps=vals[0], qps_per_dollar=vals[1], ttft_p90=vals[2],
+                        tbt_p99=vals[3], delay_p99=vals[4], makespan=vals[5], slo_pass=bool(slo),
+                        error=err))
+    return out

@@ -77,6 +77,13 @@ _SIGNATURES = {
     "ssg_search_finalize": (C.c_int, [C.c_char_p, P, C.c_size_t, C.POINTER(C.c_void_p),
                                       C.POINTER(Status)]),
     "ssg_search_record_size": (C.c_size_t, []),
+    "ssg_search_open": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(Status)]),
+    "ssg_search_run": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_size_t,
+                                 C.POINTER(C.c_size_t), C.POINTER(Status)]),
+    "ssg_search_num_configs": (C.c_int64, [C.c_void_p]),
+    "ssg_search_close": (None, [C.c_void_p]),
+    "ssg_stats_reset": (None, []),
+    "ssg_stats_get": (None, [C.c_void_p]),
 }
 
 
@@ -98,6 +105,13 @@ def lib():
         fn.argtypes = args
     _lib = L
     return L
+
+
+class RunStats(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in (
+        "launches_simulate", "launches_select", "launches_predict", "launches_batch", "units",
+        "iterations", "entries", "events", "predictor_bytes", "entry_bytes", "queries")] + [
+        ("simulate_ms", C.c_double), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64)]
 
 
 def exported_symbols():

@@ -264,6 +264,8 @@ __device__ bool batch_start(Unit& U, RepState& S, int r) {
   S.busy_time = __dadd_rn(S.busy_time, lat);
   S.iterations += 1;
   S.tokens += tokens;
+  U.iters += 1;
+  U.entries += S.np + S.nd;
   const double util = (double)S.allocated / (double)c.total_units;
   S.peak_kv = S.peak_kv < util ? util : S.peak_kv;
   wput(U, &U.out->flops, __dadd_rn(U.out->flops, flops));
@@ -308,6 +310,9 @@ __device__ void run_unit(Unit& U) {
   U.clock = 0.0;
   U.seq = (uint64_t)u.n;
   U.serial = 0;
+  U.qbytes = 0;
+  U.iters = 0;
+  U.entries = 0;
   int32_t next_arrival = 0;
   int32_t rr_next = 0;
   int64_t events = 0;
@@ -421,6 +426,9 @@ __device__ void run_unit(Unit& U) {
   if (U.lane == 0) {
     U.out->span = U.clock;
     U.out->events = events;
+    U.out->iterations = U.iters;
+    U.out->entries = U.entries;
+    U.out->qbytes = U.qbytes;
   }
   __syncwarp();
   if (!failed(U) && !U.out->aborted) {
@@ -499,6 +507,7 @@ __global__ void __launch_bounds__(SSG_SIM_WARPS * 32)
   U.smem_part = part[wib];
   U.lane = threadIdx.x & 31;
   U.clock = 0.0;
+  U.qbytes = 0;
   if (U.lane == 0) {
     SimUnitOut o;
     memset(&o, 0, sizeof o);
@@ -588,6 +597,7 @@ void predict_batches(const servesim::EstimatorModel& est, const SimConfig& cfg_i
   ssgk::k_predict_batch<<<(unsigned)blocks, SSG_SIM_WARPS * 32, 0, s>>>(
       d_cfg.ptr, de.view, n, static_cast<int32_t>(MB), d_ws.ptr, d_npnd.ptr, d_sec.ptr, d_fl.ptr, d_out.ptr);
   cuda_check(cudaGetLastError(), "k_predict_batch launch");
+  stats().launches_batch += 1;
   std::vector<SimUnitOut> out(n);
   d_out.download(out.data(), n, s);
   d_sec.download(seconds, n, s);

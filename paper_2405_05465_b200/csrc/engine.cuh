@@ -50,6 +50,8 @@ struct Unit {
   int64_t rep_stride;  // int32 words per replica in ws
   int32_t MB, WC;
   int32_t serial;      // schedule_iteration counter (planned_ stamp)
+  int64_t qbytes;      // predictor bytes (accounting only)
+  int64_t iters, entries;
   double clock;
   uint64_t seq;
 };
@@ -537,6 +539,7 @@ __device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, doubl
   double* secs_part = U.smem_part;       // [pp]
   double* flop_part = U.smem_part + SSG_MAX_PP;
   double acc_s = 0.0, acc_f = 0.0;
+  int64_t qb = 0;
   int cur_m = 0;
   int err = SSG_OK, err_task = 0, err_feat = 0;
   double err_val = 0.0;
@@ -581,6 +584,7 @@ __device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, doubl
         }
       }
       if (active) {
+        qb += o.qbytes;
         code = ssg_predict_one(U.E, o.slot, v0, v1, &pred, &bad);
         pred = __dmul_rn(o.count, pred);
         fl = (o.cls == SSG_CLS_COMM) ? 0.0 : __dmul_rn(o.count, fl);
@@ -619,6 +623,9 @@ __device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, doubl
     secs_part[cur_m] = acc_s;
     flop_part[cur_m] = acc_f;
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) qb += __shfl_xor_sync(SSG_FULL, qb, o);
+  U.qbytes += qb;
   __syncwarp();
   if (err != SSG_OK) {
     const SimOp& o = c.ops[err_task % nops];

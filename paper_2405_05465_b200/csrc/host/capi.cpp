@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <memory>
 
 #include "json.hpp"
 #include "runtime.h"
@@ -323,12 +324,9 @@ int ssg_search(const char* config_path, int shard, int num_shards, char** out, s
   });
 }
 
-int ssg_search_shard(const char* config_path, int shard, int num_shards, ssg_config_record* records,
-                     size_t capacity, size_t* count, ssg_status* st) {
-  return guarded(st, [&] {
-    require(num_shards >= 1 && shard >= 0 && shard < num_shards, "ssg_search_shard: bad shard");
-    auto cfg = load_search_config(config_path);
-    auto results = evaluate_configs_shard(cfg.spec, cfg.workload, cfg.options, shard, num_shards);
+namespace {
+void to_records(const std::vector<ConfigResult>& results, int shard, int num_shards,
+                ssg_config_record* records, size_t capacity, size_t* count) {
     size_t k = 0;
     for (size_t i = 0; i < results.size(); ++i) {
       if (static_cast<int>(i % static_cast<size_t>(num_shards)) != shard) continue;
@@ -348,7 +346,64 @@ int ssg_search_shard(const char* config_path, int shard, int num_shards, ssg_con
       std::memcpy(rec.error, r.error.data(), r.error.size());
     }
     *count = k;
+}
+}  // namespace
+
+int ssg_search_shard(const char* config_path, int shard, int num_shards, ssg_config_record* records,
+                     size_t capacity, size_t* count, ssg_status* st) {
+  return guarded(st, [&] {
+    require(num_shards >= 1 && shard >= 0 && shard < num_shards, "ssg_search_shard: bad shard");
+    auto cfg = load_search_config(config_path);
+    auto results = evaluate_configs_shard(cfg.spec, cfg.workload, cfg.options, shard, num_shards);
+    to_records(results, shard, num_shards, records, capacity, count);
   });
+}
+
+struct ssg_search_session {
+  std::unique_ptr<SearchSession> session;
+};
+
+int ssg_search_open(const char* config_path, ssg_search_session** out, ssg_status* st) {
+  return guarded(st, [&] {
+    auto cfg = load_search_config(config_path);
+    auto* s = new ssg_search_session{std::make_unique<SearchSession>(cfg.spec, cfg.workload, cfg.options)};
+    *out = s;
+  });
+}
+
+int ssg_search_run(ssg_search_session* s, int shard, int num_shards, ssg_config_record* records,
+                   size_t capacity, size_t* count, ssg_status* st) {
+  return guarded(st, [&] {
+    require(num_shards >= 1 && shard >= 0 && shard < num_shards, "ssg_search_run: bad shard");
+    auto results = s->session->evaluate(shard, num_shards);
+    to_records(results, shard, num_shards, records, capacity, count);
+  });
+}
+
+int64_t ssg_search_num_configs(const ssg_search_session* s) {
+  return static_cast<int64_t>(s->session->num_configs());
+}
+
+void ssg_search_close(ssg_search_session* s) { delete s; }
+
+void ssg_stats_reset(void) { ssg::stats() = ssg::RunStats{}; }
+
+void ssg_stats_get(ssg_run_stats* out) {
+  const ssg::RunStats& r = ssg::stats();
+  out->launches_simulate = r.launches_simulate;
+  out->launches_select = r.launches_select;
+  out->launches_predict = r.launches_predict;
+  out->launches_batch = r.launches_batch;
+  out->units = r.units;
+  out->iterations = r.iterations;
+  out->entries = r.entries;
+  out->events = r.events;
+  out->predictor_bytes = r.predictor_bytes;
+  out->entry_bytes = r.entry_bytes;
+  out->queries = r.queries;
+  out->simulate_ms = r.simulate_ms;
+  out->h2d_bytes = r.h2d_bytes;
+  out->d2h_bytes = r.d2h_bytes;
 }
 
 int ssg_search_finalize(const char* config_path, const ssg_config_record* records, size_t n,

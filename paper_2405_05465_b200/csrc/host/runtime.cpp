@@ -11,6 +11,7 @@ namespace ssg {
 
 namespace {
 Context g_ctx;
+RunStats g_stats;
 std::mutex g_mu;
 }  // namespace
 
@@ -51,6 +52,8 @@ int probe_host_math_variant() {
       "host libm exp/log1p match neither glibc contraction variant; device predictions "
       "cannot be made bit-identical to this host");
 }
+
+RunStats& stats() { return g_stats; }
 
 void init_context(int device) {
   std::lock_guard<std::mutex> lk(g_mu);

@@ -540,33 +540,61 @@ void run_measurements(std::vector<Candidate>& cands, const std::vector<std::size
 
 }  // namespace
 
-std::vector<ConfigResult> evaluate_configs_shard(const ModelSpec& spec,
-                                                 const std::vector<Request>& workload,
-                                                 const SearchOptions& opts, int shard,
-                                                 int num_shards) {
+struct SearchSession::State {
+  ModelSpec spec;
+  SearchOptions opts;
+  std::vector<CandidateConfig> configs;
+  std::vector<EstimatorModel> ests;
+  Workload w;
+};
+
+SearchSession::SearchSession(const ModelSpec& spec, const std::vector<Request>& workload,
+                             const SearchOptions& opts)
+    : st_(std::make_unique<State>()) {
+  State& S = *st_;
+  S.spec = spec;
+  S.opts = opts;
   PolicyConfig base;
-  auto configs = enumerate_configs(spec, opts.space, base);
-  require(!configs.empty(), "search: empty configuration space");
+  S.configs = enumerate_configs(spec, opts.space, base);
+  require(!S.configs.empty(), "search: empty configuration space");
   // one shared estimator per SKU over every valid tp (search.hpp:248-260)
   std::vector<std::int64_t> tps;
   for (auto tp : opts.space.tp_degrees)
     if (spec.num_kv_heads % tp == 0) tps.push_back(tp);
   require(!tps.empty(), "search: no valid tp degree for this model");
-  std::vector<EstimatorModel> ests;
   for (const auto& sku : opts.space.skus)
-    ests.push_back(train(generate_synthetic_profile(spec, sku, tps), opts.train));
-
-  std::vector<ConfigResult> results(configs.size());
-  std::vector<Candidate> cands;
-  Workload w;
+    S.ests.push_back(train(generate_synthetic_profile(spec, sku, tps), opts.train));
+  for (const auto& e : S.ests) e.device();  // resident in HBM before any timed work
   require(!workload.empty(), "search: empty workload");
   for (std::size_t i = 0; i < opts.capacity.probe_requests; ++i) {
     Request r = workload[i % workload.size()];
     r.id = static_cast<std::int64_t>(i);
-    w.lengths.push_back(r);
+    S.w.lengths.push_back(r);
   }
-  w.unit_exp = unit_exponentials(w.lengths.size(), opts.capacity.seed);
+  S.w.unit_exp = unit_exponentials(S.w.lengths.size(), opts.capacity.seed);
+}
 
+SearchSession::~SearchSession() = default;
+
+std::size_t SearchSession::num_configs() const { return st_->configs.size(); }
+
+std::vector<ConfigResult> evaluate_configs_shard(const ModelSpec& spec,
+                                                 const std::vector<Request>& workload,
+                                                 const SearchOptions& opts, int shard,
+                                                 int num_shards) {
+  SearchSession session(spec, workload, opts);
+  return session.evaluate(shard, num_shards);
+}
+
+std::vector<ConfigResult> SearchSession::evaluate(int shard, int num_shards) {
+  const State& S = *st_;
+  const ModelSpec& spec = S.spec;
+  const SearchOptions& opts = S.opts;
+  const auto& configs = S.configs;
+  const auto& ests = S.ests;
+  const Workload& w = S.w;
+  std::vector<ConfigResult> results(configs.size());
+  std::vector<Candidate> cands;
   for (std::size_t i = 0; i < configs.size(); ++i) {
     if (static_cast<int>(i % static_cast<std::size_t>(num_shards)) != shard) continue;
     const CandidateConfig& cand = configs[i];

@@ -21,6 +21,7 @@ void fill_sim_ops(SimConfig& c, const std::vector<OperatorDescriptor>& ops, cons
     const auto& d = ops[i];
     SimOp& o = c.ops[i];
     o.slot = de.slot(d.op, d.tp_degree);
+    o.qbytes = o.slot >= 0 ? de.qbytes[o.slot] : 0;
     o.cls = static_cast<int32_t>(d.op_class);
     o.op = static_cast<int32_t>(d.op);
     o.count = static_cast<double>(d.count);
@@ -207,7 +208,12 @@ void run_jobs(const SimJobs& J, SimResults& R, bool want_requests) {
   L.ws = d_ws.ptr;
   L.log = J.log_words > 0 ? d_log.ptr : nullptr;
   L.out = d_out.ptr;
+  cudaEvent_t ev0, ev1;
+  cuda_check(cudaEventCreate(&ev0), "event");
+  cuda_check(cudaEventCreate(&ev1), "event");
+  cuda_check(cudaEventRecord(ev0, s), "event");
   launch_simulate(L, s);
+  cuda_check(cudaEventRecord(ev1, s), "event");
 
   R.out.resize(J.units.size());
   d_out.download(R.out.data(), R.out.size(), s);
@@ -228,6 +234,21 @@ void run_jobs(const SimJobs& J, SimResults& R, bool want_requests) {
     d_log.download(R.log.data(), R.log.size(), s);
   }
   cuda_check(cudaStreamSynchronize(s), "simulate");
+  float ms = 0.f;
+  cuda_check(cudaEventElapsedTime(&ms, ev0, ev1), "event");
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  RunStats& st = stats();
+  st.launches_simulate += 1;
+  st.simulate_ms += ms;
+  st.units += static_cast<int64_t>(R.out.size());
+  for (const auto& o : R.out) {
+    st.iterations += o.iterations;
+    st.entries += o.entries;
+    st.events += o.events;
+    st.predictor_bytes += o.qbytes;
+    st.entry_bytes += 48 * o.entries;  // request progress read 32 B + write 16 B per entry
+  }
 }
 
 [[noreturn]] void raise_unit_error(const SimUnitOut& o, const SimConfig& cfg,

@@ -14,6 +14,7 @@
 // reference: estimator.hpp:105-131 (predict/find), regressor.hpp:103-108,
 //            256-264, 308-341
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 
 #include "predictor.cuh"
@@ -149,6 +150,35 @@ const DeviceEstimator& EstimatorModel::device() const {
       desc.y_hi = r.y_hi;
       for (const auto& t : r.trees) roots.push_back(append_tree(t, r.num_features, nodes));
     }
+    // algorithmic bytes per query: features + output, plus
+    // interp: 2^nf corner values + binary-search probes per axis;
+    // forest: per tree, visited nodes x 20 B + the leaf plane
+    int64_t qb = 8 * desc.nf + 8;
+    if (desc.kind == SSG_KIND_INTERP) {
+      qb += 8 * (int64_t(1) << desc.nf);
+      for (int f = 0; f < desc.nf; ++f)
+        qb += 8 * static_cast<int64_t>(std::ceil(std::log2(std::max(1, desc.axis_len[f]))));
+    } else {
+      for (const auto& t : r.trees) {
+        // mean internal-node depth of the tree's leaves
+        std::vector<std::pair<int, int>> st{{0, 0}};
+        double sum = 0.0;
+        int leaves = 0;
+        while (!st.empty()) {
+          auto [node, depth] = st.back();
+          st.pop_back();
+          if (t.feature[node] >= 0) {
+            st.push_back({t.left[node], depth + 1});
+            st.push_back({t.right[node], depth + 1});
+          } else {
+            sum += depth;
+            ++leaves;
+          }
+        }
+        qb += static_cast<int64_t>(std::llround(20.0 * sum / std::max(1, leaves))) + 8 * (desc.nf + 1);
+      }
+    }
+    d->qbytes.push_back(qb);
     d->index[key] = static_cast<int32_t>(d->host_models.size());
     d->host_models.push_back(desc);
   }
@@ -194,6 +224,8 @@ void launch_predict(const DeviceEstimator& de, int64_t n, const int32_t* slots, 
   k_predict<<<static_cast<unsigned>(blocks), threads, 0, s>>>(de.view, n, slots, uniform, f0, f1,
                                                               out, first_error);
   cuda_check(cudaGetLastError(), "k_predict launch");
+  stats().launches_predict += 1;
+  stats().queries += n;
 }
 
 // Turns the packed first-error word into the reference's exception.

@@ -34,8 +34,23 @@ Context& context();
 void init_context(int device);
 void shutdown_context();
 
+
+
 // Which glibc contraction this host's libm runs (host_math.cpp).
 int probe_host_math_variant();
+
+// Counters over the library's own kernels (reset/read through the C ABI; the
+// bench reports them next to its timings).
+struct RunStats {
+  int64_t launches_simulate = 0, launches_select = 0, launches_predict = 0, launches_batch = 0;
+  int64_t units = 0, iterations = 0, entries = 0, events = 0;
+  int64_t predictor_bytes = 0, entry_bytes = 0;
+  double simulate_ms = 0.0;  // k_simulate device time, CUDA events on the launching stream
+  int64_t queries = 0;       // k_predict queries
+  double predict_ms = 0.0;
+  int64_t h2d_bytes = 0, d2h_bytes = 0;
+};
+RunStats& stats();
 
 // Owning HBM buffer.
 template <typename T>
@@ -76,10 +91,12 @@ struct DeviceBuffer {
   void upload(const T* src, std::size_t n, cudaStream_t s) {
     resize(n);
     if (n) cuda_check(cudaMemcpyAsync(ptr, src, n * sizeof(T), cudaMemcpyHostToDevice, s), "H2D");
+    stats().h2d_bytes += static_cast<int64_t>(n * sizeof(T));
   }
   void upload(const std::vector<T>& v, cudaStream_t s) { upload(v.data(), v.size(), s); }
   void download(T* dst, std::size_t n, cudaStream_t s) const {
     if (n) cuda_check(cudaMemcpyAsync(dst, ptr, n * sizeof(T), cudaMemcpyDeviceToHost, s), "D2H");
+    stats().d2h_bytes += static_cast<int64_t>(n * sizeof(T));
   }
 };
 
@@ -95,6 +112,7 @@ struct DeviceEstimator {
   ssg::DeviceBuffer<int32_t> roots;
   std::vector<SsgModelDesc> host_models;
   std::map<OpModelKey, int32_t> index;  // (op, tp) -> model slot
+  std::vector<int64_t> qbytes;          // algorithmic bytes of one query per slot
   SsgEstView view{};
   std::size_t bytes = 0;  // HBM footprint
 

@@ -86,6 +86,7 @@ void launch_select(const double* d_samples, const int64_t* d_seg_off, const Sele
   ssgk::k_select<<<(unsigned)ntasks, ssgk::kSelectThreads, 0, s>>>(d_samples, d_seg_off, d_tasks,
                                                                    ntasks, d_out);
   cuda_check(cudaGetLastError(), "k_select launch");
+  stats().launches_select += 1;
 }
 
 std::vector<double> device_percentiles(const std::vector<double>& samples,

@@ -42,6 +42,7 @@ struct SimOp {
   double kvb;     // 2.0 * e * double(kv_heads_per_device * head_dim)
   double payload; // double(payload_bytes_per_token)
   double fa, fb;  // flop operands: matmul in/out, act/add_norm in, attention hq
+  int64_t qbytes; // algorithmic bytes of one prediction of this op's model
 };
 
 struct SimConfig {
@@ -115,4 +116,7 @@ struct SimUnitOut {
   double flops;       // total_model_flops
   int64_t log_used;   // batch-log words written
   int64_t events;
+  int64_t iterations; // batches executed (all replicas of the unit)
+  int64_t entries;    // batch entries (prefill chunks + decodes)
+  int64_t qbytes;     // algorithmic predictor bytes touched
 };
