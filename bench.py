@@ -263,23 +263,11 @@ def main():
     session = ssg.SearchSession(cfg_path)  # untimed setup: load, train, upload
     n_configs = session.num_configs
     rec_size = ssg.record_size()
-    per_rank = -(-n_configs // world)
+
+    from paper_2405_05465_b200.shard import gather_records
 
     def gather(records: bytes) -> bytes:
-        if world == 1:
-            return records
-        buf = torch.zeros(per_rank * rec_size, dtype=torch.uint8, device=dev)
-        if records:
-            buf[: len(records)] = torch.frombuffer(bytearray(records), dtype=torch.uint8).to(dev)
-        out = torch.empty(world * per_rank * rec_size, dtype=torch.uint8, device=dev)
-        dist.all_gather_into_tensor(out, buf)  # one NCCL all-gather over NVLink
-        host = out.cpu().numpy().tobytes()
-        parts = []
-        for r in range(world):
-            n_r = len(range(r, n_configs, world))
-            base = r * per_rank * rec_size
-            parts.append(host[base: base + n_r * rec_size])
-        return b"".join(parts)
+        return gather_records(records, n_configs, rank, world, rec_size, device=dev)
 
     def step(e2e: bool):
         if e2e:
@@ -333,7 +321,7 @@ def main():
     alg_bytes = st["predictor_bytes"] + st["entry_bytes"]
     achieved = alg_bytes / sim_s / 1e9 if sim_s > 0 else 0.0
     launches = (st["launches_simulate"] + st["launches_select"] + st["launches_predict"]
-                + st["launches_batch"])
+                + st["launches_batch"] + st["launches_setup"])
     result = {
         "metric": METRIC, "value": n_configs / t_step, "unit": UNIT, "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": t_step * 1e3,

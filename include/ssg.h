@@ -153,6 +153,7 @@ typedef struct ssg_run_stats {
   int64_t queries;         /* k_predict queries */
   double simulate_ms;      /* k_simulate device time (CUDA events, library stream) */
   int64_t h2d_bytes, d2h_bytes; /* host<->device copies issued by the library */
+  int64_t launches_setup;  /* probe-stream setup and SLO sample kernels */
 } ssg_run_stats;
 void ssg_stats_reset(void);
 void ssg_stats_get(ssg_run_stats* out);

@@ -203,8 +203,11 @@ __device__ bool batch_start(Unit& U, RepState& S, int r) {
     S.ev_kind = 0;
     return true;
   }
-  int32_t tokens = S.nd;
-  for (int32_t k = 0; k < S.np; ++k) tokens += P_CHUNK(U, r)[k];
+  int32_t tokens = 0;
+  for (int32_t k = U.lane; k < S.np; k += 32) tokens += P_CHUNK(U, r)[k];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tokens += __shfl_xor_sync(SSG_FULL, tokens, o);
+  tokens += S.nd;
   if (c.policy == SSG_POL_SARATHI && tokens > c.chunk) {
     set_error(U, SSG_ERR_INTERNAL, 5, tokens, 0, 0.0);  // sarathi: token budget exceeded
     return false;
@@ -484,8 +487,9 @@ __global__ void __launch_bounds__(SSG_SIM_WARPS * 32)
 // estimator.hpp:294-380 API): one warp per composition, same device code path
 // as the engine's per-iteration latency.
 __global__ void __launch_bounds__(SSG_SIM_WARPS * 32)
-    k_predict_batch(const SimConfig* cfg, SsgEstView E, int64_t n, int32_t MB, int32_t* ws,
-                    const int32_t* np_nd, double* seconds, double* flops, SimUnitOut* out) {
+    k_predict_batch(const SimConfig* cfgs, const SsgEstView* ests, const int32_t* comp_cfg,
+                    int64_t n, int32_t MB, int32_t* ws, const int32_t* np_nd, double* seconds,
+                    double* flops, SimUnitOut* out) {
   __shared__ int64_t stats[SSG_SIM_WARPS][SSG_MAX_PP * 6];
   __shared__ double part[SSG_SIM_WARPS][4 * SSG_MAX_PP];
   const int wib = threadIdx.x >> 5;
@@ -496,8 +500,8 @@ __global__ void __launch_bounds__(SSG_SIM_WARPS * 32)
   memset(&dummy, 0, sizeof dummy);
   dummy.R = 1;
   U.u = &dummy;
-  U.cfg = cfg;
-  U.E = E;
+  U.cfg = cfgs + comp_cfg[c];
+  U.E = ests[U.cfg->est];
   U.MB = MB;
   U.WC = 2;
   U.rep_stride = 6LL * MB + 2;
@@ -540,18 +544,22 @@ void launch_simulate(const SimLaunch& L, cudaStream_t s) {
 
 namespace ssg {
 
-void predict_batches(const servesim::EstimatorModel& est, const SimConfig& cfg_in, int64_t n,
-                     const int64_t* p_off, const int64_t* p_len, const int64_t* p_prior,
-                     const int64_t* d_off, const int64_t* d_ctx, double* seconds, double* flops) {
+void predict_batches_multi(const std::vector<SimConfig>& cfgs_in, const std::vector<SsgEstView>& ests,
+                           const std::vector<int32_t>& comp_cfg, int64_t n, const int64_t* p_off,
+                           const int64_t* p_len, const int64_t* p_prior, const int64_t* d_off,
+                           const int64_t* d_ctx, double* seconds, double* flops,
+                           std::vector<SimUnitOut>& status) {
   using namespace servesim;
+  status.assign(static_cast<std::size_t>(std::max<int64_t>(n, 0)), SimUnitOut{});
   if (n <= 0) return;
   auto& ctx = context();
   cudaStream_t s = ctx.stream;
-  const auto& de = est.device();
-  SimConfig cfg = cfg_in;
-  cfg.pp = 1;
-  cfg.tp = 1;
-  cfg.cpu_overhead = 0.0;
+  std::vector<SimConfig> cfgs = cfgs_in;
+  for (auto& c : cfgs) {  // predict_batch on the whole composition: no microbatches, no tp scaling
+    c.pp = 1;
+    c.tp = 1;
+    c.cpu_overhead = 0.0;
+  }
   int64_t MB = 1;
   for (int64_t c = 0; c < n; ++c) {
     const int64_t np = p_off[c + 1] - p_off[c], nd = d_off[c + 1] - d_off[c];
@@ -584,10 +592,13 @@ void predict_batches(const servesim::EstimatorModel& est, const SimConfig& cfg_i
     }
   }
   DeviceBuffer<SimConfig> d_cfg;
-  DeviceBuffer<int32_t> d_ws, d_npnd;
+  DeviceBuffer<SsgEstView> d_est;
+  DeviceBuffer<int32_t> d_ws, d_npnd, d_cc;
   DeviceBuffer<double> d_sec, d_fl;
   DeviceBuffer<SimUnitOut> d_out;
-  d_cfg.upload(&cfg, 1, s);
+  d_cfg.upload(cfgs, s);
+  d_est.upload(ests, s);
+  d_cc.upload(comp_cfg, s);
   d_ws.upload(ws, s);
   d_npnd.upload(np_nd, s);
   d_sec.resize(n);
@@ -595,16 +606,26 @@ void predict_batches(const servesim::EstimatorModel& est, const SimConfig& cfg_i
   d_out.resize(n);
   const int64_t blocks = (n + SSG_SIM_WARPS - 1) / SSG_SIM_WARPS;
   ssgk::k_predict_batch<<<(unsigned)blocks, SSG_SIM_WARPS * 32, 0, s>>>(
-      d_cfg.ptr, de.view, n, static_cast<int32_t>(MB), d_ws.ptr, d_npnd.ptr, d_sec.ptr, d_fl.ptr, d_out.ptr);
+      d_cfg.ptr, d_est.ptr, d_cc.ptr, n, static_cast<int32_t>(MB), d_ws.ptr, d_npnd.ptr, d_sec.ptr,
+      d_fl.ptr, d_out.ptr);
   cuda_check(cudaGetLastError(), "k_predict_batch launch");
   stats().launches_batch += 1;
-  std::vector<SimUnitOut> out(n);
-  d_out.download(out.data(), n, s);
+  d_out.download(status.data(), n, s);
   d_sec.download(seconds, n, s);
   d_fl.download(flops, n, s);
   cuda_check(cudaStreamSynchronize(s), "predict_batch");
+}
+
+void predict_batches(const servesim::EstimatorModel& est, const SimConfig& cfg_in, int64_t n,
+                     const int64_t* p_off, const int64_t* p_len, const int64_t* p_prior,
+                     const int64_t* d_off, const int64_t* d_ctx, double* seconds, double* flops) {
+  SimConfig cfg = cfg_in;
+  cfg.est = 0;
+  std::vector<SimUnitOut> status;
+  predict_batches_multi({cfg}, {est.device().view}, std::vector<int32_t>(n, 0), n, p_off, p_len,
+                        p_prior, d_off, d_ctx, seconds, flops, status);
   for (int64_t c = 0; c < n; ++c)
-    if (out[c].code != SSG_OK) raise_unit_error(out[c], cfg, est);
+    if (status[c].code != SSG_OK) raise_unit_error(status[c], cfg, est);
 }
 
 }  // namespace ssg

@@ -420,21 +420,43 @@ __device__ void schedule_orca(Unit& U, RepState& S, int r) {
   schedule_decodes(U, S, r, c.max_batch, &budget);
 }
 
+// First position >= i of the running queue whose request matches `pred`
+// (warp-parallel 32-entry windows); run_n if none.
+#define PRED_PREFILL_LEFT 0
+__device__ int32_t next_running(Unit& U, const RepState& S, int r, int32_t i, int pred) {
+  const int32_t* a = RUN(U, r);
+  for (; i < S.run_n; i += 32) {
+    const int32_t p = i + U.lane;
+    bool hit = false;
+    if (p < S.run_n) {
+      const ReqHot h = U.hot[a[p]];
+      hit = !finished(h) && !prefill_complete(h);
+    }
+    const unsigned m = __ballot_sync(SSG_FULL, hit);
+    if (m) return i + __ffs(m) - 1;
+  }
+  return S.run_n;
+}
+
 __device__ void schedule_sarathi(Unit& U, RepState& S, int r) {
   const SimConfig& c = *U.cfg;
   int32_t budget = c.chunk;
   schedule_decodes(U, S, r, c.max_batch, &budget);
-  for (int32_t i = 0; i < S.run_n; ++i) {
+  // in-flight chunks in running order; a 32-entry window is scanned at once
+  // and only the requests with prefill left are visited one by one
+  for (int32_t i = 0; i < S.run_n;) {
     if (budget < 1 || S.np + S.nd >= c.max_batch) break;
-    const int32_t j = RUN(U, r)[i];
+    const int32_t k = next_running(U, S, r, i, PRED_PREFILL_LEFT);
+    if (k >= S.run_n) break;
+    const int32_t j = RUN(U, r)[k];
     const ReqHot h = U.hot[j];
-    if (finished(h) || prefill_complete(h)) continue;
     const int32_t rem = h.target - h.done;
     const int32_t chunk = budget < rem ? budget : rem;
     if (!admit_reserve(U, S, r, j, (int64_t)h.done + chunk, false, false)) break;
     mark_scheduled(U, j);
     push_prefill(U, S, r, j, chunk, h.done);
     budget -= chunk;
+    i = k + 1;
   }
   while (budget > 0 && S.wait_n > 0 && S.run_n < c.max_batch && S.np + S.nd < c.max_batch) {
     const int32_t head = wait_front(U, S, r);
@@ -466,25 +488,35 @@ __device__ void schedule_ft(Unit& U, RepState& S, int r) {
     if (S.run_n == 0) return;
     S.ft_inflight = 1;
   }
-  const int32_t* a = RUN(U, r);
-  for (int32_t i = 0; i < S.run_n; ++i) {
-    const int32_t j = a[i];
+  // prompts run one member per iteration ...
+  const int32_t k = next_running(U, S, r, 0, PRED_PREFILL_LEFT);
+  if (k < S.run_n) {
+    const int32_t j = RUN(U, r)[k];
     const ReqHot h = U.hot[j];
-    if (!finished(h) && !prefill_complete(h)) {
-      mark_scheduled(U, j);
-      push_prefill(U, S, r, j, h.target - h.done, h.done);
-      __syncwarp();
-      return;
-    }
-  }
-  for (int32_t i = 0; i < S.run_n; ++i) {
-    const int32_t j = a[i];
-    const ReqHot h = U.hot[j];
-    if (finished(h)) continue;
     mark_scheduled(U, j);
-    wput(U, &D_IDX(U, r)[S.nd], j);
-    wput(U, &D_CTX(U, r)[S.nd], h.kv + 1);
-    S.nd += 1;
+    push_prefill(U, S, r, j, h.target - h.done, h.done);
+    return;
+  }
+  // ... then every unfinished member decodes in lockstep (order = running order)
+  const int32_t* a = RUN(U, r);
+  for (int32_t base = 0; base < S.run_n; base += 32) {
+    const int32_t p = base + U.lane;
+    bool live = false;
+    int32_t j = -1;
+    if (p < S.run_n) {
+      j = a[p];
+      live = !finished(U.hot[j]);
+    }
+    const unsigned m = __ballot_sync(SSG_FULL, live);
+    if (live) {
+      const int32_t slot = S.nd + __popc(m & ((1u << U.lane) - 1u));
+      if (U.tm[j].first_sched < 0) U.tm[j].first_sched = U.clock;
+      U.hot[j].planned = U.serial;
+      D_IDX(U, r)[slot] = j;
+      D_CTX(U, r)[slot] = U.hot[j].kv + 1;
+    }
+    __syncwarp();
+    S.nd += __popc(m);
   }
 }
 

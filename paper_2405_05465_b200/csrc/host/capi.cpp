@@ -403,6 +403,7 @@ void ssg_stats_get(ssg_run_stats* out) {
   out->queries = r.queries;
   out->simulate_ms = r.simulate_ms;
   out->h2d_bytes = r.h2d_bytes;
+  out->launches_setup = r.launches_setup;
   out->d2h_bytes = r.d2h_bytes;
 }
 

@@ -24,6 +24,7 @@
 #include "select.h"
 #include "servesim_b200.hpp"
 #include "sim_host.h"
+#include "sweep.h"
 
 namespace servesim {
 
@@ -195,70 +196,199 @@ struct Workload {
   std::vector<double> unit_exp;  // E_i of the probe seed
 };
 
-// Arrivals of one probe: t += max(E_i / qps, 1e-12) (workload.hpp:96-103).
-void probe_arrivals(const Workload& w, double qps, std::vector<Request>& out) {
-  out = w.lengths;
-  double t = 0.0;
-  for (std::size_t i = 0; i < out.size(); ++i) {
-    t += std::max(w.unit_exp[i] / qps, 1e-12);
-    out[i].arrival_time = t;
-  }
-}
-
 struct Candidate {
   std::size_t index;  // enumeration index
   CandidateConfig cand;
   ClusterConfig cluster;
   const EstimatorModel* est = nullptr;
-  int32_t est_slot = 0;
   SimConfig sim{};
   bool sim_ok = false;  // make_sim_config succeeded (else the first probe raises)
   std::string sim_error;
-  int sim_error_kind = 0;  // 1 Error, 2 InternalError
-  double guess = 0;
   CapacitySearchOptions copts;
   std::unordered_map<double, bool> memo;
   bool done = false;
   ConfigResult res;
 };
 
-// One probe = one full arrival sequence at `qps` for one candidate.
-struct ProbeSlot {
-  std::size_t cand;
-  double qps;
-  int32_t first_unit, nunits;
-  bool coupled;
+// Persistent (grow-only) device buffers of the sweep's launches.
+struct SweepBuffers {
+  DeviceBuffer<SimConfig> cfg;
+  DeviceBuffer<SsgEstView> est;
+  DeviceBuffer<SimUnit> units;
+  DeviceBuffer<ProbeDesc> probes;
+  DeviceBuffer<int32_t> order, ws, restarts;
+  DeviceBuffer<ReqHot> hot;
+  DeviceBuffer<ReqTimes> tm;
+  DeviceBuffer<int64_t> ids, emit_base, seg_off;
+  DeviceBuffer<double> emis, samples, sel;
+  DeviceBuffer<RepState> reps;
+  DeviceBuffer<SimUnitOut> out;
+  DeviceBuffer<SelectTask> tasks;
 };
 
-// Adds a probe (or an SLO / static run) of candidate C to `jobs`.
-ProbeSlot add_probe(SimJobs& jobs, const Candidate& C, int32_t config_index,
-                    const std::vector<Request>& trace, int flags, double thr, int32_t max_late,
-                    bool coupled) {
-  ProbeSlot p{};
-  p.first_unit = static_cast<int32_t>(jobs.units.size());
-  const int R = static_cast<int>(C.cluster.par.num_replicas);
-  UnitSpec us;
-  us.config = config_index;
-  us.flags = flags;
-  us.abort_thr = thr;
-  us.abort_max_late = max_late;
-  // arrivals are strictly increasing and ids ascend with the trace index, so
-  // (arrival, id) order == trace order == arrival-event order
-  if (C.cluster.routing == RoutingPolicy::RoundRobin && !coupled) {
-    us.R = 1;
-    for (int r = 0; r < R; ++r) {
-      std::vector<Request> sub;
-      for (std::size_t i = r; i < trace.size(); i += R) sub.push_back(trace[i]);
-      jobs.add_unit(us, sub, {});
+// A launch under construction: per-candidate configs, probes and their units.
+struct ProbeLaunch {
+  std::vector<SimConfig> configs;
+  std::vector<SsgEstView> ests;
+  std::unordered_map<const EstimatorModel*, int32_t> est_index;
+  std::vector<SimUnit> units;
+  std::vector<ProbeDesc> probes;
+  std::vector<std::size_t> probe_cand;
+  int64_t nreq = 0, ws_words = 0, nreps = 0;
+
+  int32_t add_config(const Candidate& C) {
+    auto it = est_index.find(C.est);
+    if (it == est_index.end()) {
+      it = est_index.emplace(C.est, static_cast<int32_t>(ests.size())).first;
+      ests.push_back(C.est->device().view);
     }
-    p.nunits = R;
-  } else {
-    us.R = R;
-    jobs.add_unit(us, trace, {});
-    p.nunits = 1;
-    p.coupled = true;
+    SimConfig sc = C.sim;
+    sc.est = it->second;
+    configs.push_back(sc);
+    return static_cast<int32_t>(configs.size() - 1);
   }
-  return p;
+
+  // One probe of candidate `cand` (config `ci`): RR replicas become independent
+  // units (replica r owns trace positions r, r+R, ...), otherwise one coupled unit.
+  void add_probe(std::size_t cand, const Candidate& C, int32_t ci, double qps, int32_t n, int flags,
+                 double thr, int32_t max_late, bool coupled, bool static_run, int64_t emis_base) {
+    const SimConfig& cfg = configs[ci];
+    const int R = static_cast<int>(C.cluster.par.num_replicas);
+    ProbeDesc p{};
+    p.qps = qps;
+    p.R = R;
+    p.first_unit = static_cast<int32_t>(units.size());
+    p.decoupled = (C.cluster.routing == RoutingPolicy::RoundRobin && !coupled) ? 1 : 0;
+    p.static_run = static_run ? 1 : 0;
+    p.emis_base = emis_base;
+    const int nu = p.decoupled ? R : 1;
+    for (int r = 0; r < nu; ++r) {
+      SimUnit u{};
+      u.config = ci;
+      u.n = p.decoupled ? (n - r + R - 1) / R : n;
+      u.R = p.decoupled ? 1 : R;
+      u.flags = flags;
+      u.req_off = nreq;
+      nreq += u.n;
+      int64_t wc = 2;
+      while (wc <= u.n) wc <<= 1;
+      u.wait_cap = static_cast<int32_t>(wc);
+      u.ws_off = ws_words;
+      ws_words += static_cast<int64_t>(u.R) * (6LL * cfg.max_batch + wc) + wc + 2;
+      u.rep_off = nreps;
+      nreps += u.R;
+      u.abort_thr = thr;
+      u.abort_max_late = max_late;
+      units.push_back(u);
+    }
+    probes.push_back(p);
+    probe_cand.push_back(cand);
+  }
+};
+
+// Runs a launch entirely on the device: request streams built from the resident
+// workload, simulation, and (measure) the SLO samples + their percentiles.
+// Returns the per-unit outputs; `sel` gets delay p99, TTFT p90, TBT p99 per probe.
+void run_launch(SweepBuffers& B, ProbeLaunch& L, const ResidentWorkload& w, bool emissions,
+                bool measure, std::vector<SimUnitOut>& out, std::vector<double>& sel) {
+  auto& ctx = context();
+  cudaStream_t s = ctx.stream;
+  const int32_t np = static_cast<int32_t>(L.probes.size());
+  B.cfg.upload(L.configs, s);
+  B.est.upload(L.ests, s);
+  B.units.upload(L.units, s);
+  B.probes.upload(L.probes, s);
+  B.hot.resize(std::max<int64_t>(1, L.nreq));
+  B.tm.resize(std::max<int64_t>(1, L.nreq));
+  B.ids.resize(std::max<int64_t>(1, L.nreq));
+  B.restarts.resize(std::max<int64_t>(1, L.nreq));
+  B.ws.resize(std::max<int64_t>(1, L.ws_words));
+  B.reps.resize(std::max<int64_t>(1, L.nreps));
+  B.out.resize(std::max<std::size_t>(1, L.units.size()));
+  if (emissions) {
+    B.emit_base.resize(std::max<int64_t>(1, L.nreq));
+    B.emis.resize(std::max<int64_t>(1, w.emis_per_probe * np));
+  }
+  // longest units first (fewest replicas share the trace => most requests per unit)
+  std::vector<int32_t> order(L.units.size());
+  for (std::size_t u = 0; u < order.size(); ++u) order[u] = static_cast<int32_t>(u);
+  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+    if (L.units[a].n != L.units[b].n) return L.units[a].n > L.units[b].n;
+    return L.probes.empty() ? false : a < b;
+  });
+  B.order.upload(order, s);
+  launch_probe_setup(B.probes.ptr, np, B.units.ptr, w, B.hot.ptr, B.tm.ptr, B.ids.ptr,
+                     emissions ? B.emit_base.ptr : nullptr, s);
+  SimLaunch K{};
+  K.configs = B.cfg.ptr;
+  K.units = B.units.ptr;
+  K.order = B.order.ptr;
+  K.nunits = static_cast<int64_t>(L.units.size());
+  K.ests = B.est.ptr;
+  K.hot = B.hot.ptr;
+  K.tm = B.tm.ptr;
+  K.ids = B.ids.ptr;
+  K.restarts = B.restarts.ptr;
+  K.emit_base = emissions ? B.emit_base.ptr : nullptr;
+  K.emissions = emissions ? B.emis.ptr : nullptr;
+  K.arr_order = nullptr;
+  K.reps = B.reps.ptr;
+  K.ws = B.ws.ptr;
+  K.log = nullptr;
+  K.out = B.out.ptr;
+  cudaEvent_t e0, e1;
+  cuda_check(cudaEventCreate(&e0), "event");
+  cuda_check(cudaEventCreate(&e1), "event");
+  cuda_check(cudaEventRecord(e0, s), "event");
+  launch_simulate(K, s);
+  cuda_check(cudaEventRecord(e1, s), "event");
+  if (measure) {
+    // samples: [delay | ttft] per probe (n each) then TBT gaps (emis_per_probe each)
+    const int64_t n = w.n, E = w.emis_per_probe;
+    B.samples.resize(std::max<int64_t>(1, np * (2 * n + E)));
+    double* delay = B.samples.ptr;
+    double* ttft = delay + np * n;
+    double* gaps = ttft + np * n;
+    launch_slo_samples(B.probes.ptr, np, B.units.ptr, B.tm.ptr, w, B.emis.ptr, delay, ttft, gaps, s);
+    std::vector<int64_t> off;
+    std::vector<SelectTask> tasks;
+    for (int32_t k = 0; k < np; ++k) off.push_back(k * n);                // delay segments
+    for (int32_t k = 0; k < np; ++k) off.push_back(np * n + k * n);       // ttft segments
+    for (int32_t k = 0; k < np; ++k) off.push_back(2 * np * n + k * E);   // tbt segments
+    off.push_back(2 * np * n + np * E);
+    // contiguous segments: segment s spans [off[s], off[s+1])
+    const int64_t n_tbt = E - n;  // decode_tokens - 1 samples per request
+    for (int32_t k = 0; k < np; ++k) {
+      tasks.push_back({k, nearest_rank_index(n, 0.99)});
+      tasks.push_back({np + k, nearest_rank_index(n, 0.90)});
+      tasks.push_back({2 * np + k, n_tbt > 0 ? nearest_rank_index(n_tbt, 0.99) : 0});
+    }
+    B.seg_off.upload(off, s);
+    B.tasks.upload(tasks, s);
+    B.sel.resize(tasks.size());
+    launch_select(B.samples.ptr, B.seg_off.ptr, B.tasks.ptr, static_cast<int64_t>(tasks.size()),
+                  B.sel.ptr, s);
+    sel.resize(tasks.size());
+    B.sel.download(sel.data(), sel.size(), s);
+  }
+  out.resize(L.units.size());
+  B.out.download(out.data(), out.size(), s);
+  cuda_check(cudaStreamSynchronize(s), "sweep launch");
+  float ms = 0.f;
+  cuda_check(cudaEventElapsedTime(&ms, e0, e1), "event");
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  RunStats& st = stats();
+  st.launches_simulate += 1;
+  st.simulate_ms += ms;
+  st.units += static_cast<int64_t>(out.size());
+  for (const auto& o : out) {
+    st.iterations += o.iterations;
+    st.entries += o.entries;
+    st.events += o.events;
+    st.predictor_bytes += o.qbytes;
+    st.entry_bytes += 48 * o.entries;
+  }
 }
 
 }  // namespace
@@ -316,223 +446,121 @@ SweepKnobs knobs_from_env() {
 // Runs one launch of probes; answers are written into the candidates' memos.
 // Errors inside a probe end that candidate's evaluation (as the reference's
 // exception would), unless the probe aborted first.
-void run_probe_round(std::vector<Candidate>& cands, const std::vector<std::size_t>& active,
-                     const std::vector<std::vector<double>>& rates, const Workload& w,
-                     const CapacitySearchOptions& base) {
-  SimJobs jobs;
-  std::unordered_map<const EstimatorModel*, int32_t> est_index;
-  std::vector<ProbeSlot> slots;
-  const std::size_t n = w.lengths.size();
-  const int32_t max_late =
-      static_cast<int32_t>(n - static_cast<std::size_t>(std::ceil(0.99 * static_cast<double>(n))));
-  std::vector<Request> trace;
-  for (std::size_t a = 0; a < active.size(); ++a) {
-    Candidate& C = cands[active[a]];
-    auto it = est_index.find(C.est);
-    if (it == est_index.end()) {
-      it = est_index.emplace(C.est, static_cast<int32_t>(jobs.ests.size())).first;
-      jobs.ests.push_back(C.est->device().view);
-    }
-    SimConfig sc = C.sim;
-    sc.est = it->second;
-    const int32_t ci = static_cast<int32_t>(jobs.configs.size());
-    jobs.configs.push_back(sc);
-    for (double q : rates[a]) {
-      probe_arrivals(w, q, trace);
-      ProbeSlot p = add_probe(jobs, C, ci, trace, SSG_UF_ABORT, base.delay_p99_threshold, max_late, false);
-      p.cand = active[a];
-      p.qps = q;
-      slots.push_back(p);
-    }
-  }
-  SimResults res;
-  run_jobs(jobs, res, false);
-  std::vector<std::size_t> redo;  // probes needing the exact coupled event order
-  for (std::size_t k = 0; k < slots.size(); ++k) {
-    const ProbeSlot& p = slots[k];
-    Candidate& C = cands[p.cand];
-    int64_t late = 0;
-    int errors = 0;
-    bool aborted = false;
-    for (int32_t u = p.first_unit; u < p.first_unit + p.nunits; ++u) {
-      late += res.out[u].late;
-      aborted |= res.out[u].aborted != 0;
-      errors += res.out[u].code != SSG_OK;
-    }
-    if (errors == 0) {
-      C.memo[p.qps] = !aborted && late <= max_late;
-      continue;
-    }
-    if (!p.coupled && static_cast<int>(C.cluster.par.num_replicas) <= kMaxCoupledReplicas) {
-      redo.push_back(k);
-      continue;
-    }
-    // coupled unit: exact reference order -- an abort ends the probe before any
-    // later error; otherwise the error is the probe's (and the config's) outcome
-    const SimUnitOut* e = nullptr;
-    for (int32_t u = p.first_unit; u < p.first_unit + p.nunits; ++u)
-      if (res.out[u].code != SSG_OK && (!e || res.out[u].err_time < e->err_time)) e = &res.out[u];
-    if (aborted && p.coupled) {
-      C.memo[p.qps] = false;
-      continue;
-    }
-    try {
-      raise_unit_error(*e, C.sim, *C.est);
-    } catch (const Error& ex) {
-      C.res.error = ex.what();
-      C.done = true;
-    }
-  }
-  if (redo.empty()) return;
-  // replay the ambiguous probes with all replicas in one unit
-  SimJobs j2;
-  j2.ests = jobs.ests;
-  std::vector<ProbeSlot> s2;
-  for (std::size_t k : redo) {
-    const ProbeSlot& p = slots[k];
-    Candidate& C = cands[p.cand];
-    const int32_t ci = static_cast<int32_t>(j2.configs.size());
-    j2.configs.push_back(jobs.configs[jobs.units[p.first_unit].config]);
-    probe_arrivals(w, p.qps, trace);
-    ProbeSlot q = add_probe(j2, C, ci, trace, SSG_UF_ABORT, base.delay_p99_threshold, max_late, true);
-    q.cand = p.cand;
-    q.qps = p.qps;
-    s2.push_back(q);
-  }
-  SimResults r2;
-  run_jobs(j2, r2, false);
-  for (const auto& p : s2) {
-    Candidate& C = cands[p.cand];
-    const SimUnitOut& o = r2.out[p.first_unit];
-    if (o.aborted) {
-      C.memo[p.qps] = false;
-    } else if (o.code == SSG_OK) {
-      C.memo[p.qps] = o.late <= max_late;
-    } else {
-      try {
-        raise_unit_error(o, C.sim, *C.est);
-      } catch (const Error& ex) {
-        C.res.error = ex.what();
-        C.done = true;
-      }
-    }
+int32_t max_late_of(std::size_t n) {
+  return static_cast<int32_t>(n - static_cast<std::size_t>(std::ceil(0.99 * static_cast<double>(n))));
+}
+
+// First error of a probe's units in simulated time.
+const SimUnitOut* first_error(const std::vector<SimUnitOut>& out, const ProbeDesc& p) {
+  const SimUnitOut* e = nullptr;
+  const int nu = p.decoupled ? p.R : 1;
+  for (int u = p.first_unit; u < p.first_unit + nu; ++u)
+    if (out[u].code != SSG_OK && (!e || out[u].err_time < e->err_time)) e = &out[u];
+  return e;
+}
+
+void fail(Candidate& C, const SimUnitOut& o) {
+  try {
+    raise_unit_error(o, C.sim, *C.est);
+  } catch (const Error& ex) {
+    C.res.error = ex.what();
+    C.done = true;
   }
 }
 
-// Full runs (SLO measurement or the static makespan run) of several
-// candidates in one launch, then their TTFT p90 / TBT p99 / delay p99 by one
-// segmented select.  `qps` <= 0 means the static run (all arrivals at 0).
-void run_measurements(std::vector<Candidate>& cands, const std::vector<std::size_t>& which,
-                      const std::vector<double>& qps, const Workload& w, bool static_run) {
-  if (which.empty()) return;
-  SimJobs jobs;
-  std::unordered_map<const EstimatorModel*, int32_t> est_index;
-  std::vector<ProbeSlot> slots;
-  std::vector<Request> trace;
-  for (std::size_t a = 0; a < which.size(); ++a) {
-    Candidate& C = cands[which[a]];
-    auto it = est_index.find(C.est);
-    if (it == est_index.end()) {
-      it = est_index.emplace(C.est, static_cast<int32_t>(jobs.ests.size())).first;
-      jobs.ests.push_back(C.est->device().view);
+// One round of capacity probes; answers go into the candidates' memos.  An
+// error inside a probe ends that candidate's evaluation (the reference's
+// exception), unless the probe's abort came first in event order.
+void run_probe_round(SweepBuffers& B, std::vector<Candidate>& cands,
+                     const std::vector<std::size_t>& active,
+                     const std::vector<std::vector<double>>& rates, const ResidentWorkload& w,
+                     const CapacitySearchOptions& base) {
+  const int32_t n = w.n;
+  const int32_t max_late = max_late_of(static_cast<std::size_t>(n));
+  ProbeLaunch L;
+  for (std::size_t a = 0; a < active.size(); ++a) {
+    const Candidate& C = cands[active[a]];
+    const int32_t ci = L.add_config(C);
+    for (double q : rates[a])
+      L.add_probe(active[a], C, ci, q, n, SSG_UF_ABORT, base.delay_p99_threshold, max_late, false,
+                  false, -1);
+  }
+  std::vector<SimUnitOut> out;
+  std::vector<double> sel;
+  run_launch(B, L, w, false, false, out, sel);
+  ProbeLaunch redo;
+  for (std::size_t k = 0; k < L.probes.size(); ++k) {
+    const ProbeDesc& p = L.probes[k];
+    Candidate& C = cands[L.probe_cand[k]];
+    int64_t late = 0;
+    bool aborted = false;
+    const int nu = p.decoupled ? p.R : 1;
+    for (int u = p.first_unit; u < p.first_unit + nu; ++u) {
+      late += out[u].late;
+      aborted |= out[u].aborted != 0;
     }
-    SimConfig sc = C.sim;
-    sc.est = it->second;
-    const int32_t ci = static_cast<int32_t>(jobs.configs.size());
-    jobs.configs.push_back(sc);
-    if (static_run) {
-      trace = w.lengths;
-      for (auto& r : trace) r.arrival_time = 0.0;
+    const SimUnitOut* e = first_error(out, p);
+    if (!e) {
+      C.memo[p.qps] = !aborted && late <= max_late;
+    } else if (p.decoupled && p.R <= kMaxCoupledReplicas) {
+      // independent replicas cannot order an error against the global abort:
+      // replay this probe with every replica in one unit
+      const int32_t ci = redo.add_config(C);
+      redo.add_probe(L.probe_cand[k], C, ci, p.qps, n, SSG_UF_ABORT, base.delay_p99_threshold,
+                     max_late, true, false, -1);
+    } else if (aborted && !p.decoupled) {
+      C.memo[p.qps] = false;
     } else {
-      probe_arrivals(w, qps[a], trace);
-    }
-    // static runs put every arrival at t=0: the event order is the trace
-    // order and RR still splits by position, so replicas stay independent
-    ProbeSlot p = add_probe(jobs, C, ci, trace, SSG_UF_EMISSIONS, 0.0, 0, false);
-    p.cand = which[a];
-    slots.push_back(p);
-  }
-  SimResults res;
-  auto& ctx = context();
-  cudaStream_t s = ctx.stream;
-  run_jobs(jobs, res, true);
-  // errors first (a failing SLO run fails the config)
-  std::vector<char> ok(slots.size(), 1);
-  for (std::size_t k = 0; k < slots.size(); ++k) {
-    const ProbeSlot& p = slots[k];
-    const SimUnitOut* e = nullptr;
-    for (int32_t u = p.first_unit; u < p.first_unit + p.nunits; ++u)
-      if (res.out[u].code != SSG_OK && (!e || res.out[u].err_time < e->err_time)) e = &res.out[u];
-    if (!e) continue;
-    ok[k] = 0;
-    Candidate& C = cands[p.cand];
-    try {
-      raise_unit_error(*e, C.sim, *C.est);
-    } catch (const Error& ex) {
-      C.res.error = ex.what();
-      C.done = true;
+      fail(C, *e);
     }
   }
-  // samples: per request delay and TTFT; per emission gap (first emission of
-  // each request marked +inf, which sorts last and never reaches the ranks)
-  const std::size_t nreq = jobs.tm.size();
-  std::vector<double> delay(nreq), ttft(nreq), tbt(static_cast<std::size_t>(jobs.emissions));
-  for (std::size_t g = 0; g < nreq; ++g) {
-    delay[g] = res.tm[g].first_sched - res.tm[g].arrival;
-    ttft[g] = res.tm[g].first_tok - res.tm[g].arrival;
+  if (redo.probes.empty()) return;
+  run_launch(B, redo, w, false, false, out, sel);
+  for (std::size_t k = 0; k < redo.probes.size(); ++k) {
+    const ProbeDesc& p = redo.probes[k];
+    Candidate& C = cands[redo.probe_cand[k]];
+    const SimUnitOut& o = out[p.first_unit];
+    if (o.aborted)
+      C.memo[p.qps] = false;
+    else if (o.code == SSG_OK)
+      C.memo[p.qps] = o.late <= max_late;
+    else
+      fail(C, o);
   }
-  for (std::size_t g = 0; g < nreq; ++g) {
-    const int64_t b = jobs.emit_base[g];
-    const int64_t d = jobs.hot[g].decode;
-    tbt[b] = INFINITY;
-    for (int64_t k = 1; k < d; ++k) tbt[b + k] = res.emissions[b + k] - res.emissions[b + k - 1];
+}
+
+// Full runs -- the SLO measurement at evaluation_fraction x capacity, or the
+// static makespan run -- of several candidates in one launch; their TTFT p90,
+// TBT p99 and delay p99 come from one segmented select on the device.
+void run_measurements(SweepBuffers& B, std::vector<Candidate>& cands,
+                      const std::vector<std::size_t>& which, const std::vector<double>& qps,
+                      const ResidentWorkload& w, bool static_run) {
+  if (which.empty()) return;
+  ProbeLaunch L;
+  for (std::size_t a = 0; a < which.size(); ++a) {
+    const Candidate& C = cands[which[a]];
+    const int32_t ci = L.add_config(C);
+    const int64_t emis_base = static_cast<int64_t>(a) * w.emis_per_probe;
+    L.add_probe(which[a], C, ci, static_run ? 0.0 : qps[a], w.n, SSG_UF_EMISSIONS, 0.0, 0, false,
+                static_run, emis_base);
   }
-  // segments: [delay of probe k] [ttft of probe k] [tbt of probe k]
-  std::vector<double> pool;
-  std::vector<int64_t> off{0};
-  std::vector<SelectTask> tasks;
-  std::vector<int64_t> tbt_count(slots.size());
-  for (std::size_t k = 0; k < slots.size(); ++k) {
-    const ProbeSlot& p = slots[k];
-    const SimUnit& u0 = jobs.units[p.first_unit];
-    const SimUnit& u1 = jobs.units[p.first_unit + p.nunits - 1];
-    const int64_t r0 = u0.req_off, r1 = u1.req_off + u1.n;
-    const int64_t e0 = jobs.emit_base[r0], e1 = jobs.emit_base[r1 - 1] + jobs.hot[r1 - 1].decode;
-    const int64_t nr = r1 - r0, nt = (e1 - e0) - nr;
-    tbt_count[k] = nt;
-    pool.insert(pool.end(), delay.begin() + r0, delay.begin() + r1);
-    off.push_back(static_cast<int64_t>(pool.size()));
-    pool.insert(pool.end(), ttft.begin() + r0, ttft.begin() + r1);
-    off.push_back(static_cast<int64_t>(pool.size()));
-    pool.insert(pool.end(), tbt.begin() + e0, tbt.begin() + e1);
-    off.push_back(static_cast<int64_t>(pool.size()));
-    const int64_t seg = 3 * static_cast<int64_t>(k);
-    tasks.push_back({seg + 0, nearest_rank_index(nr, 0.99)});
-    tasks.push_back({seg + 1, nearest_rank_index(nr, 0.90)});
-    tasks.push_back({seg + 2, nt > 0 ? nearest_rank_index(nt, 0.99) : 0});
-  }
-  DeviceBuffer<double> d_pool, d_out;
-  DeviceBuffer<int64_t> d_off;
-  DeviceBuffer<SelectTask> d_tasks;
-  d_pool.upload(pool, s);
-  d_off.upload(off, s);
-  d_tasks.upload(tasks, s);
-  d_out.resize(tasks.size());
-  launch_select(d_pool.ptr, d_off.ptr, d_tasks.ptr, static_cast<int64_t>(tasks.size()), d_out.ptr, s);
-  std::vector<double> sel(tasks.size());
-  d_out.download(sel.data(), sel.size(), s);
-  cuda_check(cudaStreamSynchronize(s), "slo select");
-  for (std::size_t k = 0; k < slots.size(); ++k) {
-    if (!ok[k]) continue;
-    Candidate& C = cands[slots[k].cand];
-    const bool has_tbt = tbt_count[k] > 0;
+  std::vector<SimUnitOut> out;
+  std::vector<double> sel;
+  run_launch(B, L, w, true, true, out, sel);
+  for (std::size_t k = 0; k < L.probes.size(); ++k) {
+    const ProbeDesc& p = L.probes[k];
+    Candidate& C = cands[L.probe_cand[k]];
+    if (const SimUnitOut* e = first_error(out, p)) {
+      fail(C, *e);
+      continue;
+    }
     C.res.delay_p99 = sel[3 * k + 0];
     C.res.ttft_p90 = sel[3 * k + 1];
-    C.res.tbt_p99 = has_tbt ? sel[3 * k + 2] : 0.0;  // summarize({}) leaves 0
+    C.res.tbt_p99 = (w.emis_per_probe - w.n) > 0 ? sel[3 * k + 2] : 0.0;  // summarize({}) -> 0
     if (static_run) {
       double span = 0.0;
-      for (int32_t u = slots[k].first_unit; u < slots[k].first_unit + slots[k].nunits; ++u)
-        span = std::max(span, res.out[u].span);
+      const int nu = p.decoupled ? p.R : 1;
+      for (int u = p.first_unit; u < p.first_unit + nu; ++u) span = std::max(span, out[u].span);
       C.res.makespan = span;
     }
   }
@@ -546,6 +574,8 @@ struct SearchSession::State {
   std::vector<CandidateConfig> configs;
   std::vector<EstimatorModel> ests;
   Workload w;
+  ResidentWorkload rw;
+  SweepBuffers buffers;
 };
 
 SearchSession::SearchSession(const ModelSpec& spec, const std::vector<Request>& workload,
@@ -572,6 +602,31 @@ SearchSession::SearchSession(const ModelSpec& spec, const std::vector<Request>& 
     S.w.lengths.push_back(r);
   }
   S.w.unit_exp = unit_exponentials(S.w.lengths.size(), opts.capacity.seed);
+  // resident probe stream inputs
+  auto& ctx = context();
+  const std::size_t n = S.w.lengths.size();
+  require(n < static_cast<std::size_t>(INT32_MAX), "search: probe_requests too large");
+  std::vector<int32_t> pre(n), dec(n);
+  std::vector<int64_t> prefix(n);
+  int64_t acc = 0;
+  for (std::size_t i = 0; i < n; ++i) {
+    require(S.w.lengths[i].prefill_tokens < INT32_MAX / 2 && S.w.lengths[i].decode_tokens < INT32_MAX / 2,
+            "ssg: request lengths above the device engine limit");
+    pre[i] = static_cast<int32_t>(S.w.lengths[i].prefill_tokens);
+    dec[i] = static_cast<int32_t>(S.w.lengths[i].decode_tokens);
+    prefix[i] = acc;
+    acc += dec[i];
+  }
+  std::vector<uint8_t> first(static_cast<std::size_t>(acc), 0);
+  for (std::size_t i = 0; i < n; ++i) first[prefix[i]] = 1;
+  S.rw.n = static_cast<int32_t>(n);
+  S.rw.emis_per_probe = acc;
+  S.rw.pre.upload(pre, ctx.stream);
+  S.rw.dec.upload(dec, ctx.stream);
+  S.rw.unit_exp.upload(S.w.unit_exp, ctx.stream);
+  S.rw.dec_prefix.upload(prefix, ctx.stream);
+  S.rw.first_emis.upload(first, ctx.stream);
+  cuda_check(cudaStreamSynchronize(ctx.stream), "session upload");
 }
 
 SearchSession::~SearchSession() = default;
@@ -592,7 +647,8 @@ std::vector<ConfigResult> SearchSession::evaluate(int shard, int num_shards) {
   const SearchOptions& opts = S.opts;
   const auto& configs = S.configs;
   const auto& ests = S.ests;
-  const Workload& w = S.w;
+  const ResidentWorkload& w = S.rw;
+  SweepBuffers& B = st_->buffers;
   std::vector<ConfigResult> results(configs.size());
   std::vector<Candidate> cands;
   for (std::size_t i = 0; i < configs.size(); ++i) {
@@ -612,33 +668,89 @@ std::vector<ConfigResult> SearchSession::evaluate(int shard, int num_shards) {
       C.sim_ok = true;
     } catch (const Error& e) {
       C.sim_error = e.what();
-      C.sim_error_kind = 1;
     }
     cands.push_back(std::move(C));
   }
 
   const bool makespan = opts.objective == "makespan";
   std::vector<std::size_t> live;
-  for (std::size_t k = 0; k < cands.size(); ++k) {
-    Candidate& C = cands[k];
-    if (makespan) {
-      // the static run is the first simulation: its preamble errors surface
+  if (makespan) {
+    // the static run is the first simulation: its preamble errors surface
+    for (auto& C : cands)
       if (!C.sim_ok) {
         C.res.error = C.sim_error;
         C.done = true;
       }
-      continue;
+  } else {
+    // initial_qps_guess (search.hpp:278-290) for every candidate in one launch:
+    // predict_batch of a 512-token prefill and of one 512-context decode
+    std::vector<SimConfig> gcfg;
+    std::vector<SsgEstView> gest;
+    std::unordered_map<const EstimatorModel*, int32_t> gidx;
+    std::vector<int32_t> comp_cfg;
+    std::vector<std::size_t> who;
+    std::vector<int64_t> p_off{0}, d_off{0}, p_len, p_prior, d_ctx;
+    const std::int64_t len = std::min<std::int64_t>(512, spec.max_context);
+    for (std::size_t k = 0; k < cands.size(); ++k) {
+      Candidate& C = cands[k];
+      try {
+        auto ops = derive_operators(spec, C.cand.par);
+        // predict()'s find() order over the two compositions (a missing model
+        // raises the reference's message for the first op looked up)
+        for (int pass = 0; pass < 2; ++pass)
+          for (const auto& d : ops) {
+            if (pass == 0 && d.op == OpName::AttnDecode) continue;
+            if (pass == 1 && d.op == OpName::AttnPrefill) continue;
+            C.est->find(d.op, d.tp_degree);
+          }
+        SimConfig g{};
+        fill_sim_ops(g, ops, C.est->device());
+        auto it = gidx.find(C.est);
+        if (it == gidx.end()) {
+          it = gidx.emplace(C.est, static_cast<int32_t>(gest.size())).first;
+          gest.push_back(C.est->device().view);
+        }
+        g.est = it->second;
+        gcfg.push_back(g);
+        const int32_t ci = static_cast<int32_t>(gcfg.size() - 1);
+        comp_cfg.push_back(ci);  // prefill composition
+        p_len.push_back(len);
+        p_prior.push_back(0);
+        p_off.push_back(static_cast<int64_t>(p_len.size()));
+        d_off.push_back(static_cast<int64_t>(d_ctx.size()));
+        comp_cfg.push_back(ci);  // decode composition
+        d_ctx.push_back(len);
+        p_off.push_back(static_cast<int64_t>(p_len.size()));
+        d_off.push_back(static_cast<int64_t>(d_ctx.size()));
+        who.push_back(k);
+      } catch (const Error& e) {
+        C.res.error = e.what();
+        C.done = true;
+      }
     }
-    try {
-      C.guess = initial_qps_guess(spec, C.cand, *C.est, C.cluster);
-      C.copts.initial_guess = C.guess;
-      require(C.copts.initial_guess > 0 && C.copts.tolerance > 0, "find_capacity: bad options");
-      // the first probe's run_simulation preamble (validation, plan_memory)
-      if (!C.sim_ok) throw Error(C.sim_error);
-      live.push_back(k);
-    } catch (const Error& e) {
-      C.res.error = e.what();
-      C.done = true;
+    const int64_t ncomp = static_cast<int64_t>(comp_cfg.size());
+    std::vector<double> secs(ncomp), fl(ncomp);
+    std::vector<SimUnitOut> status;
+    predict_batches_multi(gcfg, gest, comp_cfg, ncomp, p_off.data(), p_len.data(), p_prior.data(),
+                          d_off.data(), d_ctx.data(), secs.data(), fl.data(), status);
+    for (std::size_t w2 = 0; w2 < who.size(); ++w2) {
+      Candidate& C = cands[who[w2]];
+      try {
+        for (int q = 0; q < 2; ++q)
+          if (status[2 * w2 + q].code != SSG_OK)
+            raise_unit_error(status[2 * w2 + q], gcfg[w2], *C.est);
+        const double service = secs[2 * w2] + 64.0 * secs[2 * w2 + 1];
+        const double per_replica = 1.0 / std::max(service, 1e-9);
+        C.copts.initial_guess =
+            std::max(1e-3, per_replica * static_cast<double>(C.cluster.par.num_replicas));
+        require(C.copts.initial_guess > 0 && C.copts.tolerance > 0, "find_capacity: bad options");
+        // the first probe's run_simulation preamble (validation, plan_memory)
+        if (!C.sim_ok) throw Error(C.sim_error);
+        live.push_back(who[w2]);
+      } catch (const Error& e) {
+        C.res.error = e.what();
+        C.done = true;
+      }
     }
   }
 
@@ -646,7 +758,7 @@ std::vector<ConfigResult> SearchSession::evaluate(int shard, int num_shards) {
     std::vector<std::size_t> ok;
     for (std::size_t k = 0; k < cands.size(); ++k)
       if (!cands[k].done) ok.push_back(k);
-    run_measurements(cands, ok, {}, w, true);
+    run_measurements(B, cands, ok, {}, w, true);
     for (auto k : ok) {
       Candidate& C = cands[k];
       if (!C.res.failed()) {
@@ -683,7 +795,7 @@ std::vector<ConfigResult> SearchSession::evaluate(int shard, int num_shards) {
         }
       }
       if (active.empty()) break;
-      run_probe_round(cands, active, rates, w, opts.capacity);
+      run_probe_round(B, cands, active, rates, w, opts.capacity);
       std::vector<std::size_t> still;
       for (auto k : active)
         if (!cands[k].done) still.push_back(k);
@@ -704,7 +816,7 @@ std::vector<ConfigResult> SearchSession::evaluate(int shard, int num_shards) {
       eval_qps.push_back(opts.evaluation_fraction * C.res.capacity_qps);
     }
     for (double q : eval_qps) require(q > 0.0, "poisson_arrivals: rate must be positive");
-    run_measurements(cands, measure, eval_qps, w, false);
+    run_measurements(B, cands, measure, eval_qps, w, false);
     for (auto k : measure) {
       Candidate& C = cands[k];
       if (C.res.failed()) continue;

@@ -43,6 +43,7 @@ int probe_host_math_variant();
 // bench reports them next to its timings).
 struct RunStats {
   int64_t launches_simulate = 0, launches_select = 0, launches_predict = 0, launches_batch = 0;
+  int64_t launches_setup = 0;
   int64_t units = 0, iterations = 0, entries = 0, events = 0;
   int64_t predictor_bytes = 0, entry_bytes = 0;
   double simulate_ms = 0.0;  // k_simulate device time, CUDA events on the launching stream

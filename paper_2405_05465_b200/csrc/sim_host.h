@@ -25,6 +25,14 @@ void predict_batches(const servesim::EstimatorModel& est, const SimConfig& cfg, 
                      const int64_t* p_off, const int64_t* p_len, const int64_t* p_prior,
                      const int64_t* d_off, const int64_t* d_ctx, double* seconds, double* flops);
 
+// Same over compositions of several configs (cfgs[comp_cfg[c]]; cfgs[].est
+// indexes ests); per-composition status instead of exceptions.
+void predict_batches_multi(const std::vector<SimConfig>& cfgs, const std::vector<SsgEstView>& ests,
+                           const std::vector<int32_t>& comp_cfg, int64_t n, const int64_t* p_off,
+                           const int64_t* p_len, const int64_t* p_prior, const int64_t* d_off,
+                           const int64_t* d_ctx, double* seconds, double* flops,
+                           std::vector<SimUnitOut>& status);
+
 struct UnitSpec {
   int32_t config = 0;
   int32_t R = 1;
