@@ -278,7 +278,60 @@ __device__ bool batch_start(Unit& U, RepState& S, int r) {
   return true;
 }
 
+// Token tables: one thread per (table, t).  Same device arithmetic as the
+// full per-batch path, so every entry equals what batch_latency would compute.
+__global__ void k_build_tables(const SimConfig* __restrict__ cfgs, int32_t n, int32_t stride,
+                               const SsgEstView* __restrict__ ests, double* __restrict__ pool,
+                               uint8_t* __restrict__ valid) {
+  const int32_t i = blockIdx.y;
+  const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || t >= stride) return;
+  const SimConfig& c = cfgs[i];
+  const SsgEstView E = ests[c.est];
+  double* tab = pool + c.tab_off;
+  const double tokens = (double)t;
+  double s6 = 0.0, f6 = 0.0, cm[3] = {0.0, 0.0, 0.0}, p0 = 0.0, p0f = 0.0;
+  bool ok_tok = t >= 1, ok_pre = t >= 1;
+  int k = 0;
+  for (int oi = 0; oi < c.nops; ++oi) {
+    const SimOp& o = c.ops[oi];
+    double pred = 0.0;
+    int bad = 0;
+    if (o.cls == SSG_CLS_TOKEN) {
+      if (ssg_predict_one(E, o.slot, tokens, 0.0, &pred, &bad) != SSG_OK) ok_tok = false;
+      s6 = __dadd_rn(s6, __dmul_rn(o.count, pred));
+      double fl;
+      if (o.flop_kind == 0)
+        fl = __dmul_rn(__dmul_rn(__dmul_rn(2.0, tokens), o.fa), o.fb);
+      else if (o.flop_kind == 1)
+        fl = __dmul_rn(tokens, o.fa);
+      else
+        fl = __dmul_rn(__dmul_rn(8.0, tokens), o.fa);
+      f6 = __dadd_rn(f6, __dmul_rn(o.count, fl));
+    } else if (o.cls == SSG_CLS_COMM) {
+      if (ssg_predict_one(E, o.slot, __dmul_rn(tokens, o.payload), 0.0, &pred, &bad) != SSG_OK)
+        ok_tok = false;
+      if (k < 3) cm[k++] = __dmul_rn(o.count, pred);
+    } else if (o.flop_kind == 3) {
+      const double v1 = __dmul_rn(0.0, o.kvb);
+      const double ctx_tokens = v1 / o.kvb;
+      if (ssg_predict_one(E, o.slot, tokens, v1, &pred, &bad) != SSG_OK) ok_pre = false;
+      p0 = __dmul_rn(o.count, pred);
+      p0f = __dmul_rn(o.count, __dmul_rn(__dmul_rn(__dmul_rn(4.0, tokens), __dadd_rn(tokens, ctx_tokens)), o.fa));
+    }
+  }
+  tab[t] = s6;
+  tab[(int64_t)stride + t] = f6;
+  tab[2LL * stride + t] = cm[0];
+  tab[3LL * stride + t] = cm[1];
+  tab[4LL * stride + t] = cm[2];
+  tab[5LL * stride + t] = p0;
+  tab[6LL * stride + t] = p0f;
+  valid[(int64_t)i * stride + t] = (ok_tok ? 1 : 0) | (ok_pre ? 2 : 0);
+}
+
 __device__ void run_unit(Unit& U) {
+  const long long t_start = clock64();
   const SimUnit& u = *U.u;
   const SimConfig& c = *U.cfg;
   const int R = u.R;
@@ -432,6 +485,7 @@ __device__ void run_unit(Unit& U) {
     U.out->iterations = U.iters;
     U.out->entries = U.entries;
     U.out->qbytes = U.qbytes;
+    U.out->cycles = clock64() - t_start;
   }
   __syncwarp();
   if (!failed(U) && !U.out->aborted) {
@@ -454,13 +508,21 @@ __global__ void __launch_bounds__(SSG_SIM_WARPS * 32)
     k_simulate(SimLaunch L) {
   __shared__ int64_t stats[SSG_SIM_WARPS][SSG_MAX_PP * 6];
   __shared__ double part[SSG_SIM_WARPS][4 * SSG_MAX_PP];
+  __shared__ SimConfig cfg_s[SSG_SIM_WARPS];  // the unit's config, read every event
   const int wib = threadIdx.x >> 5;
   const int64_t w = (int64_t)blockIdx.x * SSG_SIM_WARPS + wib;
   if (w >= L.nunits) return;
   const int32_t uid = L.order ? L.order[w] : (int32_t)w;
   Unit U;
   U.u = L.units + uid;
-  U.cfg = L.configs + U.u->config;
+  {
+    const int lane = threadIdx.x & 31;
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(L.configs + U.u->config);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(&cfg_s[wib]);
+    for (int k = lane; k < (int)(sizeof(SimConfig) / 4); k += 32) dst[k] = src[k];
+    __syncwarp();
+  }
+  U.cfg = &cfg_s[wib];
   U.E = L.ests[U.cfg->est];
   U.hot = L.hot + U.u->req_off;
   U.tm = L.tm + U.u->req_off;
@@ -475,6 +537,7 @@ __global__ void __launch_bounds__(SSG_SIM_WARPS * 32)
   U.out = L.out + uid;
   U.smem_stats = stats[wib];
   U.smem_part = part[wib];
+  U.tables = L.tables;
   U.group_late = nullptr;
   U.lane = threadIdx.x & 31;
   U.MB = U.cfg->max_batch;
@@ -509,6 +572,7 @@ __global__ void __launch_bounds__(SSG_SIM_WARPS * 32)
   U.out = out + c;
   U.smem_stats = stats[wib];
   U.smem_part = part[wib];
+  U.tables = nullptr;
   U.lane = threadIdx.x & 31;
   U.clock = 0.0;
   U.qbytes = 0;
@@ -532,6 +596,15 @@ __global__ void __launch_bounds__(SSG_SIM_WARPS * 32)
 }  // namespace ssgk
 
 namespace ssg {
+
+void launch_build_tables(const SimConfig* d_cfgs, int32_t n, int32_t stride,
+                         const SsgEstView* d_ests, double* d_pool, uint8_t* d_valid, cudaStream_t s) {
+  if (n <= 0) return;
+  dim3 grid((stride + 127) / 128, n);
+  ssgk::k_build_tables<<<grid, 128, 0, s>>>(d_cfgs, n, stride, d_ests, d_pool, d_valid);
+  cuda_check(cudaGetLastError(), "k_build_tables launch");
+  stats().launches_setup += 1;
+}
 
 void launch_simulate(const SimLaunch& L, cudaStream_t s) {
   if (L.nunits <= 0) return;

@@ -44,6 +44,7 @@ struct Unit {
   int64_t* log;
   SimUnitOut* out;
   int64_t* smem_stats;  // per-warp shared scratch [SSG_MAX_PP * 6]
+  const double* tables; // token tables pool (SimConfig::tab_off)
   double* smem_part;    // per-warp shared scratch [4 * SSG_MAX_PP]
   int* group_late;  // shared by the probe's units (may be null)
   int lane;
@@ -567,102 +568,198 @@ __device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, doubl
   }
   __syncwarp();
   const int nops = c.nops;
-  const int work = pp * nops;
   double* secs_part = U.smem_part;       // [pp]
   double* flop_part = U.smem_part + SSG_MAX_PP;
-  double acc_s = 0.0, acc_f = 0.0;
-  int64_t qb = 0;
-  int cur_m = 0;
   int err = SSG_OK, err_task = 0, err_feat = 0;
   double err_val = 0.0;
-  for (int base = 0; base < work; base += 32) {
-    const int t = base + U.lane;
+  int64_t qb = 0;
+  // token-table fast path: every non-empty microbatch within the tables' range
+  bool use_tab = c.tab_off >= 0;
+  for (int m = 0; m < pp && use_tab; ++m)
+    if (st[m * 6 + 1] > c.tab_tmax) use_tab = false;
+  if (use_tab) {
+    const int T1 = c.tab_stride;
+    const double* tab = U.tables + c.tab_off;
+    // per-lane work: lane 2m = prefill attention of microbatch m, 2m+1 = decode attention
+    const int m = U.lane >> 1;
+    const bool is_dec = U.lane & 1;
     double pred = 0.0, fl = 0.0, v0 = 0.0, v1 = 0.0;
-    bool active = false;
     int code = SSG_OK, bad = 0;
-    if (t < work) {
-      const int m = t / nops;
-      const SimOp& o = c.ops[t - m * nops];
-      const int64_t* s = st + m * 6;
-      const double tokens = (double)s[1];
-      if (s[1] > 0) {
-        if (o.cls == SSG_CLS_TOKEN) {
-          active = true;
-          v0 = tokens;
-          if (o.flop_kind == 0)
-            fl = __dmul_rn(__dmul_rn(__dmul_rn(2.0, tokens), o.fa), o.fb);
-          else if (o.flop_kind == 1)
-            fl = __dmul_rn(tokens, o.fa);
-          else
-            fl = __dmul_rn(__dmul_rn(8.0, tokens), o.fa);
-        } else if (o.cls == SSG_CLS_SEQ) {
-          if (o.flop_kind == 3 && s[0] > 0) {
-            active = true;
-            const double n_eq = (double)ssg_llround_nonneg(sqrt((double)s[2]));
-            v0 = n_eq;
-            v1 = __dmul_rn((double)s[3], o.kvb);
-            const double ctx_tokens = v1 / o.kvb;
-            fl = __dmul_rn(__dmul_rn(__dmul_rn(4.0, n_eq), __dadd_rn(n_eq, ctx_tokens)), o.fa);
-          } else if (o.flop_kind == 4 && s[4] > 0) {
-            active = true;
-            v0 = (double)s[4];
-            v1 = __dmul_rn((double)s[5], o.kvb);
-            const double ctx_tokens = v1 / o.kvb;
-            fl = __dmul_rn(__dmul_rn(4.0, ctx_tokens), o.fa);
-          }
-        } else {
-          active = true;
-          v0 = __dmul_rn(tokens, o.payload);
-        }
+    bool active = false;
+    int op_index = 0;
+    if (m < pp) {
+      const int64_t* s6 = st + m * 6;
+      for (int k = 0; k < nops; ++k) {
+        const SimOp& o = c.ops[k];
+        if (o.cls == SSG_CLS_SEQ && (o.flop_kind == 4) == is_dec) op_index = k;
       }
-      if (active) {
-        qb += o.qbytes;
+      const SimOp& o = c.ops[op_index];
+      if (s6[1] > 0 && !is_dec && s6[0] > 0) {
+        active = true;
+        const int64_t n_eq = ssg_llround_nonneg(sqrt((double)s6[2]));
+        if (s6[3] == 0 && n_eq <= c.tab_pmax) {
+          pred = tab[5 * (int64_t)T1 + n_eq];
+          fl = tab[6 * (int64_t)T1 + n_eq];
+        } else {
+          v0 = (double)n_eq;
+          v1 = __dmul_rn((double)s6[3], o.kvb);
+          const double ctx_tokens = v1 / o.kvb;
+          code = ssg_predict_one(U.E, o.slot, v0, v1, &pred, &bad);
+          pred = __dmul_rn(o.count, pred);
+          fl = __dmul_rn(o.count, __dmul_rn(__dmul_rn(__dmul_rn(4.0, v0), __dadd_rn(v0, ctx_tokens)), o.fa));
+        }
+      } else if (s6[1] > 0 && is_dec && s6[4] > 0) {
+        active = true;
+        v0 = (double)s6[4];
+        v1 = __dmul_rn((double)s6[5], o.kvb);
+        const double ctx_tokens = v1 / o.kvb;
         code = ssg_predict_one(U.E, o.slot, v0, v1, &pred, &bad);
         pred = __dmul_rn(o.count, pred);
-        fl = (o.cls == SSG_CLS_COMM) ? 0.0 : __dmul_rn(o.count, fl);
+        fl = __dmul_rn(o.count, __dmul_rn(__dmul_rn(4.0, ctx_tokens), o.fa));
       }
     }
     const unsigned em = __ballot_sync(SSG_FULL, code != SSG_OK);
-    if (em && err == SSG_OK) {
-      const int src = __ffs(em) - 1;
+    if (em) {
+      const int src = __ffs(em) - 1;  // lanes are in (microbatch, prefill < decode) order
       err = __shfl_sync(SSG_FULL, code, src);
-      err_task = base + src;
       err_feat = __shfl_sync(SSG_FULL, bad, src);
       err_val = __shfl_sync(SSG_FULL, bad ? v1 : v0, src);
+      err_task = __shfl_sync(SSG_FULL, op_index, src);  // op index within microbatch 0's numbering
     }
-    const int kmax = (work - base) < 32 ? (work - base) : 32;
-    for (int k = 0; k < kmax; ++k) {
-      const double pk = __shfl_sync(SSG_FULL, pred, k);
-      const double fk = __shfl_sync(SSG_FULL, fl, k);
-      const int ak = __shfl_sync(SSG_FULL, (int)active, k);
-      const int m = (base + k) / nops;
-      if (m != cur_m) {
-        if (U.lane == 0) {
-          secs_part[cur_m] = acc_s;
-          flop_part[cur_m] = acc_f;
+    // algorithmic bytes: every query the reference makes, however it is served
+    for (int mm = 0; mm < pp; ++mm) {
+      const int64_t* s6 = st + mm * 6;
+      if (s6[1] == 0) continue;
+      for (int k = 0; k < nops; ++k) {
+        const SimOp& o = c.ops[k];
+        if (o.cls != SSG_CLS_SEQ || (o.flop_kind == 3 && s6[0] > 0) || (o.flop_kind == 4 && s6[4] > 0))
+          qb += o.qbytes;
+      }
+    }
+    U.qbytes += qb;
+    for (int mm = 0; mm < pp; ++mm) {
+      const double pp_pred = __shfl_sync(SSG_FULL, pred, 2 * mm);
+      const double pp_fl = __shfl_sync(SSG_FULL, fl, 2 * mm);
+      const int pp_act = __shfl_sync(SSG_FULL, (int)active, 2 * mm);
+      const double dd_pred = __shfl_sync(SSG_FULL, pred, 2 * mm + 1);
+      const double dd_fl = __shfl_sync(SSG_FULL, fl, 2 * mm + 1);
+      const int dd_act = __shfl_sync(SSG_FULL, (int)active, 2 * mm + 1);
+      const int64_t t = st[mm * 6 + 1];
+      double acc_s = 0.0, acc_f = 0.0;
+      if (t > 0) {
+        acc_s = tab[t];                 // token-level ops, op order
+        acc_f = tab[(int64_t)T1 + t];
+        if (pp_act) {
+          acc_s = __dadd_rn(acc_s, pp_pred);
+          acc_f = __dadd_rn(acc_f, pp_fl);
         }
-        acc_s = 0.0;
-        acc_f = 0.0;
-        cur_m = m;
+        if (dd_act) {
+          acc_s = __dadd_rn(acc_s, dd_pred);
+          acc_f = __dadd_rn(acc_f, dd_fl);
+        }
+        int k = 0;
+        for (int oi = 0; oi < nops; ++oi)
+          if (c.ops[oi].cls == SSG_CLS_COMM) acc_s = __dadd_rn(acc_s, tab[(int64_t)(2 + k++) * T1 + t]);
       }
-      if (ak) {
-        acc_s = __dadd_rn(acc_s, pk);
-        if (c.ops[(base + k) - m * nops].cls != SSG_CLS_COMM) acc_f = __dadd_rn(acc_f, fk);
+      if (U.lane == 0) {
+        secs_part[mm] = acc_s;
+        flop_part[mm] = acc_f;
       }
     }
-  }
-  if (U.lane == 0) {
-    secs_part[cur_m] = acc_s;
-    flop_part[cur_m] = acc_f;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) qb += __shfl_xor_sync(SSG_FULL, qb, o);
-  U.qbytes += qb;
-  __syncwarp();
-  if (err != SSG_OK) {
-    const SimOp& o = c.ops[err_task % nops];
-    set_error(U, err, o.slot, err_feat, 0, err_val);
-    return err;
+    __syncwarp();
+  } else {
+    const int work = pp * nops;
+    double acc_s = 0.0, acc_f = 0.0;
+    int cur_m = 0;
+    for (int base = 0; base < work; base += 32) {
+      const int t = base + U.lane;
+      double pred = 0.0, fl = 0.0, v0 = 0.0, v1 = 0.0;
+      bool active = false;
+      int code = SSG_OK, bad = 0;
+      if (t < work) {
+        const int m = t / nops;
+        const SimOp& o = c.ops[t - m * nops];
+        const int64_t* s = st + m * 6;
+        const double tokens = (double)s[1];
+        if (s[1] > 0) {
+          if (o.cls == SSG_CLS_TOKEN) {
+            active = true;
+            v0 = tokens;
+            if (o.flop_kind == 0)
+              fl = __dmul_rn(__dmul_rn(__dmul_rn(2.0, tokens), o.fa), o.fb);
+            else if (o.flop_kind == 1)
+              fl = __dmul_rn(tokens, o.fa);
+            else
+              fl = __dmul_rn(__dmul_rn(8.0, tokens), o.fa);
+          } else if (o.cls == SSG_CLS_SEQ) {
+            if (o.flop_kind == 3 && s[0] > 0) {
+              active = true;
+              const double n_eq = (double)ssg_llround_nonneg(sqrt((double)s[2]));
+              v0 = n_eq;
+              v1 = __dmul_rn((double)s[3], o.kvb);
+              const double ctx_tokens = v1 / o.kvb;
+              fl = __dmul_rn(__dmul_rn(__dmul_rn(4.0, n_eq), __dadd_rn(n_eq, ctx_tokens)), o.fa);
+            } else if (o.flop_kind == 4 && s[4] > 0) {
+              active = true;
+              v0 = (double)s[4];
+              v1 = __dmul_rn((double)s[5], o.kvb);
+              const double ctx_tokens = v1 / o.kvb;
+              fl = __dmul_rn(__dmul_rn(4.0, ctx_tokens), o.fa);
+            }
+          } else {
+            active = true;
+            v0 = __dmul_rn(tokens, o.payload);
+          }
+        }
+        if (active) {
+          qb += o.qbytes;
+          code = ssg_predict_one(U.E, o.slot, v0, v1, &pred, &bad);
+          pred = __dmul_rn(o.count, pred);
+          fl = (o.cls == SSG_CLS_COMM) ? 0.0 : __dmul_rn(o.count, fl);
+        }
+      }
+      const unsigned em = __ballot_sync(SSG_FULL, code != SSG_OK);
+      if (em && err == SSG_OK) {
+        const int src = __ffs(em) - 1;
+        err = __shfl_sync(SSG_FULL, code, src);
+        err_task = base + src;
+        err_feat = __shfl_sync(SSG_FULL, bad, src);
+        err_val = __shfl_sync(SSG_FULL, bad ? v1 : v0, src);
+      }
+      const int kmax = (work - base) < 32 ? (work - base) : 32;
+      for (int k = 0; k < kmax; ++k) {
+        const double pk = __shfl_sync(SSG_FULL, pred, k);
+        const double fk = __shfl_sync(SSG_FULL, fl, k);
+        const int ak = __shfl_sync(SSG_FULL, (int)active, k);
+        const int m = (base + k) / nops;
+        if (m != cur_m) {
+          if (U.lane == 0) {
+            secs_part[cur_m] = acc_s;
+            flop_part[cur_m] = acc_f;
+          }
+          acc_s = 0.0;
+          acc_f = 0.0;
+          cur_m = m;
+        }
+        if (ak) {
+          acc_s = __dadd_rn(acc_s, pk);
+          if (c.ops[(base + k) - m * nops].cls != SSG_CLS_COMM) acc_f = __dadd_rn(acc_f, fk);
+        }
+      }
+    }
+    if (U.lane == 0) {
+      secs_part[cur_m] = acc_s;
+      flop_part[cur_m] = acc_f;
+    }
+  #pragma unroll
+    for (int o = 16; o > 0; o >>= 1) qb += __shfl_xor_sync(SSG_FULL, qb, o);
+    U.qbytes += qb;
+    __syncwarp();
+    if (err != SSG_OK) {
+      const SimOp& o = c.ops[err_task % nops];
+      set_error(U, err, o.slot, err_feat, 0, err_val);
+      return err;
+    }
   }
   double lat = 0.0, flops = 0.0;
   if (pp == 1) {

@@ -16,6 +16,8 @@
 // then selects exactly the capacity the sequential reference would.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <sstream>
 #include <unordered_map>
@@ -169,11 +171,8 @@ void speculate(const NeedProbe& need, const CapacitySearchOptions& o, int ladder
       out.push_back(q);
     }
   } else if (need.phase == 1) {
-    double hi = need.hi / 2.0;
-    for (int k = 1; k < ladder && hi > o.min_qps; ++k) {
-      out.push_back(hi / 2.0);
-      hi /= 2.0;
-    }
+    // halving: each deeper rate is the slowest probe of its round (iterations
+    // grow ~1/qps), and the first halving usually suffices -- no speculation
   } else {
     // bisection sub-tree below (lo, hi) to `depth` levels
     std::vector<std::pair<double, double>> level{{need.lo, need.hi}}, next;
@@ -224,6 +223,7 @@ struct SweepBuffers {
   DeviceBuffer<RepState> reps;
   DeviceBuffer<SimUnitOut> out;
   DeviceBuffer<SelectTask> tasks;
+  DeviceBuffer<double> tables;  // token tables of the session's configs
 };
 
 // A launch under construction: per-candidate configs, probes and their units.
@@ -336,6 +336,7 @@ void run_launch(SweepBuffers& B, ProbeLaunch& L, const ResidentWorkload& w, bool
   K.ws = B.ws.ptr;
   K.log = nullptr;
   K.out = B.out.ptr;
+  K.tables = B.tables.ptr;
   cudaEvent_t e0, e1;
   cuda_check(cudaEventCreate(&e0), "event");
   cuda_check(cudaEventCreate(&e1), "event");
@@ -378,6 +379,24 @@ void run_launch(SweepBuffers& B, ProbeLaunch& L, const ResidentWorkload& w, bool
   cuda_check(cudaEventElapsedTime(&ms, e0, e1), "event");
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  if (const char* dump = std::getenv("SSG_DUMP_UNITS")) {
+    // diagnostics: one line per unit (launch, unit, config, n, R, iterations, cycles, qps)
+    FILE* f = std::fopen(dump, "a");
+    if (f) {
+      static int launch_no = 0;
+      std::vector<double> qps_of(L.units.size(), 0.0);
+      for (const auto& p : L.probes)
+        for (int u = p.first_unit; u < p.first_unit + (p.decoupled ? p.R : 1); ++u) qps_of[u] = p.qps;
+      for (std::size_t u = 0; u < out.size(); ++u)
+        std::fprintf(f, "%d %zu %d %d %d %lld %lld %.17g %d %d\n", launch_no, u, L.units[u].config,
+                     L.units[u].n, L.units[u].R, (long long)out[u].iterations,
+                     (long long)out[u].cycles, qps_of[u], L.configs[L.units[u].config].policy,
+                     L.configs[L.units[u].config].max_batch);
+      std::fprintf(f, "# launch %d ms %.3f\n", launch_no, ms);
+      ++launch_no;
+      std::fclose(f);
+    }
+  }
   RunStats& st = stats();
   st.launches_simulate += 1;
   st.simulate_ms += ms;
@@ -670,6 +689,34 @@ std::vector<ConfigResult> SearchSession::evaluate(int shard, int num_shards) {
       C.sim_error = e.what();
     }
     cands.push_back(std::move(C));
+  }
+
+  {
+    // token tables for every distinct (SKU, tp, pp) operator table
+    std::vector<SimConfig> tcfg;
+    std::vector<std::size_t> tk;
+    std::vector<SsgEstView> tests;
+    std::vector<const DeviceEstimator*> test_of;
+    for (const auto& e : ests) {
+      tests.push_back(e.device().view);
+      test_of.push_back(&e.device());
+    }
+    for (std::size_t k = 0; k < cands.size(); ++k) {
+      if (!cands[k].sim_ok) continue;
+      SimConfig c = cands[k].sim;
+      c.est = static_cast<int32_t>(cands[k].cand.sku_index);
+      tcfg.push_back(c);
+      tk.push_back(k);
+    }
+    if (std::getenv("SSG_NO_TABLES") == nullptr)
+      build_token_tables(tcfg, tests, test_of, B.tables);
+    for (std::size_t i = 0; i < tk.size(); ++i) {
+      SimConfig& c = cands[tk[i]].sim;
+      c.tab_off = tcfg[i].tab_off;
+      c.tab_stride = tcfg[i].tab_stride;
+      c.tab_tmax = tcfg[i].tab_tmax;
+      c.tab_pmax = tcfg[i].tab_pmax;
+    }
   }
 
   const bool makespan = opts.objective == "makespan";

@@ -5,7 +5,9 @@
 //            model_spec.hpp:203-266 (operators), memory.hpp:21-46
 #include <algorithm>
 #include <cmath>
+#include <map>
 #include <numeric>
+#include <string>
 
 #include "sim_host.h"
 #include "engine_limits.h"
@@ -17,6 +19,10 @@ using namespace servesim;
 void fill_sim_ops(SimConfig& c, const std::vector<OperatorDescriptor>& ops, const DeviceEstimator& de) {
   internal_check(ops.size() <= SSG_MAX_OPS, "operator set larger than the device table");
   c.nops = static_cast<int32_t>(ops.size());
+  c.tab_off = -1;  // no token tables unless a caller builds them (build_token_tables)
+  c.tab_tmax = 0;
+  c.tab_pmax = 0;
+  c.tab_stride = 0;
   for (std::size_t i = 0; i < ops.size(); ++i) {
     const auto& d = ops[i];
     SimOp& o = c.ops[i];
@@ -96,6 +102,73 @@ SimConfig make_sim_config(const ClusterConfig& cl, const EstimatorModel& est, in
   c.defer_threshold = static_cast<int32_t>(std::min<std::int64_t>(threshold, INT32_MAX));
   fill_sim_ops(c, ops, de);
   return c;
+}
+
+void build_token_tables(std::vector<SimConfig>& cfgs, const std::vector<SsgEstView>& ests,
+                        const std::vector<const DeviceEstimator*>& est_of,
+                        DeviceBuffer<double>& pool) {
+  if (cfgs.empty()) return;
+  auto& ctx = context();
+  cudaStream_t s = ctx.stream;
+  // table key: estimator + the op table (slot, count, payload, kvb, flop operands)
+  auto key_of = [](const SimConfig& c) {
+    std::string k(reinterpret_cast<const char*>(&c.est), sizeof c.est);
+    k.append(reinterpret_cast<const char*>(&c.nops), sizeof c.nops);
+    for (int i = 0; i < c.nops; ++i) {
+      SimOp o = c.ops[i];
+      o.qbytes = 0;
+      k.append(reinterpret_cast<const char*>(&o), sizeof o);
+    }
+    return k;
+  };
+  std::map<std::string, int32_t> table_of;
+  std::vector<SimConfig> reps;  // one representative per table
+  std::vector<int32_t> cap;
+  std::vector<int32_t> which(cfgs.size());
+  for (std::size_t i = 0; i < cfgs.size(); ++i) {
+    auto [it, fresh] = table_of.emplace(key_of(cfgs[i]), static_cast<int32_t>(reps.size()));
+    which[i] = it->second;
+    if (!fresh) continue;
+    // t can only be valid up to the smallest token-op bbox upper bound
+    double up = 1e18;
+    const DeviceEstimator& de = *est_of.at(cfgs[i].est);
+    for (int k = 0; k < cfgs[i].nops; ++k)
+      if (cfgs[i].ops[k].cls == SSG_CLS_TOKEN && cfgs[i].ops[k].slot >= 0)
+        up = std::min(up, de.host_models[cfgs[i].ops[k].slot].upper[0]);
+    cap.push_back(static_cast<int32_t>(std::min(up, 1.0e6)));
+    reps.push_back(cfgs[i]);
+  }
+  int32_t stride = 2;
+  for (auto c : cap) stride = std::max(stride, c + 1);
+  const int32_t n = static_cast<int32_t>(reps.size());
+  for (int32_t t = 0; t < n; ++t) {
+    reps[t].tab_off = static_cast<int64_t>(t) * 7 * stride;
+    reps[t].tab_stride = stride;
+  }
+  pool.resize(static_cast<std::size_t>(n) * 7 * stride);
+  DeviceBuffer<SimConfig> d_cfg;
+  DeviceBuffer<SsgEstView> d_est;
+  DeviceBuffer<uint8_t> d_valid(static_cast<std::size_t>(n) * stride);
+  d_cfg.upload(reps, s);
+  d_est.upload(ests, s);
+  launch_build_tables(d_cfg.ptr, n, stride, d_est.ptr, pool.ptr, d_valid.ptr, s);
+  std::vector<uint8_t> valid(static_cast<std::size_t>(n) * stride);
+  d_valid.download(valid.data(), valid.size(), s);
+  cuda_check(cudaStreamSynchronize(s), "token tables");
+  for (int32_t t = 0; t < n; ++t) {
+    int32_t tmax = 0, pmax = 0;
+    while (tmax + 1 < stride && (valid[static_cast<std::size_t>(t) * stride + tmax + 1] & 1)) ++tmax;
+    while (pmax + 1 < stride && (valid[static_cast<std::size_t>(t) * stride + pmax + 1] & 2)) ++pmax;
+    reps[t].tab_tmax = tmax;
+    reps[t].tab_pmax = std::min(pmax, tmax);
+  }
+  for (std::size_t i = 0; i < cfgs.size(); ++i) {
+    const SimConfig& r = reps[which[i]];
+    cfgs[i].tab_off = r.tab_tmax >= 1 ? r.tab_off : -1;
+    cfgs[i].tab_stride = r.tab_stride;
+    cfgs[i].tab_tmax = r.tab_tmax;
+    cfgs[i].tab_pmax = r.tab_pmax;
+  }
 }
 
 static int32_t pow2_above(int64_t n) {
@@ -208,6 +281,7 @@ void run_jobs(const SimJobs& J, SimResults& R, bool want_requests) {
   L.ws = d_ws.ptr;
   L.log = J.log_words > 0 ? d_log.ptr : nullptr;
   L.out = d_out.ptr;
+  L.tables = J.tables;
   cudaEvent_t ev0, ev1;
   cuda_check(cudaEventCreate(&ev0), "event");
   cuda_check(cudaEventCreate(&ev1), "event");
@@ -293,6 +367,7 @@ using namespace ssg;
 namespace {
 
 struct Placement {
+  DeviceBuffer<double> tables;
   SimJobs jobs;
   std::vector<std::pair<int32_t, int32_t>> where;  // trace index -> (unit, local)
   bool coupled = false;
@@ -309,6 +384,8 @@ Placement place(const ClusterConfig& cluster, const std::vector<Request>& trace,
   SimJobs& J = P.jobs;
   J.configs.push_back(make_sim_config(cluster, estimator, 0));
   J.ests.push_back(estimator.device().view);
+  build_token_tables(J.configs, J.ests, {&estimator.device()}, P.tables);
+  J.tables = P.tables.ptr;
   const int R = static_cast<int>(cluster.par.num_replicas);
   const std::size_t n = trace.size();
   std::vector<int32_t> ev(n);

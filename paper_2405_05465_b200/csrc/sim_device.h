@@ -51,7 +51,17 @@ struct SimConfig {
   int64_t block_size;
   int64_t total_units, watermark_units;
   double cpu_overhead;
-  int32_t nops, routing, defer_threshold, pad;
+  int32_t nops, routing, defer_threshold, tab_stride;  // tab_stride: entries per table array
+  // Token tables (predict_batch terms that depend only on the microbatch's
+  // token count t, precomputed by the same device code for t in [1, tab_tmax]):
+  //   S6[t] = fp64 sum of count*pred over the token-level ops, in op order
+  //   F6[t] = same for their flops;  C_k[t] = count*pred of the k-th comm op
+  //   P0[t], P0F[t] = prefill attention at n_eq = t with no prior context
+  // Layout at `tab_off` in the table pool: S6 | F6 | C0 | C1 | C2 | P0 | P0F,
+  // each tab_stride doubles.  tab_off < 0: no tables (full path).
+  int64_t tab_off;
+  int32_t tab_tmax;   // every token op and comm op is valid for t <= tab_tmax
+  int32_t tab_pmax;   // prefill attention at prior 0 is valid for n_eq <= tab_pmax
   SimOp ops[SSG_MAX_OPS];
 };
 
@@ -119,4 +129,5 @@ struct SimUnitOut {
   int64_t iterations; // batches executed (all replicas of the unit)
   int64_t entries;    // batch entries (prefill chunks + decodes)
   int64_t qbytes;     // algorithmic predictor bytes touched
+  int64_t cycles;     // SM clock cycles the unit's warp ran (diagnostics)
 };

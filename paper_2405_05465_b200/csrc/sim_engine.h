@@ -25,8 +25,14 @@ struct SimLaunch {
   int32_t* ws;
   int64_t* log;              // may be null
   SimUnitOut* out;
+  const double* tables;       // token tables pool, may be null
 };
 
 namespace ssg {
 void launch_simulate(const SimLaunch& L, cudaStream_t s);
+// Builds the token tables of `n` configs (cfgs[i].tab_off / tab_stride set by
+// the caller); valid[i*stride + t] gets bit0 = token/comm terms valid, bit1 =
+// prefill-at-prior-0 valid.
+void launch_build_tables(const SimConfig* d_cfgs, int32_t n, int32_t stride,
+                         const SsgEstView* d_ests, double* d_pool, uint8_t* d_valid, cudaStream_t s);
 }

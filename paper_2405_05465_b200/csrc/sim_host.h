@@ -33,6 +33,13 @@ void predict_batches_multi(const std::vector<SimConfig>& cfgs, const std::vector
                            const int64_t* d_ctx, double* seconds, double* flops,
                            std::vector<SimUnitOut>& status);
 
+// Token tables (SimConfig::tab_*) for `cfgs`: configs with equal operator
+// tables (same estimator, tp, pp) share one table.  Fills tab_off / stride /
+// tmax / pmax in place and leaves the pool in `pool` (device).
+void build_token_tables(std::vector<SimConfig>& cfgs, const std::vector<SsgEstView>& ests,
+                        const std::vector<const servesim::DeviceEstimator*>& est_of,
+                        DeviceBuffer<double>& pool);
+
 struct UnitSpec {
   int32_t config = 0;
   int32_t R = 1;
@@ -54,6 +61,7 @@ struct SimJobs {
   std::vector<int32_t> arr_order;
   int64_t ws_words = 0, nreps = 0, log_words = 0, emissions = 0;
   bool any_order = false;
+  const double* tables = nullptr;  // token tables pool (device), if built
 
   // Adds a unit over the given requests, which must already be in (arrival,
   // id) order; `event_order` (may be empty = identity) lists local indices in
