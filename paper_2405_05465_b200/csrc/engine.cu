@@ -372,6 +372,10 @@ __device__ void run_unit(Unit& U) {
   int32_t next_arrival = 0;
   int32_t rr_next = 0;
   int64_t events = 0;
+  // a lone replica (no deferred pool) keeps its scheduler state in registers
+  const bool reg1 = R == 1 && c.routing != SSG_ROUTE_DEFERRED;
+  RepState S1;
+  memset(&S1, 0, sizeof S1);
   while (true) {
     // ---- next event: (time, seq) argmin over the arrival head and replica slots
     double bt = INFINITY;
@@ -383,6 +387,19 @@ __device__ void run_unit(Unit& U) {
       bs = (uint64_t)next_arrival;
       bw = -1;
     }
+    if (R == 1) {
+      // one replica: its pending event vs the next arrival, no warp reduction
+      const RepState s0 = reg1 ? S1 : U.reps[0];
+      if (s0.ev_kind != 0) {
+        const double t = s0.ev_time;
+        const uint64_t q = s0.ev_seq;
+        if (t < bt || (t == bt && q < bs)) {
+          bt = t;
+          bs = q;
+          bw = 0;
+        }
+      }
+    } else
     for (int r0 = 0; r0 < R; r0 += 32) {
       const int r = r0 + U.lane;
       double t = INFINITY;
@@ -448,19 +465,25 @@ __device__ void run_unit(Unit& U) {
         if (failed(U)) break;
         continue;
       }
-      RepState S = load_rep(U, dest);
+      RepState S = reg1 ? S1 : load_rep(U, dest);
       const bool ok = enqueue(U, S, dest, j);
       if (ok) start_if_idle(U, S);
-      store_rep(U, dest, S);
+      if (reg1)
+        S1 = S;
+      else
+        store_rep(U, dest, S);
       if (!ok) break;
       continue;
     }
     const int r = bw;
-    RepState S = load_rep(U, r);
+    RepState S = reg1 ? S1 : load_rep(U, r);
     if (S.ev_kind == 1) {
       S.ev_kind = 0;
       const bool ok = batch_start(U, S, r);
-      store_rep(U, r, S);
+      if (reg1)
+        S1 = S;
+      else
+        store_rep(U, r, S);
       if (!ok) break;
     } else {
       // ---- BatchComplete (sim.hpp:284-293)
@@ -470,15 +493,23 @@ __device__ void run_unit(Unit& U) {
       S.nd = 0;
       S.busy = 0;
       if (failed(U)) {
-        store_rep(U, r, S);
+        if (reg1)
+          S1 = S;
+        else
+          store_rep(U, r, S);
         break;
       }
       start_if_idle(U, S);
-      store_rep(U, r, S);
-      drain_pool(U);
+      if (reg1) {
+        S1 = S;
+      } else {
+        store_rep(U, r, S);
+        drain_pool(U);
+      }
       if (failed(U)) break;
     }
   }
+  if (reg1) store_rep(U, 0, S1);
   if (U.lane == 0) {
     U.out->span = U.clock;
     U.out->events = events;

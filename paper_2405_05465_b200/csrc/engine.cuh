@@ -81,6 +81,13 @@ __device__ __forceinline__ void wput(const Unit& U, T* p, T v) {
   if (U.lane == 0) *p = v;
   __syncwarp();
 }
+// Several lane-0 stores under one pair of barriers.
+#define WSTORE_BEGIN(U) \
+  __syncwarp();         \
+  if ((U).lane == 0) {
+#define WSTORE_END \
+  }                \
+  __syncwarp();
 
 // ---------------------------------------------------------------- errors
 __device__ __forceinline__ void set_error(Unit& U, int code, int32_t i32, int64_t a, int64_t b,
@@ -100,7 +107,9 @@ __device__ __forceinline__ bool failed(Unit& U) { return U.out->code != SSG_OK; 
 
 // ---------------------------------------------------------------- blocks
 __device__ __forceinline__ int64_t units_for(const SimConfig& c, int64_t tokens) {
-  return c.token_granular ? tokens : (tokens + c.block_size - 1) / c.block_size;
+  if (c.token_granular) return tokens;
+  const int64_t t = tokens + c.block_size - 1;  // ceil(tokens / block_size), tokens >= 0
+  return c.bs_shift >= 0 ? (t >> c.bs_shift) : t / c.block_size;
 }
 __device__ __forceinline__ int64_t shortfall(const SimConfig& c, const ReqHot& h, int64_t tokens) {
   int64_t s = units_for(c, tokens) - (int64_t)h.held;
@@ -234,8 +243,11 @@ __device__ __forceinline__ bool prefill_complete(const ReqHot& h) { return h.don
 
 // mark_scheduled (scheduler.hpp:262-265)
 __device__ __forceinline__ void mark_scheduled(Unit& U, int32_t j) {
-  if (U.tm[j].first_sched < 0) wput(U, &U.tm[j].first_sched, U.clock);
-  wput(U, &U.hot[j].planned, U.serial);
+  const bool first = U.tm[j].first_sched < 0;
+  WSTORE_BEGIN(U)
+  if (first) U.tm[j].first_sched = U.clock;
+  U.hot[j].planned = U.serial;
+  WSTORE_END
 }
 
 // preempt_latest (scheduler.hpp:269-285): returns the victim or -1.
@@ -247,10 +259,13 @@ __device__ int32_t preempt_latest(Unit& U, RepState& S, int r) {
     run_erase_at(U, S, r, p);
     release(U, S, v);
     ReqHot& h = U.hot[v];
-    wput(U, &h.kv, 0);
-    wput(U, &h.done, 0);
-    wput(U, &h.target, h.prefill + h.emitted);
-    wput(U, &U.restarts[v], U.restarts[v] + 1);
+    const int32_t target = h.prefill + h.emitted, restarts = U.restarts[v] + 1;
+    WSTORE_BEGIN(U)
+    h.kv = 0;
+    h.done = 0;
+    h.target = target;
+    U.restarts[v] = restarts;
+    WSTORE_END
     S.preemptions += 1;
     wait_insert(U, S, r, v);  // victim was unfinished: outstanding unchanged
     return v;
@@ -284,9 +299,11 @@ __device__ bool admit_reserve(Unit& U, RepState& S, int r, int32_t j, int64_t ta
 
 __device__ __forceinline__ void push_prefill(Unit& U, RepState& S, int r, int32_t j, int32_t chunk,
                                              int32_t prior) {
-  wput(U, &P_IDX(U, r)[S.np], j);
-  wput(U, &P_CHUNK(U, r)[S.np], chunk);
-  wput(U, &P_PRIOR(U, r)[S.np], prior);
+  WSTORE_BEGIN(U)
+  P_IDX(U, r)[S.np] = j;
+  P_CHUNK(U, r)[S.np] = chunk;
+  P_PRIOR(U, r)[S.np] = prior;
+  WSTORE_END
   S.np += 1;
 }
 
@@ -366,8 +383,11 @@ __device__ void schedule_decodes(Unit& U, RepState& S, int r, int32_t max_entrie
       continue;
     }
     mark_scheduled(U, js);
-    wput(U, &D_IDX(U, r)[S.nd], js);
-    wput(U, &D_CTX(U, r)[S.nd], U.hot[js].kv + 1);
+    const int32_t ctx = U.hot[js].kv + 1;
+    WSTORE_BEGIN(U)
+    D_IDX(U, r)[S.nd] = js;
+    D_CTX(U, r)[S.nd] = ctx;
+    WSTORE_END
     S.nd += 1;
     if (budget) *budget -= 1;
     int32_t pos = 0;
@@ -548,14 +568,25 @@ __device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, doubl
         a5 += D_CTX(U, r)[k - S.np];
       }
     }
+    // 32-lane sums of values below 2^26 fit in 31 bits: one REDUX each
+    const bool small = ((a1 | a2 | a3 | a5) >> 26) == 0;
+    if (__all_sync(SSG_FULL, small)) {
+      a0 = __reduce_add_sync(SSG_FULL, (unsigned)a0);
+      a1 = __reduce_add_sync(SSG_FULL, (unsigned)a1);
+      a2 = __reduce_add_sync(SSG_FULL, (unsigned)a2);
+      a3 = __reduce_add_sync(SSG_FULL, (unsigned)a3);
+      a4 = __reduce_add_sync(SSG_FULL, (unsigned)a4);
+      a5 = __reduce_add_sync(SSG_FULL, (unsigned)a5);
+    } else {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      a0 += __shfl_xor_sync(SSG_FULL, a0, o);
-      a1 += __shfl_xor_sync(SSG_FULL, a1, o);
-      a2 += __shfl_xor_sync(SSG_FULL, a2, o);
-      a3 += __shfl_xor_sync(SSG_FULL, a3, o);
-      a4 += __shfl_xor_sync(SSG_FULL, a4, o);
-      a5 += __shfl_xor_sync(SSG_FULL, a5, o);
+      for (int o = 16; o > 0; o >>= 1) {
+        a0 += __shfl_xor_sync(SSG_FULL, a0, o);
+        a1 += __shfl_xor_sync(SSG_FULL, a1, o);
+        a2 += __shfl_xor_sync(SSG_FULL, a2, o);
+        a3 += __shfl_xor_sync(SSG_FULL, a3, o);
+        a4 += __shfl_xor_sync(SSG_FULL, a4, o);
+        a5 += __shfl_xor_sync(SSG_FULL, a5, o);
+      }
     }
     if (U.lane == 0) {
       st[m * 6 + 0] = a0;
@@ -586,13 +617,9 @@ __device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, doubl
     double pred = 0.0, fl = 0.0, v0 = 0.0, v1 = 0.0;
     int code = SSG_OK, bad = 0;
     bool active = false;
-    int op_index = 0;
-    if (m < pp) {
+    const int op_index = is_dec ? c.idx_dec : c.idx_pre;
+    if (m < pp && op_index >= 0) {
       const int64_t* s6 = st + m * 6;
-      for (int k = 0; k < nops; ++k) {
-        const SimOp& o = c.ops[k];
-        if (o.cls == SSG_CLS_SEQ && (o.flop_kind == 4) == is_dec) op_index = k;
-      }
       const SimOp& o = c.ops[op_index];
       if (s6[1] > 0 && !is_dec && s6[0] > 0) {
         active = true;
@@ -630,11 +657,7 @@ __device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, doubl
     for (int mm = 0; mm < pp; ++mm) {
       const int64_t* s6 = st + mm * 6;
       if (s6[1] == 0) continue;
-      for (int k = 0; k < nops; ++k) {
-        const SimOp& o = c.ops[k];
-        if (o.cls != SSG_CLS_SEQ || (o.flop_kind == 3 && s6[0] > 0) || (o.flop_kind == 4 && s6[4] > 0))
-          qb += o.qbytes;
-      }
+      qb += c.qb_fixed + (s6[0] > 0 ? c.qb_pre : 0) + (s6[4] > 0 ? c.qb_dec : 0);
     }
     U.qbytes += qb;
     for (int mm = 0; mm < pp; ++mm) {
@@ -657,9 +680,7 @@ __device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, doubl
           acc_s = __dadd_rn(acc_s, dd_pred);
           acc_f = __dadd_rn(acc_f, dd_fl);
         }
-        int k = 0;
-        for (int oi = 0; oi < nops; ++oi)
-          if (c.ops[oi].cls == SSG_CLS_COMM) acc_s = __dadd_rn(acc_s, tab[(int64_t)(2 + k++) * T1 + t]);
+        for (int k = 0; k < c.ncomm; ++k) acc_s = __dadd_rn(acc_s, tab[(int64_t)(2 + k) * T1 + t]);
       }
       if (U.lane == 0) {
         secs_part[mm] = acc_s;

@@ -23,6 +23,9 @@ void fill_sim_ops(SimConfig& c, const std::vector<OperatorDescriptor>& ops, cons
   c.tab_tmax = 0;
   c.tab_pmax = 0;
   c.tab_stride = 0;
+  c.idx_pre = c.idx_dec = -1;
+  c.ncomm = 0;
+  c.qb_fixed = c.qb_pre = c.qb_dec = 0;
   for (std::size_t i = 0; i < ops.size(); ++i) {
     const auto& d = ops[i];
     SimOp& o = c.ops[i];
@@ -61,6 +64,29 @@ void fill_sim_ops(SimConfig& c, const std::vector<OperatorDescriptor>& ops, cons
         break;
     }
   }
+  bool seen_seq = false, seen_comm = false;
+  for (int i = 0; i < c.nops; ++i) {
+    const SimOp& o = c.ops[i];
+    if (o.cls == SSG_CLS_TOKEN) {
+      internal_check(!seen_seq && !seen_comm, "operator table: token ops must come first");
+      c.qb_fixed += o.qbytes;
+    } else if (o.cls == SSG_CLS_SEQ) {
+      internal_check(!seen_comm, "operator table: attention before collectives");
+      seen_seq = true;
+      if (o.flop_kind == 3) {
+        c.idx_pre = i;
+        c.qb_pre = o.qbytes;
+      } else {
+        c.idx_dec = i;
+        c.qb_dec = o.qbytes;
+      }
+    } else {
+      seen_comm = true;
+      c.qb_fixed += o.qbytes;
+      c.ncomm += 1;
+    }
+  }
+  internal_check(c.ncomm <= 3, "operator table: more than three collectives");
 }
 
 SimConfig make_sim_config(const ClusterConfig& cl, const EstimatorModel& est, int32_t est_index,
@@ -94,6 +120,9 @@ SimConfig make_sim_config(const ClusterConfig& cl, const EstimatorModel& est, in
   c.tp = static_cast<int32_t>(cl.par.tp_degree);
   c.est = est_index;
   c.block_size = plan.block_size;
+  c.bs_shift = -1;
+  for (int k = 0; k < 62; ++k)
+    if ((int64_t(1) << k) == plan.block_size) c.bs_shift = k;
   c.total_units = c.token_granular ? plan.kv_capacity_tokens : plan.num_blocks;
   c.watermark_units = c.token_granular ? plan.watermark_blocks * plan.block_size : plan.watermark_blocks;
   c.cpu_overhead = cl.cpu_overhead_per_iter;

@@ -32,51 +32,65 @@ __device__ __forceinline__ int32_t ssg_node_right(double2 n) {
   return (int32_t)((unsigned long long)__double_as_longlong(n.y) >> 32);
 }
 
-// Multilinear interpolation, corner order and product order as regressor.hpp:326-340.
+// Cell of one axis: lo index and clamped fraction (regressor.hpp:314-325).
+__device__ __forceinline__ void ssg_axis_cell(const double* __restrict__ ax, int32_t n, double x,
+                                              int32_t* lo, double* frac) {
+  if (n == 1) {
+    *lo = 0;
+    *frac = 0.0;
+    return;
+  }
+  // std::upper_bound: first level strictly greater than x
+  int32_t first = 0, count = n;
+  while (count > 0) {
+    const int32_t step = count >> 1;
+    if (!(x < __ldg(ax + first + step))) {
+      first += step + 1;
+      count -= step + 1;
+    } else {
+      count = step;
+    }
+  }
+  const int32_t hi = first < 1 ? 1 : (first > n - 1 ? n - 1 : first);
+  *lo = hi - 1;
+  const double a = __ldg(ax + hi - 1), b = __ldg(ax + hi);
+  *frac = ssg_clamp((x - a) / (b - a), 0.0, 1.0);
+}
+
+// Multilinear interpolation (regressor.hpp:308-341), unrolled for the one- and
+// two-feature models the estimator trains.  Corner order (mask 0..2^nf-1),
+// weight product order (feature nf-1 down to 0, from 1.0) and the fp64
+// accumulation are the reference's, including its duplicated corner when an
+// axis has a single level.
 __device__ __forceinline__ double ssg_interp(const SsgEstView& E, const SsgModelDesc& m,
                                              double x0, double x1) {
-  int32_t lo[2] = {0, 0};
-  double frac[2] = {0.0, 0.0};
-  const int nf = m.nf;
-#pragma unroll
-  for (int f = 0; f < 2; ++f) {
-    if (f >= nf) break;
-    const int32_t n = m.axis_len[f];
-    if (n == 1) continue;
-    const double x = f ? x1 : x0;
-    const double* ax = E.dpool + m.axis_off[f];
-    // std::upper_bound: first level strictly greater than x
-    int32_t first = 0, count = n;
-    while (count > 0) {
-      int32_t step = count >> 1;
-      if (!(x < __ldg(ax + first + step))) {
-        first += step + 1;
-        count -= step + 1;
-      } else {
-        count = step;
-      }
-    }
-    int32_t hi = first < 1 ? 1 : (first > n - 1 ? n - 1 : first);
-    lo[f] = hi - 1;
-    const double a = __ldg(ax + lo[f]), b = __ldg(ax + hi);
-    frac[f] = ssg_clamp((x - a) / (b - a), 0.0, 1.0);
-  }
   const double* vals = E.dpool + m.values_off;
-  double acc = 0.0;
-  const int corners = 1 << nf;
-  for (int mask = 0; mask < corners; ++mask) {
-    double w = 1.0;
-    int64_t flat = 0, stride = 1;
-    for (int f = nf - 1; f >= 0; --f) {
-      const int32_t n = m.axis_len[f];
-      int high = (mask >> f) & 1;
-      if (n == 1) high = 0;
-      w = __dmul_rn(w, high ? frac[f] : __dsub_rn(1.0, frac[f]));
-      flat += (int64_t)(lo[f] + high) * stride;
-      stride *= n;
-    }
-    acc = __dadd_rn(acc, __dmul_rn(w, __ldg(vals + flat)));
+  int32_t lo0;
+  double f0;
+  const int32_t n0 = m.axis_len[0];
+  ssg_axis_cell(E.dpool + m.axis_off[0], n0, x0, &lo0, &f0);
+  const int32_t h0 = n0 == 1 ? 0 : 1;  // high corner offset along axis 0
+  const double g0 = __dsub_rn(1.0, f0);
+  if (m.nf == 1) {
+    // mask 0: w = 1 * (1 - f0); mask 1: w = 1 * f0
+    double acc = __dmul_rn(g0, __ldg(vals + lo0));
+    acc = __dadd_rn(acc, __dmul_rn(h0 ? f0 : g0, __ldg(vals + lo0 + h0)));
+    return acc;
   }
+  int32_t lo1;
+  double f1;
+  const int32_t n1 = m.axis_len[1];
+  ssg_axis_cell(E.dpool + m.axis_off[1], n1, x1, &lo1, &f1);
+  const int32_t h1 = n1 == 1 ? 0 : 1;
+  const double g1 = __dsub_rn(1.0, f1);
+  // flat = (lo0 + high0) * n1 + (lo1 + high1); weight = (1 * w1) * w0
+  const int64_t r0 = (int64_t)lo0 * n1, r1 = (int64_t)(lo0 + h0) * n1;
+  const double w1lo = g1, w1hi = h1 ? f1 : g1;
+  const double w0lo = g0, w0hi = h0 ? f0 : g0;
+  double acc = __dmul_rn(__dmul_rn(w1lo, w0lo), __ldg(vals + r0 + lo1));        // mask 0
+  acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(w1lo, w0hi), __ldg(vals + r1 + lo1)));  // mask 1
+  acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(w1hi, w0lo), __ldg(vals + r0 + lo1 + h1)));  // mask 2
+  acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(w1hi, w0hi), __ldg(vals + r1 + lo1 + h1)));  // mask 3
   return acc;
 }
 

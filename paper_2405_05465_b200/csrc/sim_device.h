@@ -62,6 +62,11 @@ struct SimConfig {
   int64_t tab_off;
   int32_t tab_tmax;   // every token op and comm op is valid for t <= tab_tmax
   int32_t tab_pmax;   // prefill attention at prior 0 is valid for n_eq <= tab_pmax
+  // derived once on the host (fill_sim_ops) so the per-batch path never scans ops
+  int32_t idx_pre, idx_dec;  // op indices of attention prefill / decode (-1 if absent)
+  int32_t ncomm, bs_shift;   // comm ops (<= 3); log2(block_size) if a power of two, else -1
+  int64_t qb_fixed;          // qbytes of token + comm ops (queried every non-empty microbatch)
+  int64_t qb_pre, qb_dec;    // qbytes of the attention queries
   SimOp ops[SSG_MAX_OPS];
 };
 
