@@ -186,9 +186,13 @@ int ssg_predict_mixed(const ssg_estimator* e, size_t n, const int32_t* slots, co
                       const double* f1, double* out, ssg_status* st) {
   return guarded(st, [&] {
     const auto& de = e->model.device();
-    for (size_t i = 0; i < n; ++i)
-      require(slots[i] >= 0 && slots[i] < de.view.nmodels,
-              "predict: query " + std::to_string(i) + " has no trained model slot");
+    bool needs_f1 = false;
+    for (size_t i = 0; i < n; ++i) {
+      if (slots[i] < 0 || slots[i] >= de.view.nmodels)  // message built only on failure
+        throw Error("predict: query " + std::to_string(i) + " has no trained model slot");
+      needs_f1 |= de.host_models[slots[i]].nf > 1;
+    }
+    require(f1 != nullptr || !needs_f1, "predict: two-feature models need f1");
     predict_host(e->model, n, slots, 0, f0, f1, out);
   });
 }

@@ -205,7 +205,9 @@ struct Candidate {
   std::string sim_error;
   CapacitySearchOptions copts;
   std::unordered_map<double, bool> memo;
-  bool done = false;
+  bool done = false;       // evaluation finished (capacity known, or failed)
+  bool measured = false;   // SLO / static run taken
+  int64_t probe_iters = 0; // longest probe unit so far (iterations): speculation budget
   ConfigResult res;
 };
 
@@ -214,7 +216,7 @@ struct SweepBuffers {
   DeviceBuffer<SimConfig> cfg;
   DeviceBuffer<SsgEstView> est;
   DeviceBuffer<SimUnit> units;
-  DeviceBuffer<ProbeDesc> probes;
+  DeviceBuffer<ProbeDesc> probes, mprobes;
   DeviceBuffer<int32_t> order, ws, restarts;
   DeviceBuffer<ReqHot> hot;
   DeviceBuffer<ReqTimes> tm;
@@ -234,6 +236,7 @@ struct ProbeLaunch {
   std::vector<SimUnit> units;
   std::vector<ProbeDesc> probes;
   std::vector<std::size_t> probe_cand;
+  std::vector<int32_t> measured;  // probe indices of full (measured) runs, slot order
   int64_t nreq = 0, ws_words = 0, nreps = 0;
 
   int32_t add_config(const Candidate& C) {
@@ -281,19 +284,29 @@ struct ProbeLaunch {
       u.abort_max_late = max_late;
       units.push_back(u);
     }
+    if (emis_base >= 0) measured.push_back(static_cast<int32_t>(probes.size()));
     probes.push_back(p);
     probe_cand.push_back(cand);
+  }
+  int64_t next_emis_base(int64_t per_probe) const {
+    return static_cast<int64_t>(measured.size()) * per_probe;
   }
 };
 
 // Runs a launch entirely on the device: request streams built from the resident
 // workload, simulation, and (measure) the SLO samples + their percentiles.
 // Returns the per-unit outputs; `sel` gets delay p99, TTFT p90, TBT p99 per probe.
-void run_launch(SweepBuffers& B, ProbeLaunch& L, const ResidentWorkload& w, bool emissions,
-                bool measure, std::vector<SimUnitOut>& out, std::vector<double>& sel) {
+// Runs a launch entirely on the device: request streams built from the resident
+// workload, simulation, and for the measured (full) runs the SLO samples and
+// their percentiles.  `sel` gets delay p99, TTFT p90, TBT p99 per measured run
+// (in L.measured order).
+void run_launch(SweepBuffers& B, ProbeLaunch& L, const ResidentWorkload& w,
+                std::vector<SimUnitOut>& out, std::vector<double>& sel) {
   auto& ctx = context();
   cudaStream_t s = ctx.stream;
   const int32_t np = static_cast<int32_t>(L.probes.size());
+  const int32_t nm = static_cast<int32_t>(L.measured.size());
+  const bool emissions = nm > 0;
   B.cfg.upload(L.configs, s);
   B.est.upload(L.ests, s);
   B.units.upload(L.units, s);
@@ -307,15 +320,13 @@ void run_launch(SweepBuffers& B, ProbeLaunch& L, const ResidentWorkload& w, bool
   B.out.resize(std::max<std::size_t>(1, L.units.size()));
   if (emissions) {
     B.emit_base.resize(std::max<int64_t>(1, L.nreq));
-    B.emis.resize(std::max<int64_t>(1, w.emis_per_probe * np));
+    B.emis.resize(std::max<int64_t>(1, w.emis_per_probe * nm));
   }
   // longest units first (fewest replicas share the trace => most requests per unit)
   std::vector<int32_t> order(L.units.size());
   for (std::size_t u = 0; u < order.size(); ++u) order[u] = static_cast<int32_t>(u);
-  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
-    if (L.units[a].n != L.units[b].n) return L.units[a].n > L.units[b].n;
-    return L.probes.empty() ? false : a < b;
-  });
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int32_t a, int32_t b) { return L.units[a].n > L.units[b].n; });
   B.order.upload(order, s);
   launch_probe_setup(B.probes.ptr, np, B.units.ptr, w, B.hot.ptr, B.tm.ptr, B.ids.ptr,
                      emissions ? B.emit_base.ptr : nullptr, s);
@@ -343,26 +354,28 @@ void run_launch(SweepBuffers& B, ProbeLaunch& L, const ResidentWorkload& w, bool
   cuda_check(cudaEventRecord(e0, s), "event");
   launch_simulate(K, s);
   cuda_check(cudaEventRecord(e1, s), "event");
-  if (measure) {
-    // samples: [delay | ttft] per probe (n each) then TBT gaps (emis_per_probe each)
+  if (emissions) {
+    // samples per measured run m: [delay | ttft] (n each), then TBT gaps (E each)
+    std::vector<ProbeDesc> mp;
+    for (int32_t k : L.measured) mp.push_back(L.probes[k]);
+    B.mprobes.upload(mp, s);
     const int64_t n = w.n, E = w.emis_per_probe;
-    B.samples.resize(std::max<int64_t>(1, np * (2 * n + E)));
+    B.samples.resize(std::max<int64_t>(1, nm * (2 * n + E)));
     double* delay = B.samples.ptr;
-    double* ttft = delay + np * n;
-    double* gaps = ttft + np * n;
-    launch_slo_samples(B.probes.ptr, np, B.units.ptr, B.tm.ptr, w, B.emis.ptr, delay, ttft, gaps, s);
+    double* ttft = delay + nm * n;
+    double* gaps = ttft + nm * n;
+    launch_slo_samples(B.mprobes.ptr, nm, B.units.ptr, B.tm.ptr, w, B.emis.ptr, delay, ttft, gaps, s);
     std::vector<int64_t> off;
     std::vector<SelectTask> tasks;
-    for (int32_t k = 0; k < np; ++k) off.push_back(k * n);                // delay segments
-    for (int32_t k = 0; k < np; ++k) off.push_back(np * n + k * n);       // ttft segments
-    for (int32_t k = 0; k < np; ++k) off.push_back(2 * np * n + k * E);   // tbt segments
-    off.push_back(2 * np * n + np * E);
-    // contiguous segments: segment s spans [off[s], off[s+1])
+    for (int32_t k = 0; k < nm; ++k) off.push_back(k * n);                // delay segments
+    for (int32_t k = 0; k < nm; ++k) off.push_back(nm * n + k * n);       // ttft segments
+    for (int32_t k = 0; k < nm; ++k) off.push_back(2 * nm * n + k * E);   // tbt segments
+    off.push_back(2 * nm * n + nm * E);
     const int64_t n_tbt = E - n;  // decode_tokens - 1 samples per request
-    for (int32_t k = 0; k < np; ++k) {
+    for (int32_t k = 0; k < nm; ++k) {
       tasks.push_back({k, nearest_rank_index(n, 0.99)});
-      tasks.push_back({np + k, nearest_rank_index(n, 0.90)});
-      tasks.push_back({2 * np + k, n_tbt > 0 ? nearest_rank_index(n_tbt, 0.99) : 0});
+      tasks.push_back({nm + k, nearest_rank_index(n, 0.90)});
+      tasks.push_back({2 * nm + k, n_tbt > 0 ? nearest_rank_index(n_tbt, 0.99) : 0});
     }
     B.seg_off.upload(off, s);
     B.tasks.upload(tasks, s);
@@ -410,61 +423,6 @@ void run_launch(SweepBuffers& B, ProbeLaunch& L, const ResidentWorkload& w, bool
   }
 }
 
-}  // namespace
-
-double initial_qps_guess(const ModelSpec& spec, const CandidateConfig& cand,
-                         const EstimatorModel& est, const ClusterConfig& cluster) {
-  auto ops = derive_operators(spec, cand.par);
-  SimConfig cfg{};
-  // predict's find() order over the two compositions (prefill: attn_decode is
-  // skipped before any lookup; decode: attn_prefill is)
-  for (int pass = 0; pass < 2; ++pass)
-    for (const auto& d : ops) {
-      if (pass == 0 && d.op == OpName::AttnDecode) continue;
-      if (pass == 1 && d.op == OpName::AttnPrefill) continue;
-      est.find(d.op, d.tp_degree);
-    }
-  fill_sim_ops(cfg, ops, est.device());
-  const std::int64_t len = std::min<std::int64_t>(512, spec.max_context);
-  const int64_t p_off[3] = {0, 1, 1}, d_off[3] = {0, 0, 1};
-  const int64_t p_len[1] = {len}, p_prior[1] = {0}, d_ctx[1] = {len};
-  double secs[2], fl[2];
-  predict_batches(est, cfg, 2, p_off, p_len, p_prior, d_off, d_ctx, secs, fl);
-  const double service = secs[0] + 64.0 * secs[1];
-  const double per_replica = 1.0 / std::max(service, 1e-9);
-  return std::max(1e-3, per_replica * static_cast<double>(cluster.par.num_replicas));
-}
-
-double find_capacity_replay(const std::function<bool(double)>& feasible,
-                            const CapacitySearchOptions& opts) {
-  std::unordered_map<double, bool> memo;
-  while (true) {
-    try {
-      return replay_capacity(memo, opts);
-    } catch (const NeedProbe& n) {
-      memo[n.q] = feasible(n.q);
-    }
-  }
-}
-
-// ------------------------------------------------------------------ the sweep
-namespace {
-
-struct SweepKnobs {
-  int ladder = 4;  // doubling / halving rates probed per round
-  int depth = 3;   // bisection levels probed per round (2^depth - 1 rates)
-};
-
-SweepKnobs knobs_from_env() {
-  SweepKnobs k;
-  if (const char* s = std::getenv("SSG_SPEC_LADDER")) k.ladder = std::max(1, std::atoi(s));
-  if (const char* s = std::getenv("SSG_SPEC_DEPTH")) k.depth = std::max(1, std::atoi(s));
-  return k;
-}
-
-// Runs one launch of probes; answers are written into the candidates' memos.
-// Errors inside a probe end that candidate's evaluation (as the reference's
-// exception would), unless the probe aborted first.
 int32_t max_late_of(std::size_t n) {
   return static_cast<int32_t>(n - static_cast<std::size_t>(std::ceil(0.99 * static_cast<double>(n))));
 }
@@ -487,37 +445,82 @@ void fail(Candidate& C, const SimUnitOut& o) {
   }
 }
 
-// One round of capacity probes; answers go into the candidates' memos.  An
-// error inside a probe ends that candidate's evaluation (the reference's
-// exception), unless the probe's abort came first in event order.
-void run_probe_round(SweepBuffers& B, std::vector<Candidate>& cands,
-                     const std::vector<std::size_t>& active,
-                     const std::vector<std::vector<double>>& rates, const ResidentWorkload& w,
-                     const CapacitySearchOptions& base) {
+struct SweepKnobs {
+  int ladder = 4;  // doubling rates probed per round
+  int depth = 3;   // bisection levels probed per round (2^depth - 1 rates)
+};
+
+SweepKnobs knobs_from_env() {
+  SweepKnobs k;
+  if (const char* s = std::getenv("SSG_SPEC_LADDER")) k.ladder = std::max(1, std::atoi(s));
+  if (const char* s = std::getenv("SSG_SPEC_DEPTH")) k.depth = std::max(1, std::atoi(s));
+  return k;
+}
+
+// Records a full run's SLO measurement (or an error) on its candidate.
+void take_measurement(Candidate& C, const std::vector<SimUnitOut>& out, const ProbeDesc& p,
+                      const double* sel3, const ResidentWorkload& w) {
+  if (const SimUnitOut* e = first_error(out, p)) {
+    fail(C, *e);
+    return;
+  }
+  C.res.delay_p99 = sel3[0];
+  C.res.ttft_p90 = sel3[1];
+  C.res.tbt_p99 = (w.emis_per_probe - w.n) > 0 ? sel3[2] : 0.0;  // summarize({}) -> 0
+  if (p.static_run) {
+    double span = 0.0;
+    const int nu = p.decoupled ? p.R : 1;
+    for (int u = p.first_unit; u < p.first_unit + nu; ++u) span = std::max(span, out[u].span);
+    C.res.makespan = span;
+  }
+  C.measured = true;
+}
+
+// One launch: capacity probes (answers into the candidates' memos) together
+// with the full runs of candidates whose capacity is already known (SLO
+// measurement at evaluation_fraction x capacity, or the static makespan run).
+// An error inside a probe ends that candidate's evaluation (the reference's
+// exception) unless the probe's abort came first in event order.
+void run_round(SweepBuffers& B, std::vector<Candidate>& cands,
+               const std::vector<std::pair<std::size_t, std::vector<double>>>& probes,
+               const std::vector<std::pair<std::size_t, double>>& full, bool static_run,
+               const ResidentWorkload& w, const CapacitySearchOptions& base) {
   const int32_t n = w.n;
   const int32_t max_late = max_late_of(static_cast<std::size_t>(n));
   ProbeLaunch L;
-  for (std::size_t a = 0; a < active.size(); ++a) {
-    const Candidate& C = cands[active[a]];
-    const int32_t ci = L.add_config(C);
-    for (double q : rates[a])
-      L.add_probe(active[a], C, ci, q, n, SSG_UF_ABORT, base.delay_p99_threshold, max_late, false,
+  for (const auto& [k, rates] : probes) {
+    const int32_t ci = L.add_config(cands[k]);
+    for (double q : rates)
+      L.add_probe(k, cands[k], ci, q, n, SSG_UF_ABORT, base.delay_p99_threshold, max_late, false,
                   false, -1);
   }
+  for (const auto& [k, q] : full) {
+    const int32_t ci = L.add_config(cands[k]);
+    L.add_probe(k, cands[k], ci, static_run ? 0.0 : q, n, SSG_UF_EMISSIONS, 0.0, 0, false,
+                static_run, L.next_emis_base(w.emis_per_probe));
+  }
+  if (L.probes.empty()) return;
   std::vector<SimUnitOut> out;
   std::vector<double> sel;
-  run_launch(B, L, w, false, false, out, sel);
+  run_launch(B, L, w, out, sel);
+  for (std::size_t m = 0; m < L.measured.size(); ++m) {
+    const ProbeDesc& p = L.probes[L.measured[m]];
+    take_measurement(cands[L.probe_cand[L.measured[m]]], out, p, sel.data() + 3 * m, w);
+  }
   ProbeLaunch redo;
   for (std::size_t k = 0; k < L.probes.size(); ++k) {
     const ProbeDesc& p = L.probes[k];
+    if (p.emis_base >= 0) continue;  // measured run, handled above
     Candidate& C = cands[L.probe_cand[k]];
-    int64_t late = 0;
+    int64_t late = 0, iters = 0;
     bool aborted = false;
     const int nu = p.decoupled ? p.R : 1;
     for (int u = p.first_unit; u < p.first_unit + nu; ++u) {
       late += out[u].late;
       aborted |= out[u].aborted != 0;
+      iters = std::max<int64_t>(iters, out[u].iterations);
     }
+    C.probe_iters = std::max(C.probe_iters, iters);
     const SimUnitOut* e = first_error(out, p);
     if (!e) {
       C.memo[p.qps] = !aborted && late <= max_late;
@@ -534,7 +537,7 @@ void run_probe_round(SweepBuffers& B, std::vector<Candidate>& cands,
     }
   }
   if (redo.probes.empty()) return;
-  run_launch(B, redo, w, false, false, out, sel);
+  run_launch(B, redo, w, out, sel);
   for (std::size_t k = 0; k < redo.probes.size(); ++k) {
     const ProbeDesc& p = redo.probes[k];
     Candidate& C = cands[redo.probe_cand[k]];
@@ -545,43 +548,6 @@ void run_probe_round(SweepBuffers& B, std::vector<Candidate>& cands,
       C.memo[p.qps] = o.late <= max_late;
     else
       fail(C, o);
-  }
-}
-
-// Full runs -- the SLO measurement at evaluation_fraction x capacity, or the
-// static makespan run -- of several candidates in one launch; their TTFT p90,
-// TBT p99 and delay p99 come from one segmented select on the device.
-void run_measurements(SweepBuffers& B, std::vector<Candidate>& cands,
-                      const std::vector<std::size_t>& which, const std::vector<double>& qps,
-                      const ResidentWorkload& w, bool static_run) {
-  if (which.empty()) return;
-  ProbeLaunch L;
-  for (std::size_t a = 0; a < which.size(); ++a) {
-    const Candidate& C = cands[which[a]];
-    const int32_t ci = L.add_config(C);
-    const int64_t emis_base = static_cast<int64_t>(a) * w.emis_per_probe;
-    L.add_probe(which[a], C, ci, static_run ? 0.0 : qps[a], w.n, SSG_UF_EMISSIONS, 0.0, 0, false,
-                static_run, emis_base);
-  }
-  std::vector<SimUnitOut> out;
-  std::vector<double> sel;
-  run_launch(B, L, w, true, true, out, sel);
-  for (std::size_t k = 0; k < L.probes.size(); ++k) {
-    const ProbeDesc& p = L.probes[k];
-    Candidate& C = cands[L.probe_cand[k]];
-    if (const SimUnitOut* e = first_error(out, p)) {
-      fail(C, *e);
-      continue;
-    }
-    C.res.delay_p99 = sel[3 * k + 0];
-    C.res.ttft_p90 = sel[3 * k + 1];
-    C.res.tbt_p99 = (w.emis_per_probe - w.n) > 0 ? sel[3 * k + 2] : 0.0;  // summarize({}) -> 0
-    if (static_run) {
-      double span = 0.0;
-      const int nu = p.decoupled ? p.R : 1;
-      for (int u = p.first_unit; u < p.first_unit + nu; ++u) span = std::max(span, out[u].span);
-      C.res.makespan = span;
-    }
   }
 }
 
@@ -802,12 +768,12 @@ std::vector<ConfigResult> SearchSession::evaluate(int shard, int num_shards) {
   }
 
   if (makespan) {
-    std::vector<std::size_t> ok;
+    std::vector<std::pair<std::size_t, double>> full;
     for (std::size_t k = 0; k < cands.size(); ++k)
-      if (!cands[k].done) ok.push_back(k);
-    run_measurements(B, cands, ok, {}, w, true);
-    for (auto k : ok) {
-      Candidate& C = cands[k];
+      if (!cands[k].done) full.push_back({k, 0.0});
+    run_round(B, cands, {}, full, true, w, opts.capacity);
+    for (const auto& f : full) {
+      Candidate& C = cands[f.first];
       if (!C.res.failed()) {
         C.res.slo_pass = true;
         C.res.qps_per_dollar = 0.0;
@@ -815,56 +781,61 @@ std::vector<ConfigResult> SearchSession::evaluate(int shard, int num_shards) {
     }
   } else {
     const SweepKnobs knobs = knobs_from_env();
-    // ---- capacity rounds
-    while (!live.empty()) {
-      std::vector<std::size_t> active;
-      std::vector<std::vector<double>> rates;
+    // Rounds: every live candidate's find_capacity is replayed; unanswered rates
+    // (plus speculative successors) become probes, and candidates whose
+    // capacity resolved get their SLO run in the same launch.
+    std::vector<std::size_t> to_measure;
+    while (true) {
+      std::vector<std::pair<std::size_t, std::vector<double>>> probes;
+      std::vector<std::pair<std::size_t, double>> full;
+      int64_t longest = 1;
+      for (auto k : live) longest = std::max(longest, cands[k].probe_iters);
       for (auto k : live) {
         Candidate& C = cands[k];
-        if (C.done) continue;
+        if (C.res.failed() || C.measured) continue;
+        if (!C.done) {
+          try {
+            C.res.capacity_qps = replay_capacity(C.memo, C.copts);
+            C.done = true;  // capacity known
+          } catch (const NeedProbe& need) {
+            // candidates on the critical path (longest probes) speculate deeper,
+            // so their bisection finishes in one round
+            const bool critical = C.probe_iters * 10 >= longest * 9;
+            std::vector<double> qs;
+            speculate(need, C.copts, knobs.ladder, critical ? knobs.depth + 3 : knobs.depth, qs);
+            std::vector<double> fresh;
+            for (double q : qs)
+              if (!C.memo.count(q) && std::find(fresh.begin(), fresh.end(), q) == fresh.end())
+                fresh.push_back(q);
+            probes.push_back({k, fresh});
+            continue;
+          } catch (const Error& e) {
+            C.res.error = e.what();
+            C.res.capacity_qps = 0.0;
+            C.done = true;
+            continue;
+          }
+        }
+        // capacity known: the SLO measurement run at evaluation_fraction of it
+        if (C.res.capacity_qps <= C.copts.min_qps) {
+          C.res.capacity_qps = 0.0;
+          C.res.error = "no feasible arrival rate (scheduling delay above threshold)";
+          continue;
+        }
+        const double q = opts.evaluation_fraction * C.res.capacity_qps;
         try {
-          const double cap = replay_capacity(C.memo, C.copts);
-          C.res.capacity_qps = cap;
-          C.done = true;  // capacity known
-        } catch (const NeedProbe& need) {
-          std::vector<double> qs;
-          speculate(need, C.copts, knobs.ladder, knobs.depth, qs);
-          std::vector<double> fresh;
-          for (double q : qs)
-            if (!C.memo.count(q) && std::find(fresh.begin(), fresh.end(), q) == fresh.end())
-              fresh.push_back(q);
-          active.push_back(k);
-          rates.push_back(fresh);
+          require(q > 0.0, "poisson_arrivals: rate must be positive");
         } catch (const Error& e) {
           C.res.error = e.what();
-          C.res.capacity_qps = 0.0;
-          C.done = true;
+          continue;
         }
+        full.push_back({k, q});
+        to_measure.push_back(k);
       }
-      if (active.empty()) break;
-      run_probe_round(B, cands, active, rates, w, opts.capacity);
-      std::vector<std::size_t> still;
-      for (auto k : active)
-        if (!cands[k].done) still.push_back(k);
-      live.swap(still);
+      if (probes.empty() && full.empty()) break;
+      run_round(B, cands, probes, full, false, w, opts.capacity);
     }
-    // ---- SLO runs at evaluation_fraction of capacity
-    std::vector<std::size_t> measure;
-    std::vector<double> eval_qps;
-    for (std::size_t k = 0; k < cands.size(); ++k) {
-      Candidate& C = cands[k];
-      if (C.res.failed()) continue;
-      if (C.res.capacity_qps <= C.copts.min_qps) {
-        C.res.capacity_qps = 0.0;
-        C.res.error = "no feasible arrival rate (scheduling delay above threshold)";
-        continue;
-      }
-      measure.push_back(k);
-      eval_qps.push_back(opts.evaluation_fraction * C.res.capacity_qps);
-    }
-    for (double q : eval_qps) require(q > 0.0, "poisson_arrivals: rate must be positive");
-    run_measurements(B, cands, measure, eval_qps, w, false);
-    for (auto k : measure) {
+    for (auto k : to_measure) {
       Candidate& C = cands[k];
       if (C.res.failed()) continue;
       C.res.slo_pass = C.res.ttft_p90 <= opts.slos.ttft_p90_max &&
