@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libssg.so")
+# SSG_LIB: an alternative build of the same library (A/B experiments only)
+LIB_PATH = os.environ.get("SSG_LIB") or os.path.join(_HERE, "libssg.so")
 
 OK, INPUT, INTERNAL, CUDA = 0, 1, 2, 3
 

@@ -11,7 +11,12 @@
 // is a warp-wide (time, seq) argmin over those slots.  RequestComplete events
 // are pure bookkeeping in the reference and are not materialised; seq stays
 // monotone in push order, which is all the ordering depends on.
+#include <cstdlib>
+
 #include "engine.cuh"
+#ifndef SSG_FFWD
+#define SSG_FFWD __noinline__
+#endif
 #include "runtime.h"
 #include "sim_engine.h"
 #include "sim_host.h"
@@ -32,7 +37,7 @@ __device__ __forceinline__ void store_rep(Unit& U, int r, const RepState& s) {
 }
 
 // ReplicaScheduler::enqueue (scheduler.hpp:146-155)
-__device__ bool enqueue(Unit& U, RepState& S, int r, int32_t j) {
+__device__ SSG_COLD bool enqueue(Unit& U, RepState& S, int r, int32_t j) {
   const SimConfig& c = *U.cfg;
   const ReqHot h = U.hot[j];
   const int64_t need = units_for(c, (int64_t)h.prefill + h.decode);
@@ -57,7 +62,7 @@ __device__ __forceinline__ void start_if_idle(Unit& U, RepState& S) {
 
 // Router::drain for the deferred policy (scheduler.hpp:532-551) followed by the
 // engine's enqueue + start_if_idle per assignment (sim.hpp:197-202).
-__device__ void drain_pool(Unit& U) {
+__device__ SSG_COLD void drain_pool(Unit& U) {
   const SimConfig& c = *U.cfg;
   if (c.routing != SSG_ROUTE_DEFERRED) return;
   int32_t* pool = POOL(U);
@@ -139,8 +144,7 @@ __device__ void complete_batch(Unit& U, RepState& S, int r) {
     set_error(U, SSG_ERR_INTERNAL, 4, 0, 0, 0.0);
     return;
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) newly_finished += __shfl_xor_sync(SSG_FULL, newly_finished, o);
+  newly_finished = (int)__reduce_add_sync(SSG_FULL, (unsigned)newly_finished);
   S.outstanding -= newly_finished;
   // release finished runners; drop them from running unless FT froze membership
   int32_t* a = RUN(U, r);
@@ -171,8 +175,7 @@ __device__ void complete_batch(Unit& U, RepState& S, int r) {
     }
     __syncwarp();
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) freed += __shfl_xor_sync(SSG_FULL, freed, o);
+  freed = warp_sum64(freed);
   S.allocated -= freed;
   if (!S.ft_inflight) {
     S.run_n = write;
@@ -185,6 +188,7 @@ __device__ void complete_batch(Unit& U, RepState& S, int r) {
 
 // One BatchStart event (sim.hpp:221-283).  Returns false when the unit must
 // stop (error or probe abort).
+template <int FMA, int FOREST>
 __device__ bool batch_start(Unit& U, RepState& S, int r) {
   const SimConfig& c = *U.cfg;
   U.serial += 1;
@@ -205,8 +209,7 @@ __device__ bool batch_start(Unit& U, RepState& S, int r) {
   }
   int32_t tokens = 0;
   for (int32_t k = U.lane; k < S.np; k += 32) tokens += P_CHUNK(U, r)[k];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) tokens += __shfl_xor_sync(SSG_FULL, tokens, o);
+  tokens = (int32_t)warp_sum64(tokens);
   tokens += S.nd;
   if (c.policy == SSG_POL_SARATHI && tokens > c.chunk) {
     set_error(U, SSG_ERR_INTERNAL, 5, tokens, 0, 0.0);  // sarathi: token budget exceeded
@@ -250,8 +253,7 @@ __device__ bool batch_start(Unit& U, RepState& S, int r) {
       const ReqTimes t = U.tm[j];
       if (t.first_sched == U.clock && U.clock - t.arrival > U.u->abort_thr) ++late;
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) late += __shfl_xor_sync(SSG_FULL, late, o);
+    late = (int)__reduce_add_sync(SSG_FULL, (unsigned)late);
     if (late) {
       const int total = U.out->late + late;
       wput(U, &U.out->late, total);
@@ -262,7 +264,7 @@ __device__ bool batch_start(Unit& U, RepState& S, int r) {
     }
   }
   double lat = 0.0, flops = 0.0;
-  if (batch_latency(U, S, r, &lat, &flops) != SSG_OK) return false;
+  if (batch_latency<FMA, FOREST>(U, S, r, &lat, &flops) != SSG_OK) return false;
   if (log_hdr >= 0) wput(U, &U.log[log_hdr + 5], (int64_t)__double_as_longlong(lat));
   S.busy_time = __dadd_rn(S.busy_time, lat);
   S.iterations += 1;
@@ -330,6 +332,228 @@ __global__ void k_build_tables(const SimConfig* __restrict__ cfgs, int32_t n, in
   valid[(int64_t)i * stride + t] = (ok_tok ? 1 : 0) | (ok_pre ? 2 : 0);
 }
 
+// ---------------------------------------------------------------- fast-forward
+// Pure-decode stretches of a lone replica (vLLM / Orca+ / LightLLM / Sarathi).
+// While nothing can change the batch -- no request waits (so admission cannot
+// run), every runner is past its prefill and stays unfinished, its block
+// shortfalls fit in free memory (so nothing is preempted), the token budget
+// covers one decode per runner, and no arrival lands before the batch
+// completes -- each reference iteration is: every runner decodes (in running
+// order), reserves kv+1 tokens, the batch costs predict_batch(...) and
+// completes one token per runner.  Within such a stretch nd is constant, so
+// the token-table terms, log1p(nd) and the interp cell along the batch-size
+// axis are loop invariants, and each microbatch's context sum grows by its
+// size per iteration.  The loop performs exactly the reference's steps on
+// those quantities; it stops *before* any iteration that would break a
+// condition (or raise) and hands it to the normal path, so every decision,
+// clock value and counter stays identical.  Returns iterations executed.
+template <int FMA>
+__device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, double next_arrival_time,
+                                              double* flops_acc) {
+  const SimConfig& c = *U.cfg;
+  const int nd = S.run_n, pp = c.pp;
+  const int nm = nd < pp ? nd : pp;  // non-empty microbatches
+  const int lane = U.lane;
+  const bool mine = lane < nd;
+  // runner state, one per lane (running order == decode entry order)
+  int32_t j = 0, kv = 0, held = 0, rem = 0x7fffffff;
+  if (mine) {
+    j = RUN(U, 0)[lane];
+    const ReqHot h = U.hot[j];
+    kv = h.kv;
+    held = h.held;
+    rem = (h.done < h.target) ? 0 : h.decode - h.emitted;
+  }
+  // iterations before any runner would finish (the finishing one is left to the normal path)
+  int min_rem = rem;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const int t = __shfl_xor_sync(SSG_FULL, min_rem, o);
+    min_rem = t < min_rem ? t : min_rem;
+  }
+  const int max_iters = min_rem - 1;
+  if (max_iters < 1) return 0;
+  // per-microbatch invariants on lane m < nm: size, context sum, decode model cell
+  const SimOp& od = c.ops[c.idx_dec];
+  const SsgModelDesc& md = U.E.models[od.slot];
+  if (md.kind != SSG_KIND_INTERP) return 0;
+  const int my_m = lane % pp;
+  int64_t ctx_m = 0;
+  for (int m = 0; m < nm; ++m) {
+    const int64_t cm = warp_sum64(mine && my_m == m ? (int64_t)kv + 1 : 0);
+    if (lane == m) ctx_m = cm;
+  }
+  const int nd_m = lane < nm ? (nd - lane + pp - 1) / pp : 0;
+  const double* tab = U.tables + c.tab_off;
+  const int T1 = c.tab_stride;
+  double tok_s = 0.0, tok_f = 0.0, comm_s[3] = {0.0, 0.0, 0.0};
+  int32_t lo0 = 0;
+  double f0 = 0.0;
+  bool ok = true;
+  if (lane < nm) {
+    tok_s = tab[nd_m];
+    tok_f = tab[(int64_t)T1 + nd_m];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      if (k < c.ncomm) comm_s[k] = tab[(int64_t)(2 + k) * T1 + nd_m];
+    const double v0 = (double)nd_m;
+    ok = v0 >= md.lower[0] && v0 <= md.upper[0];
+    ssg_axis_cell(U.E.dpool + md.axis_off[0], md.axis_len[0], ssg_log1p(v0, FMA), &lo0, &f0);
+  }
+  if (!__all_sync(SSG_FULL, ok)) return 0;
+  const int32_t n1 = md.axis_len[1];
+  const int32_t h0 = md.axis_len[0] == 1 ? 0 : 1;
+  const double g0 = __dsub_rn(1.0, f0);
+  const double w0lo = g0, w0hi = h0 ? f0 : g0;
+  const double* vals = U.E.dpool + md.values_off;
+  const double* ax1 = U.E.dpool + md.axis_off[1];
+  const int64_t r0 = (int64_t)lo0 * n1, r1 = (int64_t)(lo0 + h0) * n1;
+  const bool emit_times = (U.u->flags & SSG_UF_EMISSIONS) != 0;
+  const bool logging = (U.u->flags & SSG_UF_BATCH_LOG) != 0;
+  const double fa4 = od.fa;
+  int done = 0;
+  while (done < max_iters) {
+    // schedule: every runner reserves kv+1 tokens (must all fit: no preemption)
+    const int64_t need = mine ? shortfall_held(c, held, (int64_t)kv + 1) : 0;
+    const int64_t total_need = warp_sum64(need);
+    if (total_need > c.total_units - S.allocated) break;
+    // decode attention of microbatch m on lane m, then the operator-order sum
+    double acc = 0.0, fl = 0.0;
+    int good = 1;
+    if (lane < nm) {
+      const double v1 = __dmul_rn((double)ctx_m, od.kvb);
+      if (!(v1 >= md.lower[1] && v1 <= md.upper[1])) {
+        good = 0;
+      } else {
+        int32_t lo1;
+        double f1;
+        ssg_axis_cell(ax1, n1, ssg_log1p(v1, FMA), &lo1, &f1);
+        const int32_t h1 = n1 == 1 ? 0 : 1;
+        const double g1 = __dsub_rn(1.0, f1);
+        const double w1lo = g1, w1hi = h1 ? f1 : g1;
+        double r = __dmul_rn(__dmul_rn(w1lo, w0lo), __ldg(vals + r0 + lo1));
+        r = __dadd_rn(r, __dmul_rn(__dmul_rn(w1lo, w0hi), __ldg(vals + r1 + lo1)));
+        r = __dadd_rn(r, __dmul_rn(__dmul_rn(w1hi, w0lo), __ldg(vals + r0 + lo1 + h1)));
+        r = __dadd_rn(r, __dmul_rn(__dmul_rn(w1hi, w0hi), __ldg(vals + r1 + lo1 + h1)));
+        if (!ssg_exp_in_range(r)) {
+          good = 0;
+        } else {
+          const double pred = __dmul_rn(od.count, ssg_exp(r, FMA));
+          acc = __dadd_rn(tok_s, pred);
+#pragma unroll
+          for (int k = 0; k < 3; ++k)
+            if (k < c.ncomm) acc = __dadd_rn(acc, comm_s[k]);
+          const double ctx_tokens = v1 / od.kvb;
+          fl = __dadd_rn(tok_f, __dmul_rn(od.count, __dmul_rn(__dmul_rn(4.0, ctx_tokens), fa4)));
+          if (!(acc > 0.0)) good = 0;
+        }
+      }
+    }
+    if (!__all_sync(SSG_FULL, good)) break;  // the normal path raises it
+    // latency: pipeline makespan over the microbatches (all lanes, same values)
+    double lat, fl_tot;
+    if (pp == 1) {
+      lat = __shfl_sync(SSG_FULL, acc, 0);
+      fl_tot = __dmul_rn(__shfl_sync(SSG_FULL, fl, 0), (double)c.tp);
+    } else {
+      double fin[SSG_MAX_PP];
+      double tim[SSG_MAX_PP];
+      fl_tot = 0.0;
+#pragma unroll
+      for (int m = 0; m < SSG_MAX_PP; ++m) {
+        tim[m] = __shfl_sync(SSG_FULL, acc, m);
+        const double fm = __shfl_sync(SSG_FULL, fl, m);
+        fin[m] = 0.0;
+        if (m < nm) fl_tot = __dadd_rn(fl_tot, __dmul_rn(fm, (double)(c.tp * c.pp)));
+      }
+      for (int st = 0; st < pp; ++st) {
+        double prev = 0.0;
+#pragma unroll
+        for (int m = 0; m < SSG_MAX_PP; ++m) {
+          if (m < nm) {
+            const double start = fin[m] < prev ? prev : fin[m];
+            prev = __dadd_rn(start, tim[m]);
+            fin[m] = prev;
+          }
+        }
+      }
+      lat = 0.0;
+#pragma unroll
+      for (int m = 0; m < SSG_MAX_PP; ++m)
+        if (m == nm - 1) lat = fin[m];
+    }
+    lat = __dadd_rn(lat, c.cpu_overhead);
+    if (!(lat > 0.0)) break;
+    const double t_done = __dadd_rn(U.clock, lat);
+    // an arrival at or before this completion is processed between the batch's
+    // start and completion events: that iteration belongs to the event loop
+    if (next_arrival_time <= t_done) break;
+    // ---- the iteration happens
+    U.serial += 1;
+    held += (int32_t)need;
+    S.allocated += total_need;
+    if (logging) {
+      const int64_t need_w = 6 + 2LL * nd;
+      const int64_t used = U.out->log_used;
+      if (used >= 0 && used + need_w <= U.u->log_cap) {
+        int64_t* L = U.log + used;
+        if (lane == 0) {
+          L[0] = 0;
+          L[1] = __double_as_longlong(U.clock);
+          L[2] = S.allocated;
+          L[3] = 0;
+          L[4] = nd;
+          L[5] = __double_as_longlong(lat);
+        }
+        if (mine) {
+          L[6 + 2 * lane] = U.ids[j];
+          L[7 + 2 * lane] = kv + 1;
+        }
+        wput(U, &U.out->log_used, used + need_w);
+      } else {
+        wput(U, &U.out->log_used, (int64_t)-1);
+      }
+    }
+    S.busy_time = __dadd_rn(S.busy_time, lat);
+    S.iterations += 1;
+    S.tokens += nd;
+    const double util = (double)S.allocated / (double)c.total_units;
+    S.peak_kv = S.peak_kv < util ? util : S.peak_kv;
+    *flops_acc = __dadd_rn(*flops_acc, fl_tot);
+    U.iters += 1;
+    U.entries += nd;
+    U.qbytes += (int64_t)nm * (c.qb_fixed + c.qb_dec);
+    kv += 1;
+    if (mine && emit_times) U.emissions[U.emit_base[j] + (U.hot[j].decode - rem) + done] = t_done;
+    ctx_m += nd_m;
+    U.clock = t_done;
+    ++done;
+  }
+  if (done > 0 && mine) {
+    ReqHot& h = U.hot[j];
+    h.kv = kv;
+    h.held = held;
+    h.emitted = h.emitted + done;
+  }
+  __syncwarp();
+  return done;
+}
+
+template <int FMA>
+__device__ SSG_FFWD int fast_forward(Unit& U, RepState& S, double next_arrival_time,
+                                     double* flops_acc) {
+  const SimConfig& c = *U.cfg;
+  if (c.policy != SSG_POL_VLLM && c.policy != SSG_POL_ORCA && c.policy != SSG_POL_LIGHTLLM &&
+      c.policy != SSG_POL_SARATHI)
+    return 0;
+  if (S.wait_n != 0 || S.run_n < 1 || S.run_n > 32 || c.tab_off < 0 || c.idx_dec < 0) return 0;
+  const int nd = S.run_n, pp = c.pp;
+  if (c.policy == SSG_POL_SARATHI ? nd > c.chunk : nd > c.max_tokens) return 0;
+  if (nd > c.max_batch || (nd + pp - 1) / pp > c.tab_tmax) return 0;
+  return fast_forward_t<FMA>(U, S, next_arrival_time, flops_acc);
+}
+
+template <int FMA, int FOREST>
 __device__ void run_unit(Unit& U) {
   const long long t_start = clock64();
   const SimUnit& u = *U.u;
@@ -372,8 +596,11 @@ __device__ void run_unit(Unit& U) {
   int32_t next_arrival = 0;
   int32_t rr_next = 0;
   int64_t events = 0;
+  double next_arrival_time =
+      u.n > 0 ? U.tm[U.arr_order ? U.arr_order[0] : 0].arrival : INFINITY;
   // a lone replica (no deferred pool) keeps its scheduler state in registers
   const bool reg1 = R == 1 && c.routing != SSG_ROUTE_DEFERRED;
+  const bool fast_ok = reg1 && U.fast;
   RepState S1;
   memset(&S1, 0, sizeof S1);
   while (true) {
@@ -382,8 +609,7 @@ __device__ void run_unit(Unit& U) {
     uint64_t bs = ~0ull;
     int bw = -2;  // -1 arrival, r >= 0 replica
     if (next_arrival < u.n) {
-      const int32_t j = U.arr_order ? U.arr_order[next_arrival] : next_arrival;
-      bt = U.tm[j].arrival;
+      bt = next_arrival_time;
       bs = (uint64_t)next_arrival;
       bw = -1;
     }
@@ -437,6 +663,8 @@ __device__ void run_unit(Unit& U) {
       // ---- Arrival: route, enqueue, start_if_idle (sim.hpp:211-220)
       const int32_t j = U.arr_order ? U.arr_order[next_arrival] : next_arrival;
       ++next_arrival;
+      if (next_arrival < u.n)
+        next_arrival_time = U.tm[U.arr_order ? U.arr_order[next_arrival] : next_arrival].arrival;
       int dest = 0;
       if (c.routing == SSG_ROUTE_RR) {
         dest = rr_next;
@@ -477,9 +705,23 @@ __device__ void run_unit(Unit& U) {
     }
     const int r = bw;
     RepState S = reg1 ? S1 : load_rep(U, r);
+    if (S.ev_kind == 1 && reg1 && fast_ok) {
+      // pure-decode stretch: iterations that end at the same state the event
+      // loop would reach; afterwards the replica is again "BatchStart at clock"
+      double fl = U.out->flops;
+      const int k = fast_forward<FMA>(U, S, next_arrival_time, &fl);
+      if (k > 0) {
+        wput(U, &U.out->flops, fl);
+        events += 2 * k;
+        S.ev_time = U.clock;
+        S.ev_seq = U.seq++;
+        S1 = S;
+        continue;
+      }
+    }
     if (S.ev_kind == 1) {
       S.ev_kind = 0;
-      const bool ok = batch_start(U, S, r);
+      const bool ok = batch_start<FMA, FOREST>(U, S, r);
       if (reg1)
         S1 = S;
       else
@@ -535,6 +777,7 @@ __device__ void run_unit(Unit& U) {
   }
 }
 
+template <int FMA, int FOREST>
 __global__ void __launch_bounds__(SSG_SIM_WARPS * 32)
     k_simulate(SimLaunch L) {
   __shared__ int64_t stats[SSG_SIM_WARPS][SSG_MAX_PP * 6];
@@ -569,17 +812,19 @@ __global__ void __launch_bounds__(SSG_SIM_WARPS * 32)
   U.smem_stats = stats[wib];
   U.smem_part = part[wib];
   U.tables = L.tables;
+  U.fast = L.fast_forward;
   U.group_late = nullptr;
   U.lane = threadIdx.x & 31;
   U.MB = U.cfg->max_batch;
   U.WC = U.u->wait_cap;
   U.rep_stride = 6LL * U.MB + U.WC;
-  run_unit(U);
+  run_unit<FMA, FOREST>(U);
 }
 
 // predict_batch / batch_device_flops for standalone compositions (the
 // estimator.hpp:294-380 API): one warp per composition, same device code path
 // as the engine's per-iteration latency.
+template <int FMA>
 __global__ void __launch_bounds__(SSG_SIM_WARPS * 32)
     k_predict_batch(const SimConfig* cfgs, const SsgEstView* ests, const int32_t* comp_cfg,
                     int64_t n, int32_t MB, int32_t* ws, const int32_t* np_nd, double* seconds,
@@ -618,7 +863,7 @@ __global__ void __launch_bounds__(SSG_SIM_WARPS * 32)
   S.np = np_nd[2 * c];
   S.nd = np_nd[2 * c + 1];
   double lat = 0.0, fl = 0.0;
-  if (batch_latency(U, S, 0, &lat, &fl) == SSG_OK && U.lane == 0) {
+  if (batch_latency<FMA, 1>(U, S, 0, &lat, &fl) == SSG_OK && U.lane == 0) {
     seconds[c] = lat;
     flops[c] = fl;
   }
@@ -637,10 +882,24 @@ void launch_build_tables(const SimConfig* d_cfgs, int32_t n, int32_t stride,
   stats().launches_setup += 1;
 }
 
+int fast_forward_enabled() {
+  static const int on = std::getenv("SSG_NO_FASTFWD") == nullptr ? 1 : 0;
+  return on;
+}
+
 void launch_simulate(const SimLaunch& L, cudaStream_t s) {
   if (L.nunits <= 0) return;
   const int64_t blocks = (L.nunits + SSG_SIM_WARPS - 1) / SSG_SIM_WARPS;
-  ssgk::k_simulate<<<(unsigned)blocks, SSG_SIM_WARPS * 32, 0, s>>>(L);
+  // one instantiation per glibc variant x (interp-only | with forests)
+  const int fma = context().math_fma;
+  if (fma && L.has_forest)
+    ssgk::k_simulate<1, 1><<<(unsigned)blocks, SSG_SIM_WARPS * 32, 0, s>>>(L);
+  else if (fma)
+    ssgk::k_simulate<1, 0><<<(unsigned)blocks, SSG_SIM_WARPS * 32, 0, s>>>(L);
+  else if (L.has_forest)
+    ssgk::k_simulate<0, 1><<<(unsigned)blocks, SSG_SIM_WARPS * 32, 0, s>>>(L);
+  else
+    ssgk::k_simulate<0, 0><<<(unsigned)blocks, SSG_SIM_WARPS * 32, 0, s>>>(L);
   cuda_check(cudaGetLastError(), "k_simulate launch");
 }
 
@@ -709,9 +968,14 @@ void predict_batches_multi(const std::vector<SimConfig>& cfgs_in, const std::vec
   d_fl.resize(n);
   d_out.resize(n);
   const int64_t blocks = (n + SSG_SIM_WARPS - 1) / SSG_SIM_WARPS;
-  ssgk::k_predict_batch<<<(unsigned)blocks, SSG_SIM_WARPS * 32, 0, s>>>(
-      d_cfg.ptr, d_est.ptr, d_cc.ptr, n, static_cast<int32_t>(MB), d_ws.ptr, d_npnd.ptr, d_sec.ptr,
-      d_fl.ptr, d_out.ptr);
+  if (context().math_fma)
+    ssgk::k_predict_batch<1><<<(unsigned)blocks, SSG_SIM_WARPS * 32, 0, s>>>(
+        d_cfg.ptr, d_est.ptr, d_cc.ptr, n, static_cast<int32_t>(MB), d_ws.ptr, d_npnd.ptr, d_sec.ptr,
+        d_fl.ptr, d_out.ptr);
+  else
+    ssgk::k_predict_batch<0><<<(unsigned)blocks, SSG_SIM_WARPS * 32, 0, s>>>(
+        d_cfg.ptr, d_est.ptr, d_cc.ptr, n, static_cast<int32_t>(MB), d_ws.ptr, d_npnd.ptr, d_sec.ptr,
+        d_fl.ptr, d_out.ptr);
   cuda_check(cudaGetLastError(), "k_predict_batch launch");
   stats().launches_batch += 1;
   d_out.download(status.data(), n, s);

@@ -26,6 +26,16 @@
 
 #define SSG_FULL 0xffffffffu
 
+// Code-placement knobs (the simulation kernel is instruction-fetch bound):
+// SSG_COLD marks rarely executed scheduler paths, SSG_WARM the per-policy
+// schedulers.  Each expands to __noinline__ or __forceinline__ at build time.
+#ifndef SSG_COLD
+#define SSG_COLD __noinline__
+#endif
+#ifndef SSG_WARM
+#define SSG_WARM __forceinline__
+#endif
+
 namespace ssgk {
 
 struct Unit {
@@ -47,6 +57,7 @@ struct Unit {
   const double* tables; // token tables pool (SimConfig::tab_off)
   double* smem_part;    // per-warp shared scratch [4 * SSG_MAX_PP]
   int* group_late;  // shared by the probe's units (may be null)
+  int fast;         // pure-decode fast-forward enabled
   int lane;
   int64_t rep_stride;  // int32 words per replica in ws
   int32_t MB, WC;
@@ -89,8 +100,17 @@ __device__ __forceinline__ void wput(const Unit& U, T* p, T v) {
   }                \
   __syncwarp();
 
+// Warp sum of non-negative 64-bit values: one REDUX when every lane's value is
+// below 2^26 (the 32-lane total then fits 31 bits), else a shuffle tree.
+__device__ __forceinline__ int64_t warp_sum64(int64_t v) {
+  if (__all_sync(SSG_FULL, (v >> 26) == 0)) return (int64_t)__reduce_add_sync(SSG_FULL, (unsigned)v);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(SSG_FULL, v, o);
+  return v;
+}
+
 // ---------------------------------------------------------------- errors
-__device__ __forceinline__ void set_error(Unit& U, int code, int32_t i32, int64_t a, int64_t b,
+__device__ SSG_COLD void set_error(Unit& U, int code, int32_t i32, int64_t a, int64_t b,
                                           double f) {
   __syncwarp();
   if (U.lane == 0 && U.out->code == SSG_OK) {
@@ -110,6 +130,10 @@ __device__ __forceinline__ int64_t units_for(const SimConfig& c, int64_t tokens)
   if (c.token_granular) return tokens;
   const int64_t t = tokens + c.block_size - 1;  // ceil(tokens / block_size), tokens >= 0
   return c.bs_shift >= 0 ? (t >> c.bs_shift) : t / c.block_size;
+}
+__device__ __forceinline__ int64_t shortfall_held(const SimConfig& c, int32_t held, int64_t tokens) {
+  int64_t s = units_for(c, tokens) - (int64_t)held;
+  return s > 0 ? s : 0;
 }
 __device__ __forceinline__ int64_t shortfall(const SimConfig& c, const ReqHot& h, int64_t tokens) {
   int64_t s = units_for(c, tokens) - (int64_t)h.held;
@@ -175,7 +199,7 @@ __device__ __forceinline__ int32_t ring_upper(const int32_t* a, int32_t mask, in
 }
 
 // insert_sorted(waiting_, r) (scheduler.hpp:243-247)
-__device__ void wait_insert(Unit& U, RepState& S, int r, int32_t j) {
+__device__ SSG_COLD void wait_insert(Unit& U, RepState& S, int r, int32_t j) {
   int32_t* w = WAIT(U, r);
   const int32_t mask = U.WC - 1;
   int32_t pos;
@@ -195,7 +219,7 @@ __device__ void wait_insert(Unit& U, RepState& S, int r, int32_t j) {
 
 // erase_from_waiting (scheduler.hpp:474-478); the queue is sorted, so the
 // element's position is its lower bound.
-__device__ void wait_erase(Unit& U, RepState& S, int r, int32_t j) {
+__device__ SSG_COLD void wait_erase(Unit& U, RepState& S, int r, int32_t j) {
   int32_t* w = WAIT(U, r);
   const int32_t mask = U.WC - 1;
   int32_t pos = ring_upper(w, mask, S.wait_head, S.wait_n, j - 1);
@@ -218,7 +242,7 @@ __device__ __forceinline__ int32_t wait_front(Unit& U, const RepState& S, int r)
 }
 
 // insert_sorted_running (scheduler.hpp:249-252)
-__device__ void run_insert(Unit& U, RepState& S, int r, int32_t j) {
+__device__ SSG_COLD void run_insert(Unit& U, RepState& S, int r, int32_t j) {
   int32_t* a = RUN(U, r);
   int32_t pos;
   if (S.run_n == 0 || a[S.run_n - 1] < j)
@@ -230,7 +254,7 @@ __device__ void run_insert(Unit& U, RepState& S, int r, int32_t j) {
   S.run_n += 1;
 }
 
-__device__ void run_erase_at(Unit& U, RepState& S, int r, int32_t pos) {
+__device__ SSG_COLD void run_erase_at(Unit& U, RepState& S, int r, int32_t pos) {
   int32_t* a = RUN(U, r);
   ring_shift(U, a, 0x7fffffff, 0, pos + 1, S.run_n, -1);
   S.run_n -= 1;
@@ -251,7 +275,7 @@ __device__ __forceinline__ void mark_scheduled(Unit& U, int32_t j) {
 }
 
 // preempt_latest (scheduler.hpp:269-285): returns the victim or -1.
-__device__ int32_t preempt_latest(Unit& U, RepState& S, int r) {
+__device__ SSG_COLD int32_t preempt_latest(Unit& U, RepState& S, int r) {
   int32_t* a = RUN(U, r);
   for (int32_t p = S.run_n - 1; p >= 0; --p) {
     const int32_t v = a[p];
@@ -274,7 +298,7 @@ __device__ int32_t preempt_latest(Unit& U, RepState& S, int r) {
 }
 
 // ensure_decode_memory (scheduler.hpp:290-296)
-__device__ bool ensure_decode_memory(Unit& U, RepState& S, int r, int32_t j) {
+__device__ SSG_COLD bool ensure_decode_memory(Unit& U, RepState& S, int r, int32_t j) {
   while (!try_reserve(U, S, j, (int64_t)U.hot[j].kv + 1)) {
     const int32_t victim = preempt_latest(U, S, r);
     if (victim < 0 || victim == j) return false;
@@ -283,7 +307,7 @@ __device__ bool ensure_decode_memory(Unit& U, RepState& S, int r, int32_t j) {
 }
 
 // admit_reserve (scheduler.hpp:302-316)
-__device__ bool admit_reserve(Unit& U, RepState& S, int r, int32_t j, int64_t target,
+__device__ SSG_COLD bool admit_reserve(Unit& U, RepState& S, int r, int32_t j, int64_t target,
                               bool allow_preempt, bool use_watermark) {
   const SimConfig& c = *U.cfg;
   while (true) {
@@ -335,12 +359,23 @@ __device__ void schedule_decodes(Unit& U, RepState& S, int r, int32_t max_entrie
       continue;
     }
     // exclusive count of eligible entries before this lane; inclusive need sum
+    // (32-bit scan when every need is small -- the common case: 0 or 1 block)
     const int before = __popc(em & ((1u << U.lane) - 1u));
     int64_t incl = need;
+    if (__all_sync(SSG_FULL, need < (1 << 25))) {
+      int32_t inc32 = (int32_t)need;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int64_t t = __shfl_up_sync(SSG_FULL, incl, o);
-      if (U.lane >= o) incl += t;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t t = __shfl_up_sync(SSG_FULL, inc32, o);
+        if (U.lane >= o) inc32 += t;
+      }
+      incl = inc32;
+    } else {
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t t = __shfl_up_sync(SSG_FULL, incl, o);
+        if (U.lane >= o) incl += t;
+      }
     }
     const int32_t batch0 = S.np + S.nd;
     const int64_t free0 = c.total_units - S.allocated;
@@ -397,7 +432,7 @@ __device__ void schedule_decodes(Unit& U, RepState& S, int r, int32_t max_entrie
   }
 }
 
-__device__ void schedule_vllm(Unit& U, RepState& S, int r) {
+__device__ SSG_WARM void schedule_vllm(Unit& U, RepState& S, int r) {
   const SimConfig& c = *U.cfg;
   int32_t budget = c.max_tokens;
   while (S.wait_n > 0 && S.run_n < c.max_batch) {
@@ -419,7 +454,7 @@ __device__ void schedule_vllm(Unit& U, RepState& S, int r) {
   schedule_decodes(U, S, r, c.max_batch, nullptr);
 }
 
-__device__ void schedule_orca(Unit& U, RepState& S, int r) {
+__device__ SSG_WARM void schedule_orca(Unit& U, RepState& S, int r) {
   const SimConfig& c = *U.cfg;
   int32_t budget = c.max_tokens;
   while (S.wait_n > 0 && S.run_n < c.max_batch) {
@@ -444,7 +479,7 @@ __device__ void schedule_orca(Unit& U, RepState& S, int r) {
 // First position >= i of the running queue whose request matches `pred`
 // (warp-parallel 32-entry windows); run_n if none.
 #define PRED_PREFILL_LEFT 0
-__device__ int32_t next_running(Unit& U, const RepState& S, int r, int32_t i, int pred) {
+__device__ SSG_WARM int32_t next_running(Unit& U, const RepState& S, int r, int32_t i, int pred) {
   const int32_t* a = RUN(U, r);
   for (; i < S.run_n; i += 32) {
     const int32_t p = i + U.lane;
@@ -459,7 +494,7 @@ __device__ int32_t next_running(Unit& U, const RepState& S, int r, int32_t i, in
   return S.run_n;
 }
 
-__device__ void schedule_sarathi(Unit& U, RepState& S, int r) {
+__device__ SSG_WARM void schedule_sarathi(Unit& U, RepState& S, int r) {
   const SimConfig& c = *U.cfg;
   int32_t budget = c.chunk;
   schedule_decodes(U, S, r, c.max_batch, &budget);
@@ -493,7 +528,7 @@ __device__ void schedule_sarathi(Unit& U, RepState& S, int r) {
   __syncwarp();
 }
 
-__device__ void schedule_ft(Unit& U, RepState& S, int r) {
+__device__ SSG_COLD void schedule_ft(Unit& U, RepState& S, int r) {
   const SimConfig& c = *U.cfg;
   if (!S.ft_inflight) {
     while (S.wait_n > 0 && S.run_n < c.max_batch) {
@@ -547,6 +582,107 @@ __device__ void schedule_ft(Unit& U, RepState& S, int r) {
 // (scheduler.hpp:566-579).  Per-entry sums are integer (exact in any order);
 // the per-operator predictions run one per lane and are then added strictly
 // in operator order, microbatch by microbatch, as the reference does.
+// The generic per-(microbatch, op) evaluation for batches outside the token
+// tables' range (or configs without tables): one lane per task, operator-order
+// accumulation.  Out of line -- it is the cold path of batch_latency.
+template <int FMA, int FOREST>
+__device__ SSG_COLD void batch_latency_full(Unit& U, const int64_t* st, int& err, int& err_task,
+                                                int& err_feat, double& err_val, int64_t& qb) {
+  const SimConfig& c = *U.cfg;
+  const int pp = c.pp;
+  const int nops = c.nops;
+  double* secs_part = U.smem_part;
+  double* flop_part = U.smem_part + SSG_MAX_PP;
+  const int work = pp * nops;
+  double acc_s = 0.0, acc_f = 0.0;
+  int cur_m = 0;
+  for (int base = 0; base < work; base += 32) {
+    const int t = base + U.lane;
+    double pred = 0.0, fl = 0.0, v0 = 0.0, v1 = 0.0;
+    bool active = false;
+    int code = SSG_OK, bad = 0;
+    if (t < work) {
+      const int m = t / nops;
+      const SimOp& o = c.ops[t - m * nops];
+      const int64_t* s = st + m * 6;
+      const double tokens = (double)s[1];
+      if (s[1] > 0) {
+        if (o.cls == SSG_CLS_TOKEN) {
+          active = true;
+          v0 = tokens;
+          if (o.flop_kind == 0)
+            fl = __dmul_rn(__dmul_rn(__dmul_rn(2.0, tokens), o.fa), o.fb);
+          else if (o.flop_kind == 1)
+            fl = __dmul_rn(tokens, o.fa);
+          else
+            fl = __dmul_rn(__dmul_rn(8.0, tokens), o.fa);
+        } else if (o.cls == SSG_CLS_SEQ) {
+          if (o.flop_kind == 3 && s[0] > 0) {
+            active = true;
+            const double n_eq = (double)ssg_llround_nonneg(sqrt((double)s[2]));
+            v0 = n_eq;
+            v1 = __dmul_rn((double)s[3], o.kvb);
+            const double ctx_tokens = v1 / o.kvb;
+            fl = __dmul_rn(__dmul_rn(__dmul_rn(4.0, n_eq), __dadd_rn(n_eq, ctx_tokens)), o.fa);
+          } else if (o.flop_kind == 4 && s[4] > 0) {
+            active = true;
+            v0 = (double)s[4];
+            v1 = __dmul_rn((double)s[5], o.kvb);
+            const double ctx_tokens = v1 / o.kvb;
+            fl = __dmul_rn(__dmul_rn(4.0, ctx_tokens), o.fa);
+          }
+        } else {
+          active = true;
+          v0 = __dmul_rn(tokens, o.payload);
+        }
+      }
+      if (active) {
+        qb += o.qbytes;
+        code = ssg_predict_t<FMA, FOREST>(U.E, o.slot, v0, v1, &pred, &bad);
+        pred = __dmul_rn(o.count, pred);
+        fl = (o.cls == SSG_CLS_COMM) ? 0.0 : __dmul_rn(o.count, fl);
+      }
+    }
+    const unsigned em = __ballot_sync(SSG_FULL, code != SSG_OK);
+    if (em && err == SSG_OK) {
+      const int src = __ffs(em) - 1;
+      err = __shfl_sync(SSG_FULL, code, src);
+      err_task = base + src;
+      err_feat = __shfl_sync(SSG_FULL, bad, src);
+      err_val = __shfl_sync(SSG_FULL, bad ? v1 : v0, src);
+    }
+    const int kmax = (work - base) < 32 ? (work - base) : 32;
+    for (int k = 0; k < kmax; ++k) {
+      const double pk = __shfl_sync(SSG_FULL, pred, k);
+      const double fk = __shfl_sync(SSG_FULL, fl, k);
+      const int ak = __shfl_sync(SSG_FULL, (int)active, k);
+      const int m = (base + k) / nops;
+      if (m != cur_m) {
+        if (U.lane == 0) {
+          secs_part[cur_m] = acc_s;
+          flop_part[cur_m] = acc_f;
+        }
+        acc_s = 0.0;
+        acc_f = 0.0;
+        cur_m = m;
+      }
+      if (ak) {
+        acc_s = __dadd_rn(acc_s, pk);
+        if (c.ops[(base + k) - m * nops].cls != SSG_CLS_COMM) acc_f = __dadd_rn(acc_f, fk);
+      }
+    }
+  }
+  if (U.lane == 0) {
+    secs_part[cur_m] = acc_s;
+    flop_part[cur_m] = acc_f;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) qb += __shfl_xor_sync(SSG_FULL, qb, o);
+  U.qbytes += qb;
+  __syncwarp();
+}
+
+template <int FMA, int FOREST>
 __device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, double* flops_out) {
   const SimConfig& c = *U.cfg;
   const int pp = c.pp;
@@ -631,7 +767,7 @@ __device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, doubl
           v0 = (double)n_eq;
           v1 = __dmul_rn((double)s6[3], o.kvb);
           const double ctx_tokens = v1 / o.kvb;
-          code = ssg_predict_one(U.E, o.slot, v0, v1, &pred, &bad);
+          code = ssg_predict_t<FMA, FOREST>(U.E, o.slot, v0, v1, &pred, &bad);
           pred = __dmul_rn(o.count, pred);
           fl = __dmul_rn(o.count, __dmul_rn(__dmul_rn(__dmul_rn(4.0, v0), __dadd_rn(v0, ctx_tokens)), o.fa));
         }
@@ -640,7 +776,7 @@ __device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, doubl
         v0 = (double)s6[4];
         v1 = __dmul_rn((double)s6[5], o.kvb);
         const double ctx_tokens = v1 / o.kvb;
-        code = ssg_predict_one(U.E, o.slot, v0, v1, &pred, &bad);
+        code = ssg_predict_t<FMA, FOREST>(U.E, o.slot, v0, v1, &pred, &bad);
         pred = __dmul_rn(o.count, pred);
         fl = __dmul_rn(o.count, __dmul_rn(__dmul_rn(4.0, ctx_tokens), o.fa));
       }
@@ -689,98 +825,12 @@ __device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, doubl
     }
     __syncwarp();
   } else {
-    const int work = pp * nops;
-    double acc_s = 0.0, acc_f = 0.0;
-    int cur_m = 0;
-    for (int base = 0; base < work; base += 32) {
-      const int t = base + U.lane;
-      double pred = 0.0, fl = 0.0, v0 = 0.0, v1 = 0.0;
-      bool active = false;
-      int code = SSG_OK, bad = 0;
-      if (t < work) {
-        const int m = t / nops;
-        const SimOp& o = c.ops[t - m * nops];
-        const int64_t* s = st + m * 6;
-        const double tokens = (double)s[1];
-        if (s[1] > 0) {
-          if (o.cls == SSG_CLS_TOKEN) {
-            active = true;
-            v0 = tokens;
-            if (o.flop_kind == 0)
-              fl = __dmul_rn(__dmul_rn(__dmul_rn(2.0, tokens), o.fa), o.fb);
-            else if (o.flop_kind == 1)
-              fl = __dmul_rn(tokens, o.fa);
-            else
-              fl = __dmul_rn(__dmul_rn(8.0, tokens), o.fa);
-          } else if (o.cls == SSG_CLS_SEQ) {
-            if (o.flop_kind == 3 && s[0] > 0) {
-              active = true;
-              const double n_eq = (double)ssg_llround_nonneg(sqrt((double)s[2]));
-              v0 = n_eq;
-              v1 = __dmul_rn((double)s[3], o.kvb);
-              const double ctx_tokens = v1 / o.kvb;
-              fl = __dmul_rn(__dmul_rn(__dmul_rn(4.0, n_eq), __dadd_rn(n_eq, ctx_tokens)), o.fa);
-            } else if (o.flop_kind == 4 && s[4] > 0) {
-              active = true;
-              v0 = (double)s[4];
-              v1 = __dmul_rn((double)s[5], o.kvb);
-              const double ctx_tokens = v1 / o.kvb;
-              fl = __dmul_rn(__dmul_rn(4.0, ctx_tokens), o.fa);
-            }
-          } else {
-            active = true;
-            v0 = __dmul_rn(tokens, o.payload);
-          }
-        }
-        if (active) {
-          qb += o.qbytes;
-          code = ssg_predict_one(U.E, o.slot, v0, v1, &pred, &bad);
-          pred = __dmul_rn(o.count, pred);
-          fl = (o.cls == SSG_CLS_COMM) ? 0.0 : __dmul_rn(o.count, fl);
-        }
-      }
-      const unsigned em = __ballot_sync(SSG_FULL, code != SSG_OK);
-      if (em && err == SSG_OK) {
-        const int src = __ffs(em) - 1;
-        err = __shfl_sync(SSG_FULL, code, src);
-        err_task = base + src;
-        err_feat = __shfl_sync(SSG_FULL, bad, src);
-        err_val = __shfl_sync(SSG_FULL, bad ? v1 : v0, src);
-      }
-      const int kmax = (work - base) < 32 ? (work - base) : 32;
-      for (int k = 0; k < kmax; ++k) {
-        const double pk = __shfl_sync(SSG_FULL, pred, k);
-        const double fk = __shfl_sync(SSG_FULL, fl, k);
-        const int ak = __shfl_sync(SSG_FULL, (int)active, k);
-        const int m = (base + k) / nops;
-        if (m != cur_m) {
-          if (U.lane == 0) {
-            secs_part[cur_m] = acc_s;
-            flop_part[cur_m] = acc_f;
-          }
-          acc_s = 0.0;
-          acc_f = 0.0;
-          cur_m = m;
-        }
-        if (ak) {
-          acc_s = __dadd_rn(acc_s, pk);
-          if (c.ops[(base + k) - m * nops].cls != SSG_CLS_COMM) acc_f = __dadd_rn(acc_f, fk);
-        }
-      }
-    }
-    if (U.lane == 0) {
-      secs_part[cur_m] = acc_s;
-      flop_part[cur_m] = acc_f;
-    }
-  #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) qb += __shfl_xor_sync(SSG_FULL, qb, o);
-    U.qbytes += qb;
-    __syncwarp();
-    if (err != SSG_OK) {
-      const SimOp& o = c.ops[err_task % nops];
-      set_error(U, err, o.slot, err_feat, 0, err_val);
-      return err;
-    }
+    batch_latency_full<FMA, FOREST>(U, st, err, err_task, err_feat, err_val, qb);
+  }
+  if (err != SSG_OK) {  // first failing (microbatch, op) in order -- either path
+    const SimOp& o = c.ops[err_task % nops];
+    set_error(U, err, o.slot, err_feat, 0, err_val);
+    return err;
   }
   double lat = 0.0, flops = 0.0;
   if (pp == 1) {

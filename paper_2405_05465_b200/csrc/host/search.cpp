@@ -237,6 +237,7 @@ struct ProbeLaunch {
   std::vector<ProbeDesc> probes;
   std::vector<std::size_t> probe_cand;
   std::vector<int32_t> measured;  // probe indices of full (measured) runs, slot order
+  bool has_forest = false;
   int64_t nreq = 0, ws_words = 0, nreps = 0;
 
   int32_t add_config(const Candidate& C) {
@@ -244,6 +245,7 @@ struct ProbeLaunch {
     if (it == est_index.end()) {
       it = est_index.emplace(C.est, static_cast<int32_t>(ests.size())).first;
       ests.push_back(C.est->device().view);
+      has_forest = has_forest || C.est->device().has_forest;
     }
     SimConfig sc = C.sim;
     sc.est = it->second;
@@ -348,6 +350,8 @@ void run_launch(SweepBuffers& B, ProbeLaunch& L, const ResidentWorkload& w,
   K.log = nullptr;
   K.out = B.out.ptr;
   K.tables = B.tables.ptr;
+  K.fast_forward = fast_forward_enabled();
+  K.has_forest = L.has_forest ? 1 : 0;
   cudaEvent_t e0, e1;
   cuda_check(cudaEventCreate(&e0), "event");
   cuda_check(cudaEventCreate(&e1), "event");

@@ -311,6 +311,8 @@ void run_jobs(const SimJobs& J, SimResults& R, bool want_requests) {
   L.log = J.log_words > 0 ? d_log.ptr : nullptr;
   L.out = d_out.ptr;
   L.tables = J.tables;
+  L.fast_forward = fast_forward_enabled();
+  L.has_forest = J.has_forest ? 1 : 0;
   cudaEvent_t ev0, ev1;
   cuda_check(cudaEventCreate(&ev0), "event");
   cuda_check(cudaEventCreate(&ev1), "event");
@@ -414,6 +416,7 @@ Placement place(const ClusterConfig& cluster, const std::vector<Request>& trace,
   J.configs.push_back(make_sim_config(cluster, estimator, 0));
   J.ests.push_back(estimator.device().view);
   build_token_tables(J.configs, J.ests, {&estimator.device()}, P.tables);
+  J.has_forest = estimator.device().has_forest;
   J.tables = P.tables.ptr;
   const int R = static_cast<int>(cluster.par.num_replicas);
   const std::size_t n = trace.size();

@@ -142,6 +142,7 @@ const DeviceEstimator& EstimatorModel::device() const {
       dpool.insert(dpool.end(), r.values.begin(), r.values.end());
     } else {
       desc.kind = SSG_KIND_FOREST;
+      d->has_forest = true;
       internal_check(r.num_features == static_cast<std::size_t>(desc.nf),
                      "forest predict: feature count mismatch");
       desc.ntrees = static_cast<int32_t>(r.trees.size());

@@ -138,24 +138,39 @@ __device__ __forceinline__ double ssg_forest(const SsgEstView& E, const SsgModel
 
 // Full EstimatorModel::predict for one query.  Returns SSG_OK and the
 // runtime in *out, or an SSG_ERR_* code (*bad_feature = schema index).
-__device__ __forceinline__ int ssg_predict_one(const SsgEstView& E, int32_t model, double v0,
-                                               double v1, double* out, int* bad_feature) {
+// FMA selects the glibc contraction variant at compile time (the host's);
+// FOREST = 0 compiles the interpolator only (the search default), keeping the
+// simulation kernels' instruction footprint small.
+template <int FMA, int FOREST>
+__device__ __forceinline__ int ssg_predict_t(const SsgEstView& E, int32_t model, double v0,
+                                             double v1, double* out, int* bad_feature) {
   const SsgModelDesc& m = E.models[model];
   if (!(v0 >= m.lower[0] && v0 <= m.upper[0])) {
     *bad_feature = 0;
     return SSG_ERR_BBOX;
   }
-  const double x0 = ssg_log1p(v0, E.math_fma);
+  const double x0 = ssg_log1p(v0, FMA);
   double x1 = 0.0;
   if (m.nf > 1) {
     if (!(v1 >= m.lower[1] && v1 <= m.upper[1])) {
       *bad_feature = 1;
       return SSG_ERR_BBOX;
     }
-    x1 = ssg_log1p(v1, E.math_fma);
+    x1 = ssg_log1p(v1, FMA);
   }
-  const double r = (m.kind == SSG_KIND_FOREST) ? ssg_forest(E, m, x0, x1) : ssg_interp(E, m, x0, x1);
+  double r;
+  if (FOREST && m.kind == SSG_KIND_FOREST)
+    r = ssg_forest(E, m, x0, x1);
+  else
+    r = ssg_interp(E, m, x0, x1);
   if (!ssg_exp_in_range(r)) return SSG_ERR_EXP_RANGE;
-  *out = ssg_exp(r, E.math_fma);
+  *out = ssg_exp(r, FMA);
   return SSG_OK;
+}
+
+// Runtime-dispatched form for the batched predictor kernel (one call site).
+__device__ __forceinline__ int ssg_predict_one(const SsgEstView& E, int32_t model, double v0,
+                                               double v1, double* out, int* bad_feature) {
+  return E.math_fma ? ssg_predict_t<1, 1>(E, model, v0, v1, out, bad_feature)
+                    : ssg_predict_t<0, 1>(E, model, v0, v1, out, bad_feature);
 }

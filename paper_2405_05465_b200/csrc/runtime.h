@@ -116,6 +116,7 @@ struct DeviceEstimator {
   std::vector<int64_t> qbytes;          // algorithmic bytes of one query per slot
   SsgEstView view{};
   std::size_t bytes = 0;  // HBM footprint
+  bool has_forest = false;
 
   int32_t slot(OpName op, std::int64_t tp) const {
     auto it = index.find({op, tp});

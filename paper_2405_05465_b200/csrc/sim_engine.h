@@ -26,9 +26,13 @@ struct SimLaunch {
   int64_t* log;              // may be null
   SimUnitOut* out;
   const double* tables;       // token tables pool, may be null
+  int32_t fast_forward;       // 1: pure-decode stretches of lone replicas take the fast loop
+  int32_t has_forest;         // any estimator of the launch has forest models
 };
 
 namespace ssg {
+// SSG_NO_FASTFWD=1 disables the pure-decode fast-forward (A/B checks).
+int fast_forward_enabled();
 void launch_simulate(const SimLaunch& L, cudaStream_t s);
 // Builds the token tables of `n` configs (cfgs[i].tab_off / tab_stride set by
 // the caller); valid[i*stride + t] gets bit0 = token/comm terms valid, bit1 =

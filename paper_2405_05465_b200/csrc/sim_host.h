@@ -62,6 +62,7 @@ struct SimJobs {
   int64_t ws_words = 0, nreps = 0, log_words = 0, emissions = 0;
   bool any_order = false;
   const double* tables = nullptr;  // token tables pool (device), if built
+  bool has_forest = false;         // any estimator of the launch uses forests
 
   // Adds a unit over the given requests, which must already be in (arrival,
   // id) order; `event_order` (may be empty = identity) lists local indices in

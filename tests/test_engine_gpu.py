@@ -173,3 +173,26 @@ def test_predict_batch_parity(ssg, ref):
         assert res == {}
         assert np.array_equal(s_m.view(np.uint64), s_t.view(np.uint64))
         assert np.array_equal(f_m.view(np.uint64), f_t.view(np.uint64))
+
+
+def test_bbox_error_inside_a_batch(ssg, ref):
+    """A decode batch whose KV volume leaves the trained box (estimator.hpp:115-119)
+    surfaces the reference's exact Error from inside the simulation (token-table
+    path: tokens stay in range, the attention feature does not)."""
+    tiny = dict(catalog.MODELS["llama2_7b"], name="tiny-ctx", max_context=128)
+    text = ref.train(tiny, catalog.DEVICES["a100_80g"], [1], "interp", 0)
+    m, t = ssg.Estimator.from_json(text), ref.Estimator(text)
+    cluster = catalog.cluster_doc(tiny, "a100_80g", policy="sarathi_serve", chunk_size=128,
+                                  max_batch_size=128)
+    n = 120
+    ids = np.arange(n, dtype=np.int64)
+    arr = np.arange(n, dtype=np.float64) * 1e-3
+    pre = np.full(n, 300, dtype=np.int64)
+    dec = np.full(n, 2000, dtype=np.int64)
+    from oracle.ref import RefError
+    with pytest.raises(RefError) as er:
+        t.simulate(cluster, ids, arr, pre, dec)
+    with pytest.raises(ssg.InputError) as ei:
+        ssg.simulate(cluster, m, ids, arr, pre, dec)
+    assert "attn_decode@tp1 outside extrapolation margin" in str(er.value)
+    assert str(ei.value) == str(er.value)
