@@ -15,7 +15,7 @@
 
 #include "engine.cuh"
 #ifndef SSG_FFWD
-#define SSG_FFWD __noinline__
+#define SSG_FFWD __forceinline__
 #endif
 #include "runtime.h"
 #include "sim_engine.h"
@@ -37,7 +37,7 @@ __device__ __forceinline__ void store_rep(Unit& U, int r, const RepState& s) {
 }
 
 // ReplicaScheduler::enqueue (scheduler.hpp:146-155)
-__device__ SSG_COLD bool enqueue(Unit& U, RepState& S, int r, int32_t j) {
+__device__ __forceinline__ bool enqueue(Unit& U, RepState& S, int r, int32_t j) {
   const SimConfig& c = *U.cfg;
   const ReqHot h = U.hot[j];
   const int64_t need = units_for(c, (int64_t)h.prefill + h.decode);
@@ -553,7 +553,7 @@ __device__ SSG_FFWD int fast_forward(Unit& U, RepState& S, double next_arrival_t
   return fast_forward_t<FMA>(U, S, next_arrival_time, flops_acc);
 }
 
-template <int FMA, int FOREST>
+template <int FMA, int FOREST, int FAST>
 __device__ void run_unit(Unit& U) {
   const long long t_start = clock64();
   const SimUnit& u = *U.u;
@@ -600,7 +600,6 @@ __device__ void run_unit(Unit& U) {
       u.n > 0 ? U.tm[U.arr_order ? U.arr_order[0] : 0].arrival : INFINITY;
   // a lone replica (no deferred pool) keeps its scheduler state in registers
   const bool reg1 = R == 1 && c.routing != SSG_ROUTE_DEFERRED;
-  const bool fast_ok = reg1 && U.fast;
   RepState S1;
   memset(&S1, 0, sizeof S1);
   while (true) {
@@ -705,7 +704,7 @@ __device__ void run_unit(Unit& U) {
     }
     const int r = bw;
     RepState S = reg1 ? S1 : load_rep(U, r);
-    if (S.ev_kind == 1 && reg1 && fast_ok) {
+    if (FAST && S.ev_kind == 1 && reg1 && S.wait_n == 0 && S.run_n >= 1 && S.run_n <= 32) {
       // pure-decode stretch: iterations that end at the same state the event
       // loop would reach; afterwards the replica is again "BatchStart at clock"
       double fl = U.out->flops;
@@ -777,7 +776,7 @@ __device__ void run_unit(Unit& U) {
   }
 }
 
-template <int FMA, int FOREST>
+template <int FMA, int FOREST, int FAST>
 __global__ void __launch_bounds__(SSG_SIM_WARPS * 32)
     k_simulate(SimLaunch L) {
   __shared__ int64_t stats[SSG_SIM_WARPS][SSG_MAX_PP * 6];
@@ -818,7 +817,7 @@ __global__ void __launch_bounds__(SSG_SIM_WARPS * 32)
   U.MB = U.cfg->max_batch;
   U.WC = U.u->wait_cap;
   U.rep_stride = 6LL * U.MB + U.WC;
-  run_unit<FMA, FOREST>(U);
+  run_unit<FMA, FOREST, FAST>(U);
 }
 
 // predict_batch / batch_device_flops for standalone compositions (the
@@ -887,19 +886,30 @@ int fast_forward_enabled() {
   return on;
 }
 
+int sweep_fast_forward_enabled() {
+  static const int on = std::getenv("SSG_SWEEP_FASTFWD") != nullptr ? 1 : 0;
+  return on;
+}
+
 void launch_simulate(const SimLaunch& L, cudaStream_t s) {
   if (L.nunits <= 0) return;
   const int64_t blocks = (L.nunits + SSG_SIM_WARPS - 1) / SSG_SIM_WARPS;
-  // one instantiation per glibc variant x (interp-only | with forests)
+  // one instantiation per glibc variant x (interp-only | with forests) x
+  // (decode fast-forward compiled in | out): the kernel is instruction-fetch
+  // bound, so each launch runs the smallest body that covers it
   const int fma = context().math_fma;
-  if (fma && L.has_forest)
-    ssgk::k_simulate<1, 1><<<(unsigned)blocks, SSG_SIM_WARPS * 32, 0, s>>>(L);
-  else if (fma)
-    ssgk::k_simulate<1, 0><<<(unsigned)blocks, SSG_SIM_WARPS * 32, 0, s>>>(L);
-  else if (L.has_forest)
-    ssgk::k_simulate<0, 1><<<(unsigned)blocks, SSG_SIM_WARPS * 32, 0, s>>>(L);
-  else
-    ssgk::k_simulate<0, 0><<<(unsigned)blocks, SSG_SIM_WARPS * 32, 0, s>>>(L);
+  const int key = (fma ? 4 : 0) | (L.has_forest ? 2 : 0) | (L.fast_forward ? 1 : 0);
+  const unsigned grid = (unsigned)blocks, block = SSG_SIM_WARPS * 32;
+  switch (key) {
+    case 0: ssgk::k_simulate<0, 0, 0><<<grid, block, 0, s>>>(L); break;
+    case 1: ssgk::k_simulate<0, 0, 1><<<grid, block, 0, s>>>(L); break;
+    case 2: ssgk::k_simulate<0, 1, 0><<<grid, block, 0, s>>>(L); break;
+    case 3: ssgk::k_simulate<0, 1, 1><<<grid, block, 0, s>>>(L); break;
+    case 4: ssgk::k_simulate<1, 0, 0><<<grid, block, 0, s>>>(L); break;
+    case 5: ssgk::k_simulate<1, 0, 1><<<grid, block, 0, s>>>(L); break;
+    case 6: ssgk::k_simulate<1, 1, 0><<<grid, block, 0, s>>>(L); break;
+    default: ssgk::k_simulate<1, 1, 1><<<grid, block, 0, s>>>(L); break;
+  }
   cuda_check(cudaGetLastError(), "k_simulate launch");
 }
 

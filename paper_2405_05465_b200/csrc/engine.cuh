@@ -30,7 +30,7 @@
 // SSG_COLD marks rarely executed scheduler paths, SSG_WARM the per-policy
 // schedulers.  Each expands to __noinline__ or __forceinline__ at build time.
 #ifndef SSG_COLD
-#define SSG_COLD __noinline__
+#define SSG_COLD __forceinline__
 #endif
 #ifndef SSG_WARM
 #define SSG_WARM __forceinline__
@@ -199,7 +199,7 @@ __device__ __forceinline__ int32_t ring_upper(const int32_t* a, int32_t mask, in
 }
 
 // insert_sorted(waiting_, r) (scheduler.hpp:243-247)
-__device__ SSG_COLD void wait_insert(Unit& U, RepState& S, int r, int32_t j) {
+__device__ __forceinline__ void wait_insert(Unit& U, RepState& S, int r, int32_t j) {
   int32_t* w = WAIT(U, r);
   const int32_t mask = U.WC - 1;
   int32_t pos;
@@ -219,7 +219,7 @@ __device__ SSG_COLD void wait_insert(Unit& U, RepState& S, int r, int32_t j) {
 
 // erase_from_waiting (scheduler.hpp:474-478); the queue is sorted, so the
 // element's position is its lower bound.
-__device__ SSG_COLD void wait_erase(Unit& U, RepState& S, int r, int32_t j) {
+__device__ __forceinline__ void wait_erase(Unit& U, RepState& S, int r, int32_t j) {
   int32_t* w = WAIT(U, r);
   const int32_t mask = U.WC - 1;
   int32_t pos = ring_upper(w, mask, S.wait_head, S.wait_n, j - 1);
@@ -242,7 +242,7 @@ __device__ __forceinline__ int32_t wait_front(Unit& U, const RepState& S, int r)
 }
 
 // insert_sorted_running (scheduler.hpp:249-252)
-__device__ SSG_COLD void run_insert(Unit& U, RepState& S, int r, int32_t j) {
+__device__ __forceinline__ void run_insert(Unit& U, RepState& S, int r, int32_t j) {
   int32_t* a = RUN(U, r);
   int32_t pos;
   if (S.run_n == 0 || a[S.run_n - 1] < j)
@@ -254,7 +254,7 @@ __device__ SSG_COLD void run_insert(Unit& U, RepState& S, int r, int32_t j) {
   S.run_n += 1;
 }
 
-__device__ SSG_COLD void run_erase_at(Unit& U, RepState& S, int r, int32_t pos) {
+__device__ __forceinline__ void run_erase_at(Unit& U, RepState& S, int r, int32_t pos) {
   int32_t* a = RUN(U, r);
   ring_shift(U, a, 0x7fffffff, 0, pos + 1, S.run_n, -1);
   S.run_n -= 1;
@@ -298,7 +298,7 @@ __device__ SSG_COLD int32_t preempt_latest(Unit& U, RepState& S, int r) {
 }
 
 // ensure_decode_memory (scheduler.hpp:290-296)
-__device__ SSG_COLD bool ensure_decode_memory(Unit& U, RepState& S, int r, int32_t j) {
+__device__ __forceinline__ bool ensure_decode_memory(Unit& U, RepState& S, int r, int32_t j) {
   while (!try_reserve(U, S, j, (int64_t)U.hot[j].kv + 1)) {
     const int32_t victim = preempt_latest(U, S, r);
     if (victim < 0 || victim == j) return false;
@@ -307,7 +307,7 @@ __device__ SSG_COLD bool ensure_decode_memory(Unit& U, RepState& S, int r, int32
 }
 
 // admit_reserve (scheduler.hpp:302-316)
-__device__ SSG_COLD bool admit_reserve(Unit& U, RepState& S, int r, int32_t j, int64_t target,
+__device__ __forceinline__ bool admit_reserve(Unit& U, RepState& S, int r, int32_t j, int64_t target,
                               bool allow_preempt, bool use_watermark) {
   const SimConfig& c = *U.cfg;
   while (true) {

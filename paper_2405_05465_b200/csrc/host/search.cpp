@@ -350,7 +350,7 @@ void run_launch(SweepBuffers& B, ProbeLaunch& L, const ResidentWorkload& w,
   K.log = nullptr;
   K.out = B.out.ptr;
   K.tables = B.tables.ptr;
-  K.fast_forward = fast_forward_enabled();
+  K.fast_forward = sweep_fast_forward_enabled();
   K.has_forest = L.has_forest ? 1 : 0;
   cudaEvent_t e0, e1;
   cuda_check(cudaEventCreate(&e0), "event");

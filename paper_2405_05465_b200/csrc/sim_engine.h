@@ -33,6 +33,9 @@ struct SimLaunch {
 namespace ssg {
 // SSG_NO_FASTFWD=1 disables the pure-decode fast-forward (A/B checks).
 int fast_forward_enabled();
+// Sweeps compile the fast-forward out (measured faster: the many concurrent
+// probe warps are instruction-fetch bound); SSG_SWEEP_FASTFWD=1 turns it on.
+int sweep_fast_forward_enabled();
 void launch_simulate(const SimLaunch& L, cudaStream_t s);
 // Builds the token tables of `n` configs (cfgs[i].tab_off / tab_stride set by
 // the caller); valid[i*stride + t] gets bit0 = token/comm terms valid, bit1 =
