@@ -2,6 +2,8 @@
 #include "runtime.h"
 
 #include <cmath>
+#include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -13,6 +15,7 @@ namespace {
 Context g_ctx;
 RunStats g_stats;
 std::mutex g_mu;
+bool g_pool = true;
 }  // namespace
 
 int probe_host_math_variant() {
@@ -75,6 +78,15 @@ void init_context(int device) {
   cuda_check(cudaStreamCreateWithFlags(&g_ctx.stream, cudaStreamNonBlocking), "stream");
   g_ctx.device = device;
   g_ctx.num_sms = prop.multiProcessorCount;
+  const char* pool_env = std::getenv("SSG_POOL");
+  g_pool = !(pool_env && pool_env[0] == '0');
+  if (g_pool) {
+    cudaMemPool_t pool;
+    cuda_check(cudaDeviceGetDefaultMemPool(&pool, device), "cudaDeviceGetDefaultMemPool");
+    std::uint64_t keep = UINT64_MAX;
+    cuda_check(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep),
+               "cudaMemPoolSetAttribute");
+  }
   if (g_ctx.math_fma < 0) g_ctx.math_fma = probe_host_math_variant();
 }
 
@@ -82,6 +94,23 @@ Context& context() {
   if (!g_ctx.stream) init_context(0);
   cuda_check(cudaSetDevice(g_ctx.device), "cudaSetDevice");
   return g_ctx;
+}
+
+void* device_alloc(std::size_t bytes) {
+  Context& c = context();
+  void* p = nullptr;
+  if (g_pool)
+    cuda_check(cudaMallocAsync(&p, bytes, c.stream), "cudaMallocAsync");
+  else
+    cuda_check(cudaMalloc(&p, bytes), "cudaMalloc");
+  return p;
+}
+
+void device_free(void* p) {
+  if (g_pool && g_ctx.stream)
+    cudaFreeAsync(p, g_ctx.stream);
+  else
+    cudaFree(p);
 }
 
 void shutdown_context() {

@@ -34,7 +34,15 @@ Context& context();
 void init_context(int device);
 void shutdown_context();
 
-
+// HBM for DeviceBuffer: stream-ordered allocations on the context stream from the
+// device's memory pool, which keeps freed blocks (release threshold = max), so a
+// new search session or simulation reuses the previous one's HBM instead of paying
+// cudaMalloc/cudaFree (a device-wide sync) per buffer.  SSG_POOL=0 falls back to
+// plain cudaMalloc/cudaFree (A/B only).  Every library kernel and copy runs on the
+// context stream; callers that pass their own stream only read buffers whose
+// upload was synchronised.
+void* device_alloc(std::size_t bytes);
+void device_free(void* p);
 
 // Which glibc contraction this host's libm runs (host_math.cpp).
 int probe_host_math_variant();
@@ -81,11 +89,11 @@ struct DeviceBuffer {
     if (n <= count && ptr) return;
     release();
     if (n == 0) return;
-    cuda_check(cudaMalloc(&ptr, n * sizeof(T)), "cudaMalloc");
+    ptr = static_cast<T*>(device_alloc(n * sizeof(T)));
     count = n;
   }
   void release() {
-    if (ptr) cudaFree(ptr);
+    if (ptr) device_free(ptr);
     ptr = nullptr;
     count = 0;
   }
