@@ -154,6 +154,8 @@ typedef struct ssg_run_stats {
   double simulate_ms;      /* k_simulate device time (CUDA events, library stream) */
   int64_t h2d_bytes, d2h_bytes; /* host<->device copies issued by the library */
   int64_t launches_setup;  /* probe-stream setup and SLO sample kernels */
+  double simulate_busy_ms; /* union of k_simulate intervals: sweep launches of candidate groups
+                              overlap on separate streams, so this is <= simulate_ms */
 } ssg_run_stats;
 void ssg_stats_reset(void);
 void ssg_stats_get(ssg_run_stats* out);

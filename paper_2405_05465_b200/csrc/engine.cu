@@ -776,8 +776,11 @@ __device__ void run_unit(Unit& U) {
   }
 }
 
+#ifndef SSG_SIM_MINB
+#define SSG_SIM_MINB 1
+#endif
 template <int FMA, int FOREST, int FAST>
-__global__ void __launch_bounds__(SSG_SIM_WARPS * 32)
+__global__ void __launch_bounds__(SSG_SIM_WARPS * 32, SSG_SIM_MINB)
     k_simulate(SimLaunch L) {
   __shared__ int64_t stats[SSG_SIM_WARPS][SSG_MAX_PP * 6];
   __shared__ double part[SSG_SIM_WARPS][4 * SSG_MAX_PP];
@@ -900,15 +903,27 @@ void launch_simulate(const SimLaunch& L, cudaStream_t s) {
   const int fma = context().math_fma;
   const int key = (fma ? 4 : 0) | (L.has_forest ? 2 : 0) | (L.fast_forward ? 1 : 0);
   const unsigned grid = (unsigned)blocks, block = SSG_SIM_WARPS * 32;
+  // diagnostic: SSG_SIM_SMEM bytes of dynamic shared memory per block caps
+  // the resident warps per SM (A/B of occupancy vs instruction-cache reuse)
+  static const int smem = [] {
+    const char* e = std::getenv("SSG_SIM_SMEM");
+    return e ? std::atoi(e) : 0;
+  }();
+  auto go = [&](auto kern) {
+    if (smem > 48 * 1024)
+      cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+                 "k_simulate smem");
+    kern<<<grid, block, smem, s>>>(L);
+  };
   switch (key) {
-    case 0: ssgk::k_simulate<0, 0, 0><<<grid, block, 0, s>>>(L); break;
-    case 1: ssgk::k_simulate<0, 0, 1><<<grid, block, 0, s>>>(L); break;
-    case 2: ssgk::k_simulate<0, 1, 0><<<grid, block, 0, s>>>(L); break;
-    case 3: ssgk::k_simulate<0, 1, 1><<<grid, block, 0, s>>>(L); break;
-    case 4: ssgk::k_simulate<1, 0, 0><<<grid, block, 0, s>>>(L); break;
-    case 5: ssgk::k_simulate<1, 0, 1><<<grid, block, 0, s>>>(L); break;
-    case 6: ssgk::k_simulate<1, 1, 0><<<grid, block, 0, s>>>(L); break;
-    default: ssgk::k_simulate<1, 1, 1><<<grid, block, 0, s>>>(L); break;
+    case 0: go(ssgk::k_simulate<0, 0, 0>); break;
+    case 1: go(ssgk::k_simulate<0, 0, 1>); break;
+    case 2: go(ssgk::k_simulate<0, 1, 0>); break;
+    case 3: go(ssgk::k_simulate<0, 1, 1>); break;
+    case 4: go(ssgk::k_simulate<1, 0, 0>); break;
+    case 5: go(ssgk::k_simulate<1, 0, 1>); break;
+    case 6: go(ssgk::k_simulate<1, 1, 0>); break;
+    default: go(ssgk::k_simulate<1, 1, 1>); break;
   }
   cuda_check(cudaGetLastError(), "k_simulate launch");
 }

@@ -409,6 +409,7 @@ void ssg_stats_get(ssg_run_stats* out) {
   out->h2d_bytes = r.h2d_bytes;
   out->launches_setup = r.launches_setup;
   out->d2h_bytes = r.d2h_bytes;
+  out->simulate_busy_ms = r.simulate_busy_ms;
 }
 
 int ssg_search_finalize(const char* config_path, const ssg_config_record* records, size_t n,

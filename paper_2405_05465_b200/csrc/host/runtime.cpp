@@ -1,6 +1,7 @@
 // runtime.cpp -- device context and the host-libm variant probe.
 #include "runtime.h"
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -16,7 +17,41 @@ Context g_ctx;
 RunStats g_stats;
 std::mutex g_mu;
 bool g_pool = true;
+std::mutex g_stats_mu;
+thread_local RunStats* t_stats = nullptr;
+thread_local cudaStream_t t_stream = nullptr;
 }  // namespace
+
+void RunStats::add(const RunStats& o) {
+  launches_simulate += o.launches_simulate;
+  launches_select += o.launches_select;
+  launches_predict += o.launches_predict;
+  launches_batch += o.launches_batch;
+  launches_setup += o.launches_setup;
+  units += o.units;
+  iterations += o.iterations;
+  entries += o.entries;
+  events += o.events;
+  predictor_bytes += o.predictor_bytes;
+  entry_bytes += o.entry_bytes;
+  simulate_ms += o.simulate_ms;
+  queries += o.queries;
+  predict_ms += o.predict_ms;
+  h2d_bytes += o.h2d_bytes;
+  d2h_bytes += o.d2h_bytes;
+  simulate_busy_ms += o.simulate_busy_ms;
+}
+
+StatsScope::StatsScope() : prev(t_stats) { t_stats = &local; }
+StatsScope::~StatsScope() {
+  t_stats = prev;
+  std::lock_guard<std::mutex> lk(g_stats_mu);
+  stats().add(local);
+}
+
+StreamScope::StreamScope(cudaStream_t s) : prev(t_stream) { t_stream = s; }
+StreamScope::~StreamScope() { t_stream = prev; }
+cudaStream_t current_stream() { return t_stream ? t_stream : context().stream; }
 
 int probe_host_math_variant() {
   // Walk inputs until both routines have separated the two contractions at
@@ -56,7 +91,7 @@ int probe_host_math_variant() {
       "cannot be made bit-identical to this host");
 }
 
-RunStats& stats() { return g_stats; }
+RunStats& stats() { return t_stats ? *t_stats : g_stats; }
 
 void init_context(int device) {
   std::lock_guard<std::mutex> lk(g_mu);
@@ -86,6 +121,13 @@ void init_context(int device) {
     std::uint64_t keep = UINT64_MAX;
     cuda_check(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep),
                "cudaMemPoolSetAttribute");
+    // no allocator-inserted waits: a block freed on one sweep lane's stream
+    // behind a running kernel must not make another lane's allocation wait
+    // for that kernel (lanes exist to overlap); opportunistic reuse of frees
+    // that already completed stays on
+    int no = 0;
+    cuda_check(cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no),
+               "cudaMemPoolSetAttribute");
   }
   if (g_ctx.math_fma < 0) g_ctx.math_fma = probe_host_math_variant();
 }
@@ -96,21 +138,56 @@ Context& context() {
   return g_ctx;
 }
 
-void* device_alloc(std::size_t bytes) {
-  Context& c = context();
+void* device_alloc(std::size_t bytes, cudaStream_t s) {
+  context();
   void* p = nullptr;
   if (g_pool)
-    cuda_check(cudaMallocAsync(&p, bytes, c.stream), "cudaMallocAsync");
+    cuda_check(cudaMallocAsync(&p, bytes, s), "cudaMallocAsync");
   else
     cuda_check(cudaMalloc(&p, bytes), "cudaMalloc");
   return p;
 }
 
-void device_free(void* p) {
-  if (g_pool && g_ctx.stream)
-    cudaFreeAsync(p, g_ctx.stream);
+void device_free(void* p, cudaStream_t s) {
+  if (g_pool && g_ctx.stream && s)
+    cudaFreeAsync(p, s);
   else
     cudaFree(p);
+}
+
+HostStaging::~HostStaging() {
+  for (auto& c : chunks_) cudaFreeHost(c.p);
+}
+
+void* HostStaging::take(std::size_t bytes) {
+  bytes = (bytes + 255) & ~static_cast<std::size_t>(255);
+  if (chunks_.empty() || used_ + bytes > chunks_.back().cap) {
+    const std::size_t cap = std::max<std::size_t>(bytes, std::max<std::size_t>(1 << 20, total_));
+    char* p = nullptr;
+    cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&p), cap, cudaHostAllocPortable),
+               "cudaHostAlloc");
+    chunks_.push_back({p, cap});
+    total_ += cap;
+    used_ = 0;
+  }
+  void* p = chunks_.back().p + used_;
+  used_ += bytes;
+  return p;
+}
+
+void HostStaging::reset() {
+  if (chunks_.size() > 1) {  // consolidate into one chunk of the high-water size
+    for (auto& c : chunks_) cudaFreeHost(c.p);
+    chunks_.clear();
+    const std::size_t cap = total_;
+    total_ = 0;
+    char* p = nullptr;
+    cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&p), cap, cudaHostAllocPortable),
+               "cudaHostAlloc");
+    chunks_.push_back({p, cap});
+    total_ = cap;
+  }
+  used_ = 0;
 }
 
 void shutdown_context() {

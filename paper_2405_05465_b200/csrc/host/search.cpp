@@ -18,8 +18,13 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <exception>
 #include <map>
+#include <memory>
+#include <mutex>
 #include <sstream>
+#include <thread>
 #include <unordered_map>
 
 #include "engine_limits.h"
@@ -225,7 +230,6 @@ struct SweepBuffers {
   DeviceBuffer<RepState> reps;
   DeviceBuffer<SimUnitOut> out;
   DeviceBuffer<SelectTask> tasks;
-  DeviceBuffer<double> tables;  // token tables of the session's configs
 };
 
 // A launch under construction: per-candidate configs, probes and their units.
@@ -302,17 +306,37 @@ struct ProbeLaunch {
 // workload, simulation, and for the measured (full) runs the SLO samples and
 // their percentiles.  `sel` gets delay p99, TTFT p90, TBT p99 per measured run
 // (in L.measured order).
-void run_launch(SweepBuffers& B, ProbeLaunch& L, const ResidentWorkload& w,
+// A sweep lane: one stream and its launch buffers.  Candidate groups advance
+// their capacity searches on separate lanes, so one group's long probes do not
+// hold the others' next rounds (their launches overlap on the device).
+struct SweepLane {
+  struct Stream {
+    cudaStream_t s = nullptr;
+    Stream() { cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "lane stream"); }
+    ~Stream() {
+      if (s) cudaStreamDestroy(s);
+    }
+  } stream;          // declared first: destroyed after the buffers freed on it
+  SweepBuffers B;
+  HostStaging staging;             // pinned: this lane's copies never touch pageable memory
+  const double* tables = nullptr;  // token tables (session-wide, read-only)
+  cudaEvent_t origin = nullptr;    // sweep start, for k_simulate busy intervals
+  std::vector<std::pair<float, float>> intervals;
+};
+
+std::mutex g_dump_mu;
+
+void run_launch(SweepLane& lane, ProbeLaunch& L, const ResidentWorkload& w,
                 std::vector<SimUnitOut>& out, std::vector<double>& sel) {
-  auto& ctx = context();
-  cudaStream_t s = ctx.stream;
+  SweepBuffers& B = lane.B;
+  cudaStream_t s = lane.stream.s;
   const int32_t np = static_cast<int32_t>(L.probes.size());
   const int32_t nm = static_cast<int32_t>(L.measured.size());
   const bool emissions = nm > 0;
-  B.cfg.upload(L.configs, s);
-  B.est.upload(L.ests, s);
-  B.units.upload(L.units, s);
-  B.probes.upload(L.probes, s);
+  B.cfg.upload(L.configs, s, lane.staging);
+  B.est.upload(L.ests, s, lane.staging);
+  B.units.upload(L.units, s, lane.staging);
+  B.probes.upload(L.probes, s, lane.staging);
   B.hot.resize(std::max<int64_t>(1, L.nreq));
   B.tm.resize(std::max<int64_t>(1, L.nreq));
   B.ids.resize(std::max<int64_t>(1, L.nreq));
@@ -327,9 +351,23 @@ void run_launch(SweepBuffers& B, ProbeLaunch& L, const ResidentWorkload& w,
   // longest units first (fewest replicas share the trace => most requests per unit)
   std::vector<int32_t> order(L.units.size());
   for (std::size_t u = 0; u < order.size(); ++u) order[u] = static_cast<int32_t>(u);
-  std::stable_sort(order.begin(), order.end(),
-                   [&](int32_t a, int32_t b) { return L.units[a].n > L.units[b].n; });
-  B.order.upload(order, s);
+  static const int sort_mode = [] {
+    const char* e = std::getenv("SSG_UNIT_SORT");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (sort_mode == 1) {
+    // length, then policy: co-resident warps share their scheduler's code
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+      const auto& ua = L.units[a];
+      const auto& ub = L.units[b];
+      if (ua.n != ub.n) return ua.n > ub.n;
+      return L.configs[ua.config].policy < L.configs[ub.config].policy;
+    });
+  } else {
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int32_t a, int32_t b) { return L.units[a].n > L.units[b].n; });
+  }
+  B.order.upload(order, s, lane.staging);
   launch_probe_setup(B.probes.ptr, np, B.units.ptr, w, B.hot.ptr, B.tm.ptr, B.ids.ptr,
                      emissions ? B.emit_base.ptr : nullptr, s);
   SimLaunch K{};
@@ -349,7 +387,7 @@ void run_launch(SweepBuffers& B, ProbeLaunch& L, const ResidentWorkload& w,
   K.ws = B.ws.ptr;
   K.log = nullptr;
   K.out = B.out.ptr;
-  K.tables = B.tables.ptr;
+  K.tables = lane.tables;
   K.fast_forward = sweep_fast_forward_enabled();
   K.has_forest = L.has_forest ? 1 : 0;
   cudaEvent_t e0, e1;
@@ -358,11 +396,12 @@ void run_launch(SweepBuffers& B, ProbeLaunch& L, const ResidentWorkload& w,
   cuda_check(cudaEventRecord(e0, s), "event");
   launch_simulate(K, s);
   cuda_check(cudaEventRecord(e1, s), "event");
+  const double* sel_staged = nullptr;
   if (emissions) {
     // samples per measured run m: [delay | ttft] (n each), then TBT gaps (E each)
     std::vector<ProbeDesc> mp;
     for (int32_t k : L.measured) mp.push_back(L.probes[k]);
-    B.mprobes.upload(mp, s);
+    B.mprobes.upload(mp, s, lane.staging);
     const int64_t n = w.n, E = w.emis_per_probe;
     B.samples.resize(std::max<int64_t>(1, nm * (2 * n + E)));
     double* delay = B.samples.ptr;
@@ -381,22 +420,35 @@ void run_launch(SweepBuffers& B, ProbeLaunch& L, const ResidentWorkload& w,
       tasks.push_back({nm + k, nearest_rank_index(n, 0.90)});
       tasks.push_back({2 * nm + k, n_tbt > 0 ? nearest_rank_index(n_tbt, 0.99) : 0});
     }
-    B.seg_off.upload(off, s);
-    B.tasks.upload(tasks, s);
+    B.seg_off.upload(off, s, lane.staging);
+    B.tasks.upload(tasks, s, lane.staging);
     B.sel.resize(tasks.size());
     launch_select(B.samples.ptr, B.seg_off.ptr, B.tasks.ptr, static_cast<int64_t>(tasks.size()),
                   B.sel.ptr, s);
     sel.resize(tasks.size());
-    B.sel.download(sel.data(), sel.size(), s);
+    sel_staged = B.sel.download_staged(sel.size(), s, lane.staging);
   }
   out.resize(L.units.size());
-  B.out.download(out.data(), out.size(), s);
+  const SimUnitOut* out_staged = B.out.download_staged(out.size(), s, lane.staging);
   cuda_check(cudaStreamSynchronize(s), "sweep launch");
+  std::memcpy(out.data(), out_staged, out.size() * sizeof(SimUnitOut));
+  if (sel_staged) std::memcpy(sel.data(), sel_staged, sel.size() * sizeof(double));
+  lane.staging.reset();
   float ms = 0.f;
   cuda_check(cudaEventElapsedTime(&ms, e0, e1), "event");
+  if (lane.origin) {
+    float a = 0.f, b = 0.f;
+    cuda_check(cudaEventElapsedTime(&a, lane.origin, e0), "event");
+    cuda_check(cudaEventElapsedTime(&b, lane.origin, e1), "event");
+    lane.intervals.push_back({a, b});
+    if (std::getenv("SSG_TRACE_LANES"))
+      std::fprintf(stderr, "lane %p launch [%.1f, %.1f] ms units %zu\n", (void*)&lane, a, b,
+                   L.units.size());
+  }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   if (const char* dump = std::getenv("SSG_DUMP_UNITS")) {
+    std::lock_guard<std::mutex> lk(g_dump_mu);
     // diagnostics: one line per unit (launch, unit, config, n, R, iterations, cycles, qps)
     FILE* f = std::fopen(dump, "a");
     if (f) {
@@ -452,12 +504,17 @@ void fail(Candidate& C, const SimUnitOut& o) {
 struct SweepKnobs {
   int ladder = 4;  // doubling rates probed per round
   int depth = 3;   // bisection levels probed per round (2^depth - 1 rates)
+  int lanes = 1;   // candidate groups advancing independently (streams); measured: no gain
+                   // (the sweep is issue-bound, not tail-bound), so one lane by default
+  bool block = false;  // groups = contiguous blocks of the capacity order (else dealt)
 };
 
 SweepKnobs knobs_from_env() {
   SweepKnobs k;
   if (const char* s = std::getenv("SSG_SPEC_LADDER")) k.ladder = std::max(1, std::atoi(s));
   if (const char* s = std::getenv("SSG_SPEC_DEPTH")) k.depth = std::max(1, std::atoi(s));
+  if (const char* s = std::getenv("SSG_LANES")) k.lanes = std::max(1, std::atoi(s));
+  if (const char* s = std::getenv("SSG_LANE_BLOCK")) k.block = s[0] == '1';
   return k;
 }
 
@@ -485,7 +542,7 @@ void take_measurement(Candidate& C, const std::vector<SimUnitOut>& out, const Pr
 // measurement at evaluation_fraction x capacity, or the static makespan run).
 // An error inside a probe ends that candidate's evaluation (the reference's
 // exception) unless the probe's abort came first in event order.
-void run_round(SweepBuffers& B, std::vector<Candidate>& cands,
+void run_round(SweepLane& lane, std::vector<Candidate>& cands,
                const std::vector<std::pair<std::size_t, std::vector<double>>>& probes,
                const std::vector<std::pair<std::size_t, double>>& full, bool static_run,
                const ResidentWorkload& w, const CapacitySearchOptions& base) {
@@ -506,7 +563,7 @@ void run_round(SweepBuffers& B, std::vector<Candidate>& cands,
   if (L.probes.empty()) return;
   std::vector<SimUnitOut> out;
   std::vector<double> sel;
-  run_launch(B, L, w, out, sel);
+  run_launch(lane, L, w, out, sel);
   for (std::size_t m = 0; m < L.measured.size(); ++m) {
     const ProbeDesc& p = L.probes[L.measured[m]];
     take_measurement(cands[L.probe_cand[L.measured[m]]], out, p, sel.data() + 3 * m, w);
@@ -541,7 +598,7 @@ void run_round(SweepBuffers& B, std::vector<Candidate>& cands,
     }
   }
   if (redo.probes.empty()) return;
-  run_launch(B, redo, w, out, sel);
+  run_launch(lane, redo, w, out, sel);
   for (std::size_t k = 0; k < redo.probes.size(); ++k) {
     const ProbeDesc& p = redo.probes[k];
     Candidate& C = cands[redo.probe_cand[k]];
@@ -555,6 +612,65 @@ void run_round(SweepBuffers& B, std::vector<Candidate>& cands,
   }
 }
 
+// One candidate group's capacity searches and SLO runs, round after round on
+// its lane.  Rounds: every live candidate's find_capacity is replayed;
+// unanswered rates (plus speculative successors) become probes, and candidates
+// whose capacity resolved get their SLO run in the same launch.
+void run_group(SweepLane& lane, std::vector<Candidate>& cands, const std::vector<std::size_t>& live,
+               const SearchOptions& opts, const ResidentWorkload& w, const SweepKnobs& knobs,
+               std::vector<std::size_t>& measured) {
+  while (true) {
+    std::vector<std::pair<std::size_t, std::vector<double>>> probes;
+    std::vector<std::pair<std::size_t, double>> full;
+    int64_t longest = 1;
+    for (auto k : live) longest = std::max(longest, cands[k].probe_iters);
+    for (auto k : live) {
+      Candidate& C = cands[k];
+      if (C.res.failed() || C.measured) continue;
+      if (!C.done) {
+        try {
+          C.res.capacity_qps = replay_capacity(C.memo, C.copts);
+          C.done = true;  // capacity known
+        } catch (const NeedProbe& need) {
+          // candidates on the critical path (longest probes) speculate deeper,
+          // so their bisection finishes in one round
+          const bool critical = C.probe_iters * 10 >= longest * 9;
+          std::vector<double> qs;
+          speculate(need, C.copts, knobs.ladder, critical ? knobs.depth + 3 : knobs.depth, qs);
+          std::vector<double> fresh;
+          for (double q : qs)
+            if (!C.memo.count(q) && std::find(fresh.begin(), fresh.end(), q) == fresh.end())
+              fresh.push_back(q);
+          probes.push_back({k, fresh});
+          continue;
+        } catch (const Error& e) {
+          C.res.error = e.what();
+          C.res.capacity_qps = 0.0;
+          C.done = true;
+          continue;
+        }
+      }
+      // capacity known: the SLO measurement run at evaluation_fraction of it
+      if (C.res.capacity_qps <= C.copts.min_qps) {
+        C.res.capacity_qps = 0.0;
+        C.res.error = "no feasible arrival rate (scheduling delay above threshold)";
+        continue;
+      }
+      const double q = opts.evaluation_fraction * C.res.capacity_qps;
+      try {
+        require(q > 0.0, "poisson_arrivals: rate must be positive");
+      } catch (const Error& e) {
+        C.res.error = e.what();
+        continue;
+      }
+      full.push_back({k, q});
+      measured.push_back(k);
+    }
+    if (probes.empty() && full.empty()) break;
+    run_round(lane, cands, probes, full, false, w, opts.capacity);
+  }
+}
+
 }  // namespace
 
 struct SearchSession::State {
@@ -564,7 +680,8 @@ struct SearchSession::State {
   std::vector<EstimatorModel> ests;
   Workload w;
   ResidentWorkload rw;
-  SweepBuffers buffers;
+  DeviceBuffer<double> tables;                    // token tables (context stream)
+  std::vector<std::unique_ptr<SweepLane>> lanes;  // grow-only, reused across evaluations
 };
 
 SearchSession::SearchSession(const ModelSpec& spec, const std::vector<Request>& workload,
@@ -637,7 +754,7 @@ std::vector<ConfigResult> SearchSession::evaluate(int shard, int num_shards) {
   const auto& configs = S.configs;
   const auto& ests = S.ests;
   const ResidentWorkload& w = S.rw;
-  SweepBuffers& B = st_->buffers;
+  State& SS = *st_;
   std::vector<ConfigResult> results(configs.size());
   std::vector<Candidate> cands;
   for (std::size_t i = 0; i < configs.size(); ++i) {
@@ -679,7 +796,7 @@ std::vector<ConfigResult> SearchSession::evaluate(int shard, int num_shards) {
       tk.push_back(k);
     }
     if (std::getenv("SSG_NO_TABLES") == nullptr)
-      build_token_tables(tcfg, tests, test_of, B.tables);
+      build_token_tables(tcfg, tests, test_of, SS.tables);
     for (std::size_t i = 0; i < tk.size(); ++i) {
       SimConfig& c = cands[tk[i]].sim;
       c.tab_off = tcfg[i].tab_off;
@@ -771,11 +888,31 @@ std::vector<ConfigResult> SearchSession::evaluate(int shard, int num_shards) {
     }
   }
 
+  // lanes: streams + buffers; every lane waits for the token tables
+  const SweepKnobs knobs = knobs_from_env();
+  const std::size_t nlanes =
+      makespan ? 1 : std::max<std::size_t>(1, std::min<std::size_t>(knobs.lanes, live.size()));
+  while (SS.lanes.size() < nlanes) SS.lanes.push_back(std::make_unique<SweepLane>());
+  auto& ctx = context();
+  cudaEvent_t origin;
+  cuda_check(cudaEventCreate(&origin), "event");
+  cuda_check(cudaEventRecord(origin, ctx.stream), "event");
+  for (std::size_t g = 0; g < nlanes; ++g) {
+    SweepLane& lane = *SS.lanes[g];
+    lane.tables = SS.tables.ptr;
+    lane.origin = origin;
+    lane.intervals.clear();
+    cuda_check(cudaStreamWaitEvent(lane.stream.s, origin, 0), "lane wait");
+  }
+
   if (makespan) {
     std::vector<std::pair<std::size_t, double>> full;
     for (std::size_t k = 0; k < cands.size(); ++k)
       if (!cands[k].done) full.push_back({k, 0.0});
-    run_round(B, cands, {}, full, true, w, opts.capacity);
+    {
+      StreamScope scope(SS.lanes[0]->stream.s);
+      run_round(*SS.lanes[0], cands, {}, full, true, w, opts.capacity);
+    }
     for (const auto& f : full) {
       Candidate& C = cands[f.first];
       if (!C.res.failed()) {
@@ -784,74 +921,73 @@ std::vector<ConfigResult> SearchSession::evaluate(int shard, int num_shards) {
       }
     }
   } else {
-    const SweepKnobs knobs = knobs_from_env();
-    // Rounds: every live candidate's find_capacity is replayed; unanswered rates
-    // (plus speculative successors) become probes, and candidates whose
-    // capacity resolved get their SLO run in the same launch.
-    std::vector<std::size_t> to_measure;
-    while (true) {
-      std::vector<std::pair<std::size_t, std::vector<double>>> probes;
-      std::vector<std::pair<std::size_t, double>> full;
-      int64_t longest = 1;
-      for (auto k : live) longest = std::max(longest, cands[k].probe_iters);
-      for (auto k : live) {
+    // candidate groups, one per lane: ordered by initial guess (lowest rate =
+    // longest probes first), dealt round-robin or in contiguous blocks
+    std::vector<std::size_t> order = live;
+    std::stable_sort(order.begin(), order.end(), [&](std::size_t a, std::size_t b) {
+      return cands[a].copts.initial_guess < cands[b].copts.initial_guess;
+    });
+    std::vector<std::vector<std::size_t>> groups(nlanes);
+    for (std::size_t i = 0; i < order.size(); ++i) {
+      const std::size_t g = knobs.block ? i * nlanes / order.size() : i % nlanes;
+      groups[g].push_back(order[i]);
+    }
+    std::vector<std::vector<std::size_t>> measured(nlanes);
+    std::vector<std::exception_ptr> errors(nlanes);
+    auto body = [&](std::size_t g) {
+      try {
+        cuda_check(cudaSetDevice(ctx.device), "cudaSetDevice");
+        StatsScope stats_scope;
+        StreamScope scope(SS.lanes[g]->stream.s);
+        run_group(*SS.lanes[g], cands, groups[g], opts, w, knobs, measured[g]);
+      } catch (...) {
+        errors[g] = std::current_exception();
+      }
+    };
+    std::vector<std::thread> threads;
+    for (std::size_t g = 1; g < nlanes; ++g) threads.emplace_back(body, g);
+    body(0);
+    for (auto& t : threads) t.join();
+    for (auto& e : errors)
+      if (e) std::rethrow_exception(e);
+    for (const auto& m : measured)
+      for (auto k : m) {
         Candidate& C = cands[k];
-        if (C.res.failed() || C.measured) continue;
-        if (!C.done) {
-          try {
-            C.res.capacity_qps = replay_capacity(C.memo, C.copts);
-            C.done = true;  // capacity known
-          } catch (const NeedProbe& need) {
-            // candidates on the critical path (longest probes) speculate deeper,
-            // so their bisection finishes in one round
-            const bool critical = C.probe_iters * 10 >= longest * 9;
-            std::vector<double> qs;
-            speculate(need, C.copts, knobs.ladder, critical ? knobs.depth + 3 : knobs.depth, qs);
-            std::vector<double> fresh;
-            for (double q : qs)
-              if (!C.memo.count(q) && std::find(fresh.begin(), fresh.end(), q) == fresh.end())
-                fresh.push_back(q);
-            probes.push_back({k, fresh});
-            continue;
-          } catch (const Error& e) {
-            C.res.error = e.what();
-            C.res.capacity_qps = 0.0;
-            C.done = true;
-            continue;
-          }
-        }
-        // capacity known: the SLO measurement run at evaluation_fraction of it
-        if (C.res.capacity_qps <= C.copts.min_qps) {
-          C.res.capacity_qps = 0.0;
-          C.res.error = "no feasible arrival rate (scheduling delay above threshold)";
-          continue;
-        }
-        const double q = opts.evaluation_fraction * C.res.capacity_qps;
+        if (C.res.failed()) continue;
+        C.res.slo_pass = C.res.ttft_p90 <= opts.slos.ttft_p90_max &&
+                         C.res.tbt_p99 <= opts.slos.tbt_p99_max &&
+                         C.res.delay_p99 <= opts.slos.delay_p99_max;
         try {
-          require(q > 0.0, "poisson_arrivals: rate must be positive");
+          C.res.qps_per_dollar = qps_per_dollar(C.res.capacity_qps, C.cluster.gpus_used(),
+                                                hourly_rate(opts.cost, C.res.sku_name));
         } catch (const Error& e) {
           C.res.error = e.what();
-          continue;
         }
-        full.push_back({k, q});
-        to_measure.push_back(k);
       }
-      if (probes.empty() && full.empty()) break;
-      run_round(B, cands, probes, full, false, w, opts.capacity);
+  }
+  // k_simulate busy time: the union of every lane's launch intervals
+  {
+    std::vector<std::pair<float, float>> iv;
+    for (std::size_t g = 0; g < nlanes; ++g) {
+      iv.insert(iv.end(), SS.lanes[g]->intervals.begin(), SS.lanes[g]->intervals.end());
+      SS.lanes[g]->origin = nullptr;
     }
-    for (auto k : to_measure) {
-      Candidate& C = cands[k];
-      if (C.res.failed()) continue;
-      C.res.slo_pass = C.res.ttft_p90 <= opts.slos.ttft_p90_max &&
-                       C.res.tbt_p99 <= opts.slos.tbt_p99_max &&
-                       C.res.delay_p99 <= opts.slos.delay_p99_max;
-      try {
-        C.res.qps_per_dollar = qps_per_dollar(C.res.capacity_qps, C.cluster.gpus_used(),
-                                              hourly_rate(opts.cost, C.res.sku_name));
-      } catch (const Error& e) {
-        C.res.error = e.what();
+    std::sort(iv.begin(), iv.end());
+    double busy = 0.0, a = 0.0, b = 0.0;
+    bool open = false;
+    for (auto [x, y] : iv) {
+      if (!open || x > b) {
+        if (open) busy += b - a;
+        a = x;
+        b = y;
+        open = true;
+      } else {
+        b = std::max<double>(b, y);
       }
     }
+    if (open) busy += b - a;
+    stats().simulate_busy_ms += busy;
+    cudaEventDestroy(origin);
   }
   for (auto& C : cands) results[C.index] = std::move(C.res);
   for (std::size_t i = 0; i < configs.size(); ++i)

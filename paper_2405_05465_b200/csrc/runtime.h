@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstddef>
+#include <cstring>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -41,8 +42,20 @@ void shutdown_context();
 // plain cudaMalloc/cudaFree (A/B only).  Every library kernel and copy runs on the
 // context stream; callers that pass their own stream only read buffers whose
 // upload was synchronised.
-void* device_alloc(std::size_t bytes);
-void device_free(void* p);
+// Buffers are ordered on the stream current for the allocating thread
+// (StreamScope), or the context stream; a buffer is freed on the stream it was
+// allocated on, which is the only stream that uses it.
+void* device_alloc(std::size_t bytes, cudaStream_t s);
+void device_free(void* p, cudaStream_t s);
+cudaStream_t current_stream();  // StreamScope's stream, else the context stream
+
+struct StreamScope {
+  explicit StreamScope(cudaStream_t s);
+  ~StreamScope();
+  StreamScope(const StreamScope&) = delete;
+  StreamScope& operator=(const StreamScope&) = delete;
+  cudaStream_t prev;
+};
 
 // Which glibc contraction this host's libm runs (host_math.cpp).
 int probe_host_math_variant();
@@ -58,20 +71,56 @@ struct RunStats {
   int64_t queries = 0;       // k_predict queries
   double predict_ms = 0.0;
   int64_t h2d_bytes = 0, d2h_bytes = 0;
+  double simulate_busy_ms = 0.0;  // union of k_simulate intervals (launches overlap across streams)
+  void add(const RunStats& o);
 };
+// The calling thread's counters: the process-wide ones, or a StatsScope's
+// private accumulator, merged into the process-wide ones when the scope ends.
 RunStats& stats();
+struct StatsScope {
+  StatsScope();
+  ~StatsScope();
+  StatsScope(const StatsScope&) = delete;
+  StatsScope& operator=(const StatsScope&) = delete;
+  RunStats local;
+  RunStats* prev;
+};
+
+// Pinned host staging for one stream's copies: a bump allocator over pinned
+// chunks, reset after the stream is synchronised.  Copies from pageable memory
+// can hold the issuing thread behind other streams' kernels; the sweep lanes
+// stage through pinned memory so their launches overlap.
+class HostStaging {
+ public:
+  HostStaging() = default;
+  ~HostStaging();
+  HostStaging(const HostStaging&) = delete;
+  HostStaging& operator=(const HostStaging&) = delete;
+  void* take(std::size_t bytes);  // valid until reset()
+  void reset();                   // only after the stream's copies completed
+
+ private:
+  struct Chunk {
+    char* p;
+    std::size_t cap;
+  };
+  std::vector<Chunk> chunks_;
+  std::size_t used_ = 0;  // in the last chunk
+  std::size_t total_ = 0;
+};
 
 // Owning HBM buffer.
 template <typename T>
 struct DeviceBuffer {
   T* ptr = nullptr;
   std::size_t count = 0;
+  cudaStream_t stream = nullptr;  // allocation stream
   DeviceBuffer() = default;
   explicit DeviceBuffer(std::size_t n) { resize(n); }
   ~DeviceBuffer() { release(); }
   DeviceBuffer(const DeviceBuffer&) = delete;
   DeviceBuffer& operator=(const DeviceBuffer&) = delete;
-  DeviceBuffer(DeviceBuffer&& o) noexcept : ptr(o.ptr), count(o.count) {
+  DeviceBuffer(DeviceBuffer&& o) noexcept : ptr(o.ptr), count(o.count), stream(o.stream) {
     o.ptr = nullptr;
     o.count = 0;
   }
@@ -80,6 +129,7 @@ struct DeviceBuffer {
       release();
       ptr = o.ptr;
       count = o.count;
+      stream = o.stream;
       o.ptr = nullptr;
       o.count = 0;
     }
@@ -89,11 +139,12 @@ struct DeviceBuffer {
     if (n <= count && ptr) return;
     release();
     if (n == 0) return;
-    ptr = static_cast<T*>(device_alloc(n * sizeof(T)));
+    stream = current_stream();
+    ptr = static_cast<T*>(device_alloc(n * sizeof(T), stream));
     count = n;
   }
   void release() {
-    if (ptr) device_free(ptr);
+    if (ptr) device_free(ptr, stream);
     ptr = nullptr;
     count = 0;
   }
@@ -103,6 +154,21 @@ struct DeviceBuffer {
     stats().h2d_bytes += static_cast<int64_t>(n * sizeof(T));
   }
   void upload(const std::vector<T>& v, cudaStream_t s) { upload(v.data(), v.size(), s); }
+  void upload(const std::vector<T>& v, cudaStream_t s, HostStaging& st) {
+    resize(v.size());
+    if (v.empty()) return;
+    void* p = st.take(v.size() * sizeof(T));
+    std::memcpy(p, v.data(), v.size() * sizeof(T));
+    cuda_check(cudaMemcpyAsync(ptr, p, v.size() * sizeof(T), cudaMemcpyHostToDevice, s), "H2D");
+    stats().h2d_bytes += static_cast<int64_t>(v.size() * sizeof(T));
+  }
+  // D2H into staging; the caller copies out of the returned pointer after syncing s
+  const T* download_staged(std::size_t n, cudaStream_t s, HostStaging& st) const {
+    T* p = static_cast<T*>(st.take(n * sizeof(T)));
+    if (n) cuda_check(cudaMemcpyAsync(p, ptr, n * sizeof(T), cudaMemcpyDeviceToHost, s), "D2H");
+    stats().d2h_bytes += static_cast<int64_t>(n * sizeof(T));
+    return p;
+  }
   void download(T* dst, std::size_t n, cudaStream_t s) const {
     if (n) cuda_check(cudaMemcpyAsync(dst, ptr, n * sizeof(T), cudaMemcpyDeviceToHost, s), "D2H");
     stats().d2h_bytes += static_cast<int64_t>(n * sizeof(T));

@@ -6,7 +6,9 @@
 #include "sim_device.h"
 #include "ssg_device.h"
 
+#ifndef SSG_SIM_WARPS
 #define SSG_SIM_WARPS 2  // warps per block: units differ wildly in length, keep blocks small
+#endif
 
 struct SimLaunch {
   const SimConfig* configs;
