@@ -93,6 +93,24 @@ int ssg_predict_batch(const ssg_estimator* e, const char* model_spec_json, int64
                       const int64_t* d_off, const int64_t* d_ctx, double* seconds,
                       double* flops, ssg_status* st);
 
+/* ---- workload (host) ---------------------------------------------------- */
+/* The inputs that feed simulations and probes, bit-identical to the
+ * reference's libstdc++ draws.  Host code: these run once per trace. */
+/* synth_trace (workload.hpp:213-247) from a DistConfig document
+ * (parse_dist_config, workload.hpp:169-210): n request lengths, ids 0..n-1. */
+int ssg_synth_trace(const char* dist_json, size_t n, uint64_t seed, int64_t* prefill,
+                    int64_t* decode, ssg_status* st);
+/* poisson_arrivals (workload.hpp:93-104): the arrival times of n requests. */
+int ssg_poisson_arrivals(size_t n, double rate_qps, uint64_t seed, double* arrivals,
+                         ssg_status* st);
+/* cap_total_length (workload.hpp:109-121), in place over n requests. */
+int ssg_cap_total_length(size_t n, int64_t* prefill, int64_t* decode, int64_t max_total,
+                         ssg_status* st);
+/* load_trace (workload.hpp:33-78) of CSV text: *out receives JSON
+ * {"id": [...], "arrival": [...] | null, "prefill": [...], "decode": [...]}
+ * in the reference's order (stable-sorted by arrival); free with ssg_free. */
+int ssg_load_trace(const char* csv_text, char** out, ssg_status* st);
+
 /* ---- engine ------------------------------------------------------------ */
 /* run_simulation + build_report (sim.hpp:135-320, metrics.hpp:106-126) of one
  * cluster over one trace (arrays in trace order).  cluster_json is a cluster

@@ -39,6 +39,7 @@ def lib():
                              C.c_size_t, C.c_int],
             "ref_search": [C.c_char_p, C.c_int],
             "ref_evaluate_sample": [C.c_char_p, P, C.c_size_t, C.c_int],
+            "ref_workload": [C.c_char_p],
         }.items():
             fn = getattr(L, name)
             fn.restype = C.c_void_p
@@ -155,3 +156,14 @@ def search(config_path: str, workers: int = 1) -> dict:
 def evaluate_sample(config_path: str, indices, workers: int) -> dict:
     idx = np.ascontiguousarray(indices, dtype=np.int64)
     return _text(lib().ref_evaluate_sample(config_path.encode(), _p(idx), len(idx), workers))
+
+
+def workload(op: str, **kw) -> dict:
+    """synth_trace / poisson_arrivals / cap_total_length / load_trace of the
+    reference (workload.hpp:33-247).  Doubles come back as float64 arrays."""
+    kw["op"] = op
+    j = _text(lib().ref_workload(json.dumps(kw).encode()))
+    for k in ("arrivals", "arrival"):
+        if j.get(k) is not None:
+            j[k] = np.array(j[k], dtype=np.uint64).view(np.float64)
+    return j

@@ -12,6 +12,8 @@
 //   ref_simulate         run_simulation + build_report + batch log (sim.hpp:135, metrics.hpp:106)
 //   ref_search           load_search_config + run_search + writers (config.hpp:111, search.hpp:369)
 //   ref_evaluate_sample  evaluate_config over a subset of configs (search.hpp:294), timed
+//   ref_workload         synth_trace / poisson_arrivals / cap_total_length / load_trace
+//                        (workload.hpp:33-247); request and answer as JSON
 //
 // Nothing in the product (paper_2405_05465_b200/) links or loads this file.
 // Built with the reference's own flags: -std=gnu++20 -O3 -DNDEBUG, no -march.
@@ -28,6 +30,7 @@
 #include "servesim/metrics.hpp"
 #include "servesim/search.hpp"
 #include "servesim/sim.hpp"
+#include "servesim/workload.hpp"
 
 using namespace servesim;
 using nlohmann::json;
@@ -325,6 +328,70 @@ char* ref_evaluate_sample(const char* search_config_path, const int64_t* idx, si
     j["seconds"] = secs;
     j["num_configs_total"] = configs.size();
     return j.dump();
+  });
+}
+
+// {"op": "synth", "dist": {...}, "n": n, "seed": s} -> {"prefill": [...], "decode": [...]}
+// {"op": "poisson", "n": n, "rate": q, "seed": s}  -> {"arrivals": [...]}
+// {"op": "cap", "prefill": [...], "decode": [...], "max_total": m} -> {"prefill", "decode"}
+// {"op": "load_trace", "text": csv} -> {"id", "arrival" (null when absent), "prefill", "decode"}
+// Doubles travel as their IEEE-754 bit patterns (uint64) so they compare exactly.
+char* ref_workload(const char* request_json) {
+  return wrap([&] {
+    const json q = json::parse(request_json);
+    const std::string op = q.at("op").get<std::string>();
+    std::vector<Request> reqs;
+    json out;
+    auto lengths = [&](const std::vector<Request>& rs) {
+      std::vector<std::int64_t> pre, dec, ids;
+      for (const auto& r : rs) {
+        pre.push_back(r.prefill_tokens);
+        dec.push_back(r.decode_tokens);
+        ids.push_back(r.id);
+      }
+      out["prefill"] = pre;
+      out["decode"] = dec;
+      out["id"] = ids;
+    };
+    auto bits = [](double v) {
+      std::uint64_t u;
+      std::memcpy(&u, &v, 8);
+      return u;
+    };
+    if (op == "synth") {
+      lengths(synth_trace(parse_dist_config(q.at("dist")), q.at("n").get<std::size_t>(),
+                          q.at("seed").get<std::uint64_t>()));
+    } else if (op == "poisson") {
+      std::vector<Request> rs(q.at("n").get<std::size_t>());
+      rs = poisson_arrivals(std::move(rs), q.at("rate").get<double>(), q.at("seed").get<std::uint64_t>());
+      std::vector<std::uint64_t> a;
+      for (const auto& r : rs) a.push_back(bits(r.arrival_time));
+      out["arrivals"] = a;
+    } else if (op == "cap") {
+      const auto pre = q.at("prefill").get<std::vector<std::int64_t>>();
+      const auto dec = q.at("decode").get<std::vector<std::int64_t>>();
+      for (std::size_t i = 0; i < pre.size(); ++i) {
+        Request r;
+        r.id = static_cast<std::int64_t>(i);
+        r.prefill_tokens = pre[i];
+        r.decode_tokens = dec[i];
+        reqs.push_back(r);
+      }
+      lengths(cap_total_length(std::move(reqs), q.at("max_total").get<std::int64_t>()));
+    } else if (op == "load_trace") {
+      const auto rs = load_trace(q.at("text").get<std::string>());
+      lengths(rs);
+      if (!rs.empty() && rs.front().has_arrival()) {
+        std::vector<std::uint64_t> a;
+        for (const auto& r : rs) a.push_back(bits(r.arrival_time));
+        out["arrival"] = a;
+      } else {
+        out["arrival"] = nullptr;
+      }
+    } else {
+      throw Error("ref_workload: unknown op " + op);
+    }
+    return out.dump();
   });
 }
 

@@ -127,6 +127,37 @@ class Estimator:
             pass
 
 
+def synth_trace(dist: dict, n: int, seed: int):
+    """synth_trace (workload.hpp:213-247): (prefill, decode) int64 arrays of n requests."""
+    pre = np.zeros(n, dtype=np.int64)
+    dec = np.zeros(n, dtype=np.int64)
+    _ffi.call("ssg_synth_trace", json.dumps(dist).encode(), n, seed, _ptr(pre), _ptr(dec))
+    return pre, dec
+
+
+def poisson_arrivals(n: int, rate_qps: float, seed: int) -> np.ndarray:
+    """poisson_arrivals (workload.hpp:93-104): arrival times of n requests."""
+    out = np.zeros(n, dtype=np.float64)
+    _ffi.call("ssg_poisson_arrivals", n, rate_qps, seed, _ptr(out))
+    return out
+
+
+def cap_total_length(prefill, decode, max_total: int):
+    """cap_total_length (workload.hpp:109-121): capped copies of the lengths."""
+    pre = np.array(prefill, dtype=np.int64)
+    dec = np.array(decode, dtype=np.int64)
+    _ffi.call("ssg_cap_total_length", len(pre), _ptr(pre), _ptr(dec), max_total)
+    return pre, dec
+
+
+def load_trace(csv_text: str) -> dict:
+    """load_trace (workload.hpp:33-78): {"id", "arrival" (or None), "prefill", "decode"}."""
+    out = C.c_void_p()
+    _ffi.call("ssg_load_trace", csv_text.encode(), C.byref(out))
+    j = json.loads(_ffi.take_text(out))
+    return {k: (None if j[k] is None else np.array(j[k])) for k in ("id", "arrival", "prefill", "decode")}
+
+
 def simulate(cluster: dict, estimator: Estimator, ids, arrivals, prefill, decode,
              record_batches: bool = False, abort_delay: float = 0.0, abort_max_late: int = 0,
              static_mode: bool = False) -> dict:

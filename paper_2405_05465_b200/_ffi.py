@@ -69,6 +69,10 @@ _SIGNATURES = {
                                      C.POINTER(Status)]),
     "ssg_predict_batch": (C.c_int, [P, C.c_char_p, C.c_int64, C.c_size_t, P, P, P, P, P, P, P,
                                     C.POINTER(Status)]),
+    "ssg_synth_trace": (C.c_int, [C.c_char_p, C.c_size_t, C.c_uint64, P, P, C.POINTER(Status)]),
+    "ssg_poisson_arrivals": (C.c_int, [C.c_size_t, C.c_double, C.c_uint64, P, C.POINTER(Status)]),
+    "ssg_cap_total_length": (C.c_int, [C.c_size_t, P, P, C.c_int64, C.POINTER(Status)]),
+    "ssg_load_trace": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(Status)]),
     "ssg_simulate": (C.c_int, [C.c_char_p, P, C.c_size_t, P, P, P, P, C.c_int, C.c_double,
                                C.c_size_t, C.c_int, C.POINTER(C.c_void_p), C.POINTER(Status)]),
     "ssg_search": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.POINTER(C.c_void_p),

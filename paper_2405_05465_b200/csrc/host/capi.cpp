@@ -4,6 +4,7 @@
 // InternalError -> 2, CUDA failures -> 3.
 #include "ssg.h"
 
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
@@ -297,6 +298,63 @@ int ssg_simulate(const char* cluster_json, const ssg_estimator* e, size_t n, con
       }
       j["batches"] = std::move(log);
     }
+    *out = dup_text(j.dump(), nullptr);
+  });
+}
+
+int ssg_synth_trace(const char* dist_json, size_t n, uint64_t seed, int64_t* prefill,
+                    int64_t* decode, ssg_status* st) {
+  return guarded(st, [&] {
+    const auto reqs = synth_trace(parse_dist_config_text(dist_json), n, seed);
+    for (size_t i = 0; i < n; ++i) {
+      prefill[i] = reqs[i].prefill_tokens;
+      decode[i] = reqs[i].decode_tokens;
+    }
+  });
+}
+
+int ssg_poisson_arrivals(size_t n, double rate_qps, uint64_t seed, double* arrivals, ssg_status* st) {
+  return guarded(st, [&] {
+    const auto reqs = poisson_arrivals(std::vector<Request>(n), rate_qps, seed);
+    for (size_t i = 0; i < n; ++i) arrivals[i] = reqs[i].arrival_time;
+  });
+}
+
+int ssg_cap_total_length(size_t n, int64_t* prefill, int64_t* decode, int64_t max_total,
+                         ssg_status* st) {
+  return guarded(st, [&] {
+    std::vector<Request> reqs(n);
+    for (size_t i = 0; i < n; ++i) {
+      reqs[i].prefill_tokens = prefill[i];
+      reqs[i].decode_tokens = decode[i];
+    }
+    reqs = cap_total_length(std::move(reqs), max_total);
+    for (size_t i = 0; i < n; ++i) {
+      prefill[i] = reqs[i].prefill_tokens;
+      decode[i] = reqs[i].decode_tokens;
+    }
+  });
+}
+
+int ssg_load_trace(const char* csv_text, char** out, ssg_status* st) {
+  return guarded(st, [&] {
+    const auto reqs = load_trace(csv_text);
+    nlohmann::json j;
+    std::vector<int64_t> id, pre, dec;
+    std::vector<double> arr;
+    for (const auto& r : reqs) {
+      id.push_back(r.id);
+      pre.push_back(r.prefill_tokens);
+      dec.push_back(r.decode_tokens);
+      arr.push_back(r.arrival_time);
+    }
+    j["id"] = id;
+    j["prefill"] = pre;
+    j["decode"] = dec;
+    if (!reqs.empty() && !std::isnan(reqs.front().arrival_time))
+      j["arrival"] = arr;
+    else
+      j["arrival"] = nullptr;
     *out = dup_text(j.dump(), nullptr);
   });
 }
