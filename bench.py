@@ -134,6 +134,18 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
+def profiled_traffic(kernel: str) -> dict:
+    """DRAM traffic of one captured launch of `kernel` (ncu --set full,
+    dram__bytes_read.sum + dram__bytes_write.sum), with that same launch's
+    algorithmic bytes, from the committed profile summary (profiles/traffic.json)."""
+    try:
+        j = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))[kernel]
+        return {"traffic": j["dram_bytes"], "traffic_launch": j["launch"],
+                "traffic_alg_bytes": j["alg_bytes"], "traffic_source": j["source"]}
+    except Exception:
+        return {}
+
+
 def cpu_baseline(cfg_path: str, n_configs: int, sample: int) -> dict:
     """The compiled reference evaluating a strided sample of the grid on all host threads."""
     from oracle import ref
@@ -239,6 +251,72 @@ def predictor_bench(torch, dev, nq: int, steps: int, warmup: int) -> dict:
             "cpu_baseline": base}
 
 
+def simulate_bench(steps: int) -> dict:
+    """cfg #1 (LLaMA2-7B A100 TP1 vLLM bs128, 1K fixture, poisson qps 10 seed 5) and
+    cfg #2 (LLaMA2-70B H100 TP4 Sarathi cs512, 10K Zipf, poisson qps 10 seed 0):
+    run_simulation + build_report through ssg_simulate_run (host arrays in,
+    per-request records, emission times and the report out), the k_simulate
+    device time from the library's CUDA events, and the compiled reference's
+    run_simulation + build_report on one host core on the same inputs."""
+    import numpy as np
+
+    import paper_2405_05465_b200 as ssg
+    from paper_2405_05465_b200 import catalog
+
+    cases = {
+        "cfg1": ("llama2_7b", "a100_80g", dict(tp=1, policy="vllm", max_batch_size=128),
+                 lambda: tuple(catalog.fixture_chat_1k().T), 10.0, 5,
+                 "cfg #1: LLaMA2-7B A100 TP1 vLLM bs128, 1K chat fixture, poisson qps 10 seed 5"),
+        "cfg2": ("llama2_70b", "h100_80g", dict(tp=4, policy="sarathi_serve", max_batch_size=128,
+                                                chunk_size=512),
+                 lambda: ssg.synth_trace(catalog.zipf_histogram(), 10000, 42), 10.0, 0,
+                 "cfg #2: LLaMA2-70B H100 TP4 Sarathi-Serve cs512 bs128, 10K Zipf (seed 42), "
+                 "poisson qps 10 seed 0"),
+    }
+    out = {}
+    for key, (model, devname, par, lengths, qps, seed, label) in cases.items():
+        est = ssg.Estimator.train(catalog.MODELS[model], catalog.DEVICES[devname],
+                                  [par["tp"]], "interp", seed=0)
+        pre, dec = (np.asarray(a, dtype=np.int64) for a in lengths())
+        n = len(pre)
+        ids = np.arange(n, dtype=np.int64)
+        arr = ssg.poisson_arrivals(n, qps, seed)
+        cluster = catalog.cluster_doc(model, devname, **par)
+        run = ssg.simulate_run(cluster, est, ids, arr, pre, dec)  # warm; output buffers reused
+        walls, kern = [], []
+        for _ in range(max(1, steps)):
+            ssg.stats_reset()
+            t0 = time.perf_counter()
+            ssg.simulate_run(cluster, est, ids, arr, pre, dec, out=run)
+            walls.append(time.perf_counter() - t0)
+            st = ssg.stats()
+            kern.append(st["simulate_ms"] / 1e3)
+        iters = st["iterations"]
+        entry = {"workload": label, "requests": n, "iterations": iters,
+                 "value": 1.0 / min(walls), "unit": "simulations/s",
+                 "e2e_s": min(walls), "kernel_s": min(kern),
+                 "us_per_iteration_kernel": 1e6 * min(kern) / iters if iters else None,
+                 "h2d_bytes": st["h2d_bytes"], "d2h_bytes": st["d2h_bytes"],
+                 "simulated_span_s": run.report.simulated_span}
+        try:
+            from oracle import ref
+
+            theirs = ref.simulate_timed(ref.Estimator(est.to_json()), cluster, ids, arr, pre, dec)
+            secs = theirs["seconds"]
+            entry["cpu_baseline"] = {"value": 1.0 / secs, "unit": "simulations/s", "cores": 1,
+                                     "kind": "reference",
+                                     "sample": "run_simulation + build_report of the same trace on "
+                                               "1 thread, %.3f s" % secs}
+            entry["identical_to_reference"] = bool(
+                np.array_equal(theirs["completion"].view(np.uint64), run.completion.view(np.uint64))
+                and theirs["ttft_p90"] == run.report.ttft.p90
+                and theirs["tbt_p99"] == run.report.tbt.p99)
+        except Exception as e:  # noqa: BLE001
+            entry["cpu_baseline"] = {"unavailable": str(e)[:200]}
+        out[key] = entry
+    return out
+
+
 def main():
     a = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -317,7 +395,9 @@ def main():
     e2e_steps = max(1, a.steps)
 
     peak, peak_kind = measured_peak()
-    sim_s = st["simulate_ms"] / 1e3
+    # k_simulate device time: the union of its launch intervals (equal to the sum
+    # of launch times with one sweep lane; launches overlap with more)
+    sim_s = st["simulate_busy_ms"] / 1e3
     alg_bytes = st["predictor_bytes"] + st["entry_bytes"]
     achieved = alg_bytes / sim_s / 1e9 if sim_s > 0 else 0.0
     launches = (st["launches_simulate"] + st["launches_select"] + st["launches_predict"]
@@ -335,12 +415,15 @@ def main():
         "e2e": {"value": n_configs / (sum(e2e_times) / len(e2e_times)), "unit": UNIT,
                 "h2d_bytes_per_step": st_e2e["h2d_bytes"] // e2e_steps,
                 "d2h_bytes_per_step": st_e2e["d2h_bytes"] // e2e_steps},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak if peak else None, "traffic": None,
-                     "kernel": "k_simulate", "peak_kind": peak_kind,
-                     "alg_bytes_per_step": alg_bytes / a.steps,
-                     "kernel_ms_per_step": st["simulate_ms"] / a.steps,
-                     "kernel_share_of_step": (st["simulate_ms"] / a.steps) / (t_step * 1e3)},
+        "roofline": dict({"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                          "frac": achieved / peak if peak else None, "traffic": None,
+                          "kernel": "k_simulate", "peak_kind": peak_kind,
+                          "launches_per_step": st["launches_simulate"] / a.steps,
+                          "alg_bytes_per_launch": alg_bytes / max(1, st["launches_simulate"]),
+                          "alg_bytes_per_step": alg_bytes / a.steps,
+                          "kernel_ms_per_step": st["simulate_busy_ms"] / a.steps,
+                          "kernel_share_of_step": (st["simulate_busy_ms"] / a.steps) / (t_step * 1e3)},
+                         **profiled_traffic("k_simulate")),
         "gpu_launches": launches,
         "work": {k: st[k] // a.steps for k in ("units", "iterations", "entries", "events")},
         "clocks": clk,
@@ -352,6 +435,11 @@ def main():
             result["predictor"] = predictor_bench(torch, dev, a.predictor_queries, a.steps, a.warmup)
         except Exception as e:  # noqa: BLE001
             result["predictor"] = {"error": str(e)}
+    if rank == 0 and world == 1 and not a.quick:
+        try:
+            result["simulate"] = simulate_bench(a.steps)
+        except Exception as e:  # noqa: BLE001
+            result["simulate"] = {"error": str(e)[:300]}
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         try:
             result["cpu_baseline"] = cpu_baseline(cfg_path, n_configs, a.cpu_sample)

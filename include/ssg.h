@@ -125,6 +125,30 @@ int ssg_simulate(const char* cluster_json, const ssg_estimator* e, size_t n, con
                  int record_batches, double abort_delay, size_t abort_max_late, int static_mode,
                  char** out, ssg_status* st);
 
+/* MetricSummary (metrics.hpp:17-25) and the report of one simulation
+ * (MetricsReport + ClusterMetrics, metrics.hpp:27-60) in fixed layout. */
+typedef struct ssg_metric_summary {
+  double mean, p50, p90, p95, p99;
+} ssg_metric_summary;
+typedef struct ssg_sim_report {
+  double simulated_span, total_model_flops;
+  int64_t num_devices;
+  ssg_metric_summary scheduling_delay, ttft, tbt, e2e, normalized;
+  double mfu, kv_utilization_peak, busy_fraction;
+  int64_t preemptions;
+} ssg_sim_report;
+/* run_simulation + build_report (sim.hpp:135-320, metrics.hpp:106-126) with
+ * binary outputs: the call a C/C++ caller makes (no JSON).  Per-request arrays
+ * are in trace order and each may be NULL; emissions receives request i's
+ * decode[i] emission times back to back in trace order (sum(decode) slots) or
+ * may be NULL.  Errors as ssg_simulate; a run that hits the probe abort
+ * returns status 1 with the reference's ProbeInfeasible message. */
+int ssg_simulate_run(const char* cluster_json, const ssg_estimator* e, size_t n, const int64_t* ids,
+                     const double* arrivals, const int64_t* prefill, const int64_t* decode,
+                     int static_mode, double* first_scheduled, double* first_token,
+                     double* completion, int64_t* restarts, double* emissions,
+                     ssg_sim_report* report, ssg_status* st);
+
 /* ---- search (Vidur-Search) --------------------------------------------- */
 /* One evaluated candidate, fixed-size so shards can be all-gathered as bytes.
  * Fields as ConfigResult (search.hpp:182-194); `index` is the enumeration

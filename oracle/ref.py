@@ -40,6 +40,7 @@ def lib():
             "ref_search": [C.c_char_p, C.c_int],
             "ref_evaluate_sample": [C.c_char_p, P, C.c_size_t, C.c_int],
             "ref_workload": [C.c_char_p],
+            "ref_simulate_timed": [C.c_char_p, P, C.c_size_t, P, P, P, P],
         }.items():
             fn = getattr(L, name)
             fn.restype = C.c_void_p
@@ -147,6 +148,18 @@ class Estimator:
         return _text(lib().ref_simulate(json.dumps(cluster).encode(), self.h, len(ids), _p(ids),
                                         _p(arr), _p(pre), _p(dec), int(record_batches),
                                         abort_delay, abort_max_late, int(static_mode)))
+
+
+def simulate_timed(est: "Estimator", cluster: dict, ids, arrivals, prefill, decode) -> dict:
+    """run_simulation + build_report on one thread, timed inside the reference build."""
+    ids = np.ascontiguousarray(ids, dtype=np.int64)
+    arr = np.ascontiguousarray(arrivals, dtype=np.float64)
+    pre = np.ascontiguousarray(prefill, dtype=np.int64)
+    dec = np.ascontiguousarray(decode, dtype=np.int64)
+    j = _text(lib().ref_simulate_timed(json.dumps(cluster).encode(), est.h, len(ids), _p(ids),
+                                       _p(arr), _p(pre), _p(dec)))
+    j["completion"] = np.array(j.pop("completion_bits"), dtype=np.uint64).view(np.float64)
+    return j
 
 
 def search(config_path: str, workers: int = 1) -> dict:

@@ -270,6 +270,36 @@ char* ref_simulate(const char* cluster_json, void* est, size_t n, const int64_t*
   });
 }
 
+// run_simulation (default SimOptions) + build_report, timed on one thread: the
+// CPU baseline of a single simulation.  Returns the seconds, the report and the
+// per-request completion times as IEEE-754 bit patterns.
+char* ref_simulate_timed(const char* cluster_json, void* est, size_t n, const int64_t* ids,
+                         const double* arrivals, const int64_t* prefill, const int64_t* decode) {
+  return wrap([&] {
+    ClusterConfig c = cluster_from(json::parse(cluster_json));
+    std::vector<Request> trace(n);
+    for (size_t i = 0; i < n; ++i) trace[i] = Request{ids[i], arrivals[i], prefill[i], decode[i]};
+    const auto t0 = std::chrono::steady_clock::now();
+    SimulationResult r = run_simulation(c, trace, *static_cast<EstimatorModel*>(est), SimOptions{});
+    auto rep = build_report(r, false);
+    const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    std::vector<std::uint64_t> done;
+    for (const auto& q : r.requests) {
+      std::uint64_t u;
+      std::memcpy(&u, &q.completion, 8);
+      done.push_back(u);
+    }
+    json out;
+    out["seconds"] = secs;
+    out["completion_bits"] = done;
+    out["ttft_p90"] = rep.ttft.p90;
+    out["tbt_p99"] = rep.tbt.p99;
+    out["scheduling_delay_p99"] = rep.scheduling_delay.p99;
+    out["simulated_span"] = r.simulated_span;
+    return out.dump();
+  });
+}
+
 // Full search from a search-config file; workers host threads.
 char* ref_search(const char* search_config_path, int workers) {
   return wrap([&] {

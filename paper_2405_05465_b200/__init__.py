@@ -158,6 +158,45 @@ def load_trace(csv_text: str) -> dict:
     return {k: (None if j[k] is None else np.array(j[k])) for k in ("id", "arrival", "prefill", "decode")}
 
 
+class SimulationRun:
+    """Binary outputs of ssg_simulate_run: per-request arrays in trace order, the
+    emission times (CSR by decode length), and the report."""
+
+    def __init__(self, n: int, total_decode: int, pinned=None):
+        alloc = pinned or (lambda k, dt: np.empty(k, dtype=dt))
+        self.first_scheduled = alloc(n, np.float64)
+        self.first_token = alloc(n, np.float64)
+        self.completion = alloc(n, np.float64)
+        self.restarts = alloc(n, np.int64)
+        self.emissions = alloc(max(1, total_decode), np.float64)
+        self.report = _ffi.SimReport()
+
+    def report_dict(self) -> dict:
+        r = self.report
+        out = {k: getattr(r, k) for k in ("simulated_span", "total_model_flops", "num_devices", "mfu",
+                                          "kv_utilization_peak", "busy_fraction", "preemptions")}
+        for k in ("scheduling_delay", "ttft", "tbt", "e2e", "normalized"):
+            m = getattr(r, k)
+            out[k] = {q: getattr(m, q) for q in ("mean", "p50", "p90", "p95", "p99")}
+        return out
+
+
+def simulate_run(cluster: dict, estimator: Estimator, ids, arrivals, prefill, decode,
+                 static_mode: bool = False, out: Optional[SimulationRun] = None) -> SimulationRun:
+    """run_simulation + build_report through ssg_simulate_run (binary outputs)."""
+    ids = np.ascontiguousarray(ids, dtype=np.int64)
+    arr = np.ascontiguousarray(arrivals, dtype=np.float64)
+    pre = np.ascontiguousarray(prefill, dtype=np.int64)
+    dec = np.ascontiguousarray(decode, dtype=np.int64)
+    if out is None:
+        out = SimulationRun(len(ids), int(dec.sum()))
+    _ffi.call("ssg_simulate_run", json.dumps(cluster).encode(), estimator.handle, len(ids), _ptr(ids),
+              _ptr(arr), _ptr(pre), _ptr(dec), int(static_mode), _ptr(out.first_scheduled),
+              _ptr(out.first_token), _ptr(out.completion), _ptr(out.restarts), _ptr(out.emissions),
+              C.byref(out.report))
+    return out
+
+
 def simulate(cluster: dict, estimator: Estimator, ids, arrivals, prefill, decode,
              record_batches: bool = False, abort_delay: float = 0.0, abort_max_late: int = 0,
              static_mode: bool = False) -> dict:

@@ -73,6 +73,8 @@ _SIGNATURES = {
     "ssg_poisson_arrivals": (C.c_int, [C.c_size_t, C.c_double, C.c_uint64, P, C.POINTER(Status)]),
     "ssg_cap_total_length": (C.c_int, [C.c_size_t, P, P, C.c_int64, C.POINTER(Status)]),
     "ssg_load_trace": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(Status)]),
+    "ssg_simulate_run": (C.c_int, [C.c_char_p, P, C.c_size_t, P, P, P, P, C.c_int, P, P, P, P, P,
+                                   P, C.POINTER(Status)]),
     "ssg_simulate": (C.c_int, [C.c_char_p, P, C.c_size_t, P, P, P, P, C.c_int, C.c_double,
                                C.c_size_t, C.c_int, C.POINTER(C.c_void_p), C.POINTER(Status)]),
     "ssg_search": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.POINTER(C.c_void_p),
@@ -143,3 +145,15 @@ def take_text(ptr: C.c_void_p) -> str:
     s = C.string_at(ptr.value).decode("utf-8")
     lib().ssg_free(ptr)
     return s
+
+
+class MetricSummary(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("mean", "p50", "p90", "p95", "p99")]
+
+
+class SimReport(C.Structure):
+    _fields_ = ([("simulated_span", C.c_double), ("total_model_flops", C.c_double),
+                 ("num_devices", C.c_int64)]
+                + [(n, MetricSummary) for n in ("scheduling_delay", "ttft", "tbt", "e2e", "normalized")]
+                + [("mfu", C.c_double), ("kv_utilization_peak", C.c_double),
+                   ("busy_fraction", C.c_double), ("preemptions", C.c_int64)])

@@ -249,6 +249,7 @@ int ssg_simulate(const char* cluster_json, const ssg_estimator* e, size_t n, con
       return;
     }
     const SimulationResult& r = so.result;
+    ssg::PhaseTimer timer("ssg_simulate: json");
     nlohmann::json reqs = nlohmann::json::array();
     for (const auto& q : r.requests)
       reqs.push_back({{"id", q.id},
@@ -356,6 +357,54 @@ int ssg_load_trace(const char* csv_text, char** out, ssg_status* st) {
     else
       j["arrival"] = nullptr;
     *out = dup_text(j.dump(), nullptr);
+  });
+}
+
+int ssg_simulate_run(const char* cluster_json, const ssg_estimator* e, size_t n, const int64_t* ids,
+                     const double* arrivals, const int64_t* prefill, const int64_t* decode,
+                     int static_mode, double* first_scheduled, double* first_token,
+                     double* completion, int64_t* restarts, double* emissions,
+                     ssg_sim_report* report, ssg_status* st) {
+  return guarded(st, [&] {
+    ClusterConfig cluster = parse_cluster_inline(cluster_json);
+    std::vector<Request> trace(n);
+    for (size_t i = 0; i < n; ++i) trace[i] = Request{ids[i], arrivals[i], prefill[i], decode[i]};
+    SimulationResult r;
+    try {
+      r = run_simulation(cluster, trace, e->model, SimOptions{});
+    } catch (const ProbeInfeasible& p) {
+      throw Error(p.what());
+    }
+    size_t at = 0;
+    for (size_t i = 0; i < n; ++i) {
+      const RequestRecord& q = r.requests[i];
+      if (first_scheduled) first_scheduled[i] = q.first_scheduled;
+      if (first_token) first_token[i] = q.first_token;
+      if (completion) completion[i] = q.completion;
+      if (restarts) restarts[i] = q.restarts;
+      if (emissions) {
+        std::memcpy(emissions + at, q.emission_times.data(), q.emission_times.size() * sizeof(double));
+        at += q.emission_times.size();
+      }
+    }
+    if (report) {
+      const MetricsReport rep = build_report(r, static_mode != 0);
+      auto put = [](ssg_metric_summary& d, const MetricSummary& m) {
+        d = ssg_metric_summary{m.mean, m.p50, m.p90, m.p95, m.p99};
+      };
+      report->simulated_span = r.simulated_span;
+      report->total_model_flops = r.total_model_flops;
+      report->num_devices = r.num_devices;
+      put(report->scheduling_delay, rep.scheduling_delay);
+      put(report->ttft, rep.ttft);
+      put(report->tbt, rep.tbt);
+      put(report->e2e, rep.e2e);
+      put(report->normalized, rep.normalized);
+      report->mfu = rep.cluster.mfu;
+      report->kv_utilization_peak = rep.cluster.kv_utilization_peak;
+      report->busy_fraction = rep.cluster.busy_fraction;
+      report->preemptions = static_cast<int64_t>(rep.cluster.preemptions);
+    }
   });
 }
 

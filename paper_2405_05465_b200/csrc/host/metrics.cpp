@@ -10,6 +10,7 @@
 #include <sstream>
 
 #include "json.hpp"
+#include "runtime.h"
 #include "select.h"
 #include "servesim_b200.hpp"
 
@@ -46,6 +47,7 @@ MetricSummary summarize(const std::vector<double>& v) {
 }  // namespace
 
 MetricsReport build_report(const SimulationResult& result, bool static_mode) {
+  ssg::PhaseTimer timer("build_report");
   MetricsReport rep;
   std::vector<double> delays, ttfts, tbts, e2es, norms;
   for (const auto& r : result.requests) {

@@ -2,6 +2,8 @@
 #include "runtime.h"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -153,6 +155,21 @@ void device_free(void* p, cudaStream_t s) {
     cudaFreeAsync(p, s);
   else
     cudaFree(p);
+}
+
+namespace {
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+bool timing_on() {
+  static const bool on = std::getenv("SSG_TIMING") != nullptr;
+  return on;
+}
+}  // namespace
+
+PhaseTimer::PhaseTimer(const char* what) : what_(what), t0_(timing_on() ? now_s() : 0.0) {}
+PhaseTimer::~PhaseTimer() {
+  if (timing_on()) std::fprintf(stderr, "[ssg timing] %-28s %9.3f ms\n", what_, 1e3 * (now_s() - t0_));
 }
 
 HostStaging::~HostStaging() {

@@ -441,9 +441,15 @@ void run_launch(SweepLane& lane, ProbeLaunch& L, const ResidentWorkload& w,
     cuda_check(cudaEventElapsedTime(&a, lane.origin, e0), "event");
     cuda_check(cudaEventElapsedTime(&b, lane.origin, e1), "event");
     lane.intervals.push_back({a, b});
-    if (std::getenv("SSG_TRACE_LANES"))
-      std::fprintf(stderr, "lane %p launch [%.1f, %.1f] ms units %zu\n", (void*)&lane, a, b,
-                   L.units.size());
+  }
+  if (std::getenv("SSG_TRACE_LANES")) {
+    int64_t alg = 0, iters = 0;
+    for (const auto& o : out) {
+      alg += o.qbytes + 48 * o.entries;
+      iters += o.iterations;
+    }
+    std::fprintf(stderr, "lane %p launch %.3f ms units %zu iterations %lld alg_bytes %lld\n",
+                 (void*)&lane, ms, L.units.size(), (long long)iters, (long long)alg);
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);

@@ -334,11 +334,25 @@ void run_jobs(const SimJobs& J, SimResults& R, bool want_requests) {
     R.emissions.resize(static_cast<std::size_t>(J.emissions));
     d_emis.download(R.emissions.data(), R.emissions.size(), s);
   }
-  if (J.log_words > 0) {
-    R.log.resize(static_cast<std::size_t>(J.log_words));
-    d_log.download(R.log.data(), R.log.size(), s);
+  {
+    PhaseTimer t("sim: kernel + downloads");
+    cuda_check(cudaStreamSynchronize(s), "simulate");
   }
-  cuda_check(cudaStreamSynchronize(s), "simulate");
+  if (J.log_words > 0) {
+    // only the words each unit wrote (the arena is sized for the worst case)
+    PhaseTimer t("sim: batch log download");
+    R.log.resize(static_cast<std::size_t>(J.log_words));
+    for (std::size_t u = 0; u < J.units.size(); ++u) {
+      const int64_t used = R.out[u].log_used;
+      if (used <= 0) continue;
+      const int64_t off = J.units[u].log_off;
+      cuda_check(cudaMemcpyAsync(R.log.data() + off, d_log.ptr + off,
+                                 static_cast<std::size_t>(used) * sizeof(int64_t),
+                                 cudaMemcpyDeviceToHost, s), "D2H");
+      stats().d2h_bytes += used * static_cast<int64_t>(sizeof(int64_t));
+    }
+    cuda_check(cudaStreamSynchronize(s), "batch log");
+  }
   float ms = 0.f;
   cuda_check(cudaEventElapsedTime(&ms, ev0, ev1), "event");
   cudaEventDestroy(ev0);
@@ -415,7 +429,10 @@ Placement place(const ClusterConfig& cluster, const std::vector<Request>& trace,
   SimJobs& J = P.jobs;
   J.configs.push_back(make_sim_config(cluster, estimator, 0));
   J.ests.push_back(estimator.device().view);
-  build_token_tables(J.configs, J.ests, {&estimator.device()}, P.tables);
+  {
+    PhaseTimer t("sim: token tables");
+    build_token_tables(J.configs, J.ests, {&estimator.device()}, P.tables);
+  }
   J.has_forest = estimator.device().has_forest;
   J.tables = P.tables.ptr;
   const int R = static_cast<int>(cluster.par.num_replicas);
@@ -486,9 +503,14 @@ SimulationOutput run_simulation_logged(const ClusterConfig& cluster,
   // probes with an abort bound need the global event order of late schedules
   bool coupled = cluster.routing != RoutingPolicy::RoundRobin ||
                  (opts.abort_delay_threshold > 0.0 && R > 1);
+  PhaseTimer total("sim: run_simulation");
   Placement P = place(cluster, trace, estimator, opts, coupled);
   SimResults res;
-  run_jobs(P.jobs, res, true);
+  {
+    PhaseTimer t("sim: run_jobs");
+    run_jobs(P.jobs, res, true);
+  }
+  PhaseTimer t_assemble("sim: reassemble");
   int errors = 0;
   for (const auto& o : res.out) errors += o.code != SSG_OK;
   if (errors > 1 && !coupled && R <= kMaxCoupledReplicas) {

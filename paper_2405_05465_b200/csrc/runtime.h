@@ -109,6 +109,19 @@ class HostStaging {
   std::size_t total_ = 0;
 };
 
+// Host phase timing to stderr when SSG_TIMING is set (diagnostics only).
+class PhaseTimer {
+ public:
+  explicit PhaseTimer(const char* what);
+  ~PhaseTimer();
+  PhaseTimer(const PhaseTimer&) = delete;
+  PhaseTimer& operator=(const PhaseTimer&) = delete;
+
+ private:
+  const char* what_;
+  double t0_;
+};
+
 // Owning HBM buffer.
 template <typename T>
 struct DeviceBuffer {

@@ -85,6 +85,39 @@ def test_cfg1_vllm_7b(ssg, ref, qps):
     assert_same(mine, theirs)
 
 
+def baseline_trace(ssg, lengths, qps, seed):
+    """A trace built the reference's way: poisson_arrivals(qps, seed) over the lengths."""
+    pre, dec = lengths
+    n = len(pre)
+    return (np.arange(n, dtype=np.int64), ssg.poisson_arrivals(n, qps, seed),
+            np.asarray(pre, dtype=np.int64), np.asarray(dec, dtype=np.int64))
+
+
+@pytest.mark.parametrize("qps", [5.0, 10.0])
+def test_cfg1_fixture_poisson(ssg, ref, qps):
+    """BASELINE cfg #1 exactly: the 1K chat fixture with poisson_arrivals(qps, seed 5)."""
+    m, t = estimators(ssg, ref, "llama2_7b", "a100_80g", [1])
+    cluster = catalog.cluster_doc("llama2_7b", "a100_80g", policy="vllm", max_batch_size=128)
+    lengths = catalog.fixture_chat_1k()
+    mine, theirs = run_both(ssg, m, t, cluster, baseline_trace(ssg, (lengths[:, 0], lengths[:, 1]), qps, 5))
+    assert_same(mine, theirs)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("qps", [10.0])
+def test_cfg2_sarathi_70b_zipf_10k(ssg, ref, qps):
+    """BASELINE cfg #2 at full size: LLaMA2-70B H100 TP4, Sarathi-Serve chunk 512,
+    the 10K-request Zipf histogram trace (synth seed 42), poisson_arrivals seed 0.
+    Every batch, every emission time and the report agree with the reference."""
+    m, t = estimators(ssg, ref, "llama2_70b", "h100_80g", [4], seed=0)
+    cluster = catalog.cluster_doc("llama2_70b", "h100_80g", tp=4, policy="sarathi_serve",
+                                  max_batch_size=128, chunk_size=512)
+    lengths = ssg.synth_trace(catalog.zipf_histogram(), 10000, 42)
+    mine, theirs = run_both(ssg, m, t, cluster, baseline_trace(ssg, lengths, qps, 0))
+    assert_same(mine, theirs)
+    assert len(theirs["requests"]) == 10000
+
+
 TIGHT = dict(catalog.DEVICES["a100_80g"], device_mem=30e9)
 
 
@@ -196,3 +229,27 @@ def test_bbox_error_inside_a_batch(ssg, ref):
         ssg.simulate(cluster, m, ids, arr, pre, dec)
     assert "attn_decode@tp1 outside extrapolation margin" in str(er.value)
     assert str(ei.value) == str(er.value)
+
+
+def test_simulate_run_binary_outputs(ssg, ref):
+    """ssg_simulate_run (binary outputs) agrees with the JSON path and the reference."""
+    m, t = estimators(ssg, ref, "llama2_7b", "a100_80g", [1])
+    cluster = catalog.cluster_doc("llama2_7b", "a100_80g", policy="sarathi_serve", max_batch_size=64,
+                                  chunk_size=256)
+    lengths = catalog.fixture_chat_1k()
+    ids, arr, pre, dec = baseline_trace(ssg, (lengths[:, 0], lengths[:, 1]), 10.0, 5)
+    run = ssg.simulate_run(cluster, m, ids, arr, pre, dec)
+    theirs = t.simulate(cluster, ids, arr, pre, dec)
+    for i, q in enumerate(theirs["requests"]):
+        assert run.first_scheduled[i] == q["first_scheduled"] and run.first_token[i] == q["first_token"]
+        assert run.completion[i] == q["completion"] and run.restarts[i] == q["restarts"]
+    emis = np.concatenate([np.asarray(q["emissions"]) for q in theirs["requests"]])
+    assert np.array_equal(run.emissions[:len(emis)], emis)
+    rep = run.report_dict()
+    for k in ("scheduling_delay", "ttft", "tbt", "e2e", "normalized"):
+        for q in ("p50", "p90", "p95", "p99"):
+            assert rep[k][q] == theirs["report"][k][q], (k, q)
+    assert rep["simulated_span"] == theirs["simulated_span"]
+    assert rep["preemptions"] == theirs["report"]["preemptions"]
+    timed = ref.simulate_timed(t, cluster, ids, arr, pre, dec)
+    assert np.array_equal(timed["completion"], run.completion)
