@@ -50,17 +50,33 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=0, help="configs in the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="small grid (smoke of the bench itself)")
+    ap.add_argument("--workload", default="cfg4", choices=["cfg4", "cfg5"],
+                    help="cfg4: the LLaMA2-70B sweep (450 configs); cfg5: 12 model-trace pairs "
+                         "(4 models x chat/arxiv/bwb-like, 5400 configs)")
     return ap.parse_args()
 
 
-def search_config(directory: str, quick: bool) -> str:
+CFG5_MODELS = ("llama2_7b", "llama2_70b", "internlm_20b", "qwen_72b")
+CFG5_TRACES = ("chat_like", "arxiv_like", "bwb_like")
+
+
+def search_configs(directory: str, quick: bool, workload: str = "cfg4") -> list:
+    """[(name, search-config path)] of the sweeps one bench step runs."""
     from paper_2405_05465_b200 import catalog
 
     if quick:
-        return catalog.write_search_config(directory, model="llama2_70b", tp=(4,), pp=(1,),
-                                           batch_sizes=(64, 256), chunk_sizes=(512,),
-                                           probe_requests=500, num_requests=500)
-    return catalog.write_search_config(directory)  # cfg #4 defaults
+        return [("quick", catalog.write_search_config(
+            directory, model="llama2_70b", tp=(4,), pp=(1,), batch_sizes=(64, 256),
+            chunk_sizes=(512,), probe_requests=500, num_requests=500))]
+    if workload == "cfg5":
+        return [("%s/%s" % (m, t), catalog.write_search_config(os.path.join(directory, m + "_" + t),
+                                                                model=m, workload=t))
+                for m in CFG5_MODELS for t in CFG5_TRACES]
+    return [("llama2_70b/chat_like", catalog.write_search_config(directory))]  # cfg #4 defaults
+
+
+def search_config(directory: str, quick: bool) -> str:
+    return search_configs(directory, quick)[0][1]
 
 
 class Clocks:
@@ -337,24 +353,26 @@ def main():
 
     ssg.init(local)
     tmp = tempfile.mkdtemp(prefix="ssg_bench_")
-    cfg_path = search_config(tmp, a.quick)
-    session = ssg.SearchSession(cfg_path)  # untimed setup: load, train, upload
-    n_configs = session.num_configs
+    sweeps = search_configs(tmp, a.quick, a.workload)
+    cfg_path = sweeps[0][1]
+    # untimed setup per sweep: load, train, upload (resident in HBM)
+    sessions = [ssg.SearchSession(path) for _, path in sweeps]
+    counts = [s.num_configs for s in sessions]
+    n_configs = sum(counts)
     rec_size = ssg.record_size()
 
     from paper_2405_05465_b200.shard import gather_records
 
-    def gather(records: bytes) -> bytes:
-        return gather_records(records, n_configs, rank, world, rec_size, device=dev)
-
     def step(e2e: bool):
-        if e2e:
-            recs = ssg.search_shard(cfg_path, rank, world)
-        else:
-            recs = session.run(rank, world)
-        allrecs = gather(recs)
-        out = ssg.search_finalize(cfg_path, allrecs) if rank == 0 else None
-        return out
+        outs = []
+        for (name, path), session, count in zip(sweeps, sessions, counts):
+            if e2e:
+                recs = ssg.search_shard(path, rank, world)
+            else:
+                recs = session.run(rank, world)
+            allrecs = gather_records(recs, count, rank, world, rec_size, device=dev)
+            outs.append(ssg.search_finalize(path, allrecs) if rank == 0 else None)
+        return outs
 
     def barrier():
         if dist is not None:
@@ -406,11 +424,16 @@ def main():
         "metric": METRIC, "value": n_configs / t_step, "unit": UNIT, "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": t_step * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (chat_like lognormal lengths, synth seed 7; Poisson probes seed 1)",
-        "config": {"workload": "cfg #4: LLaMA2-70B Vidur-Search capacity sweep, %d configs "
-                               "(A100/H100 x tp,pp in {1,2,4} x vLLM/Orca+/Sarathi x bs x cs), "
-                               "2000 probe requests, tol 0.02, interp estimator" % n_configs,
-                   "configs": n_configs, "parallelism": "config shards x%d + 1 NCCL all_gather" % world,
+        "data": "synthetic (%s lognormal lengths, synth seed 7; Poisson probes seed 1)"
+                % ("chat/arxiv/bwb_like" if len(sweeps) > 1 else "chat_like"),
+        "config": {"workload": ("cfg #5: 12 model-trace pairs ({LLaMA2-7B, LLaMA2-70B, InternLM-20B, "
+                                "Qwen-72B} x {chat, arxiv, bwb}-like), %d configs" % n_configs
+                                if a.workload == "cfg5" and not a.quick else
+                                "cfg #4: LLaMA2-70B Vidur-Search capacity sweep, %d configs "
+                                "(A100/H100 x tp,pp in {1,2,4} x vLLM/Orca+/Sarathi x bs x cs), "
+                                "2000 probe requests, tol 0.02, interp estimator" % n_configs),
+                   "configs": n_configs, "sweeps": len(sweeps),
+                   "parallelism": "config shards x%d + 1 NCCL all_gather per sweep" % world,
                    "l2": "flushed (512 MB write) before every timed step"},
         "e2e": {"value": n_configs / (sum(e2e_times) / len(e2e_times)), "unit": UNIT,
                 "h2d_bytes_per_step": st_e2e["h2d_bytes"] // e2e_steps,
@@ -429,25 +452,31 @@ def main():
         "clocks": clk,
     }
     if rank == 0 and outcome is not None:
-        result["optimum"] = outcome.get("best")
-    if rank == 0 and world == 1 and not a.quick:
+        if len(sweeps) == 1:
+            result["optimum"] = outcome[0].get("best")
+        else:
+            result["optimum"] = {name: o.get("best") for (name, _), o in zip(sweeps, outcome)}
+    if rank == 0 and world == 1 and not a.quick and a.workload == "cfg4":
         try:
             result["predictor"] = predictor_bench(torch, dev, a.predictor_queries, a.steps, a.warmup)
         except Exception as e:  # noqa: BLE001
             result["predictor"] = {"error": str(e)}
-    if rank == 0 and world == 1 and not a.quick:
+    if rank == 0 and world == 1 and not a.quick and a.workload == "cfg4":
         try:
             result["simulate"] = simulate_bench(a.steps)
         except Exception as e:  # noqa: BLE001
             result["simulate"] = {"error": str(e)[:300]}
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         try:
-            result["cpu_baseline"] = cpu_baseline(cfg_path, n_configs, a.cpu_sample)
+            result["cpu_baseline"] = cpu_baseline(cfg_path, counts[0], a.cpu_sample)
+            if len(sweeps) > 1:
+                result["cpu_baseline"]["sample"] += " (of the %s sweep)" % sweeps[0][0]
         except Exception as e:  # noqa: BLE001
             result["cpu_baseline"] = {"unavailable": str(e)}
     if rank == 0:
         print(json.dumps(result), flush=True)
-    session.close()
+    for session in sessions:
+        session.close()
     if dist is not None:
         dist.destroy_process_group()
 

@@ -329,6 +329,21 @@ __global__ void k_build_tables(const SimConfig* __restrict__ cfgs, int32_t n, in
   tab[4LL * stride + t] = cm[2];
   tab[5LL * stride + t] = p0;
   tab[6LL * stride + t] = p0f;
+  if (c.tab_cells) {
+    // axis-0 interp cells of the attention models at v0 = t (same device code
+    // as ssg_interp: log1p of the host's glibc variant, then ssg_axis_cell)
+    const double x0 = E.math_fma ? ssg_log1p(tokens, 1) : ssg_log1p(tokens, 0);
+    const int idx[2] = {c.idx_dec, c.idx_pre};
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const SsgModelDesc& md = E.models[c.ops[idx[q]].slot];
+      int32_t lo = 0;
+      double f = 0.0;
+      ssg_axis_cell(E.dpool + md.axis_off[0], md.axis_len[0], x0, &lo, &f);
+      tab[(7LL + 2 * q) * stride + t] = f;
+      tab[(8LL + 2 * q) * stride + t] = (double)lo;
+    }
+  }
   valid[(int64_t)i * stride + t] = (ok_tok ? 1 : 0) | (ok_pre ? 2 : 0);
 }
 
@@ -777,10 +792,10 @@ __device__ void run_unit(Unit& U) {
 }
 
 #ifndef SSG_SIM_MINB
-#define SSG_SIM_MINB 1
+#define SSG_SIM_MINB 6  // 6 blocks x 2 warps per SM: <= 168 registers (measured best, DESIGN 6.4)
 #endif
 template <int FMA, int FOREST, int FAST>
-__global__ void __launch_bounds__(SSG_SIM_WARPS * 32, SSG_SIM_MINB)
+__global__ void __launch_bounds__(SSG_SIM_WARPS * 32, FAST ? 1 : SSG_SIM_MINB)
     k_simulate(SimLaunch L) {
   __shared__ int64_t stats[SSG_SIM_WARPS][SSG_MAX_PP * 6];
   __shared__ double part[SSG_SIM_WARPS][4 * SSG_MAX_PP];
@@ -817,6 +832,7 @@ __global__ void __launch_bounds__(SSG_SIM_WARPS * 32, SSG_SIM_MINB)
   U.fast = L.fast_forward;
   U.group_late = nullptr;
   U.lane = threadIdx.x & 31;
+  U.ax1_hint = 0;
   U.MB = U.cfg->max_batch;
   U.WC = U.u->wait_cap;
   U.rep_stride = 6LL * U.MB + U.WC;
@@ -852,6 +868,7 @@ __global__ void __launch_bounds__(SSG_SIM_WARPS * 32)
   U.smem_part = part[wib];
   U.tables = nullptr;
   U.lane = threadIdx.x & 31;
+  U.ax1_hint = 0;
   U.clock = 0.0;
   U.qbytes = 0;
   if (U.lane == 0) {

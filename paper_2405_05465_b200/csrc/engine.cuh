@@ -66,6 +66,7 @@ struct Unit {
   int64_t iters, entries;
   double clock;
   uint64_t seq;
+  int32_t ax1_hint;    // per lane: last axis-1 interp cell of this lane's attention query
 };
 
 // ---------------------------------------------------------------- workspace
@@ -682,6 +683,60 @@ __device__ SSG_COLD void batch_latency_full(Unit& U, const int64_t* st, int& err
   __syncwarp();
 }
 
+// EstimatorModel::predict of one attention query on a 2-D interpolator whose
+// axis-0 cell at the integer v0 comes from the token tables (lo0, f0 =
+// ssg_axis_cell(log1p(v0)), computed by k_build_tables with the same code) and
+// whose axis-1 search starts from the lane's previous cell: the bracket test
+// below holds exactly when std::upper_bound would land in that cell, so the
+// cell, the fraction and every later operation are the reference's.
+// estimator.hpp:105-123, regressor.hpp:308-341.
+template <int FMA>
+__device__ __forceinline__ int ssg_attn_interp(const SsgEstView& E, const SsgModelDesc& m, double v0,
+                                               double v1, int32_t lo0, double f0, int32_t& hint,
+                                               double* out, int* bad_feature) {
+  if (!(v0 >= m.lower[0] && v0 <= m.upper[0])) {
+    *bad_feature = 0;
+    return SSG_ERR_BBOX;
+  }
+  if (!(v1 >= m.lower[1] && v1 <= m.upper[1])) {
+    *bad_feature = 1;
+    return SSG_ERR_BBOX;
+  }
+  const double x1 = ssg_log1p(v1, FMA);
+  const double* ax = E.dpool + m.axis_off[1];
+  const int32_t n1 = m.axis_len[1];
+  int32_t lo1 = 0;
+  double f1 = 0.0;
+  if (n1 > 1) {
+    int32_t h = hint < 0 ? 0 : (hint > n1 - 2 ? n1 - 2 : hint);
+    const double a = __ldg(ax + h), b = __ldg(ax + h + 1);
+    // upper_bound(x) - 1 clamped to [0, n1 - 2] equals h  <=>
+    //   (h == 0 || ax[h] <= x) && (h == n1 - 2 || x < ax[h + 1])
+    if ((h == 0 || !(x1 < a)) && (h == n1 - 2 || x1 < b)) {
+      lo1 = h;
+      f1 = ssg_clamp((x1 - a) / (b - a), 0.0, 1.0);
+    } else {
+      ssg_axis_cell(ax, n1, x1, &lo1, &f1);
+    }
+    hint = lo1;
+  }
+  const int32_t n0 = m.axis_len[0];
+  const double* vals = E.dpool + m.values_off;
+  const int32_t h0 = n0 == 1 ? 0 : 1;
+  const int32_t h1 = n1 == 1 ? 0 : 1;
+  const double g0 = __dsub_rn(1.0, f0), g1 = __dsub_rn(1.0, f1);
+  const int64_t r0 = (int64_t)lo0 * n1, r1 = (int64_t)(lo0 + h0) * n1;
+  const double w1lo = g1, w1hi = h1 ? f1 : g1;
+  const double w0lo = g0, w0hi = h0 ? f0 : g0;
+  double acc = __dmul_rn(__dmul_rn(w1lo, w0lo), __ldg(vals + r0 + lo1));
+  acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(w1lo, w0hi), __ldg(vals + r1 + lo1)));
+  acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(w1hi, w0lo), __ldg(vals + r0 + lo1 + h1)));
+  acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(w1hi, w0hi), __ldg(vals + r1 + lo1 + h1)));
+  if (!ssg_exp_in_range(acc)) return SSG_ERR_EXP_RANGE;
+  *out = ssg_exp(acc, FMA);
+  return SSG_OK;
+}
+
 template <int FMA, int FOREST>
 __device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, double* flops_out) {
   const SimConfig& c = *U.cfg;
@@ -752,7 +807,8 @@ __device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, doubl
     const bool is_dec = U.lane & 1;
     double pred = 0.0, fl = 0.0, v0 = 0.0, v1 = 0.0;
     int code = SSG_OK, bad = 0;
-    bool active = false;
+    bool active = false, query = false;
+    int64_t t0 = 0;  // integer v0 of the query
     const int op_index = is_dec ? c.idx_dec : c.idx_pre;
     if (m < pp && op_index >= 0) {
       const int64_t* s6 = st + m * 6;
@@ -764,22 +820,36 @@ __device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, doubl
           pred = tab[5 * (int64_t)T1 + n_eq];
           fl = tab[6 * (int64_t)T1 + n_eq];
         } else {
+          query = true;
+          t0 = n_eq;
           v0 = (double)n_eq;
           v1 = __dmul_rn((double)s6[3], o.kvb);
           const double ctx_tokens = v1 / o.kvb;
-          code = ssg_predict_t<FMA, FOREST>(U.E, o.slot, v0, v1, &pred, &bad);
-          pred = __dmul_rn(o.count, pred);
           fl = __dmul_rn(o.count, __dmul_rn(__dmul_rn(__dmul_rn(4.0, v0), __dadd_rn(v0, ctx_tokens)), o.fa));
         }
       } else if (s6[1] > 0 && is_dec && s6[4] > 0) {
         active = true;
+        query = true;
+        t0 = s6[4];
         v0 = (double)s6[4];
         v1 = __dmul_rn((double)s6[5], o.kvb);
         const double ctx_tokens = v1 / o.kvb;
-        code = ssg_predict_t<FMA, FOREST>(U.E, o.slot, v0, v1, &pred, &bad);
-        pred = __dmul_rn(o.count, pred);
         fl = __dmul_rn(o.count, __dmul_rn(__dmul_rn(4.0, ctx_tokens), o.fa));
       }
+    }
+    // one converged predictor call for every querying lane (prefill and
+    // decode attention of every microbatch evaluate side by side)
+    if (query) {
+      const SimOp& o = c.ops[op_index];
+      if (!FOREST && c.tab_cells && t0 <= c.tab_tmax) {
+        const int64_t row = is_dec ? 7 : 9;
+        const double f0 = tab[row * T1 + t0];
+        const int32_t lo0 = (int32_t)tab[(row + 1) * T1 + t0];
+        code = ssg_attn_interp<FMA>(U.E, U.E.models[o.slot], v0, v1, lo0, f0, U.ax1_hint, &pred, &bad);
+      } else {
+        code = ssg_predict_t<FMA, FOREST>(U.E, o.slot, v0, v1, &pred, &bad);
+      }
+      pred = __dmul_rn(o.count, pred);
     }
     const unsigned em = __ballot_sync(SSG_FULL, code != SSG_OK);
     if (em) {

@@ -806,6 +806,7 @@ std::vector<ConfigResult> SearchSession::evaluate(int shard, int num_shards) {
     for (std::size_t i = 0; i < tk.size(); ++i) {
       SimConfig& c = cands[tk[i]].sim;
       c.tab_off = tcfg[i].tab_off;
+      c.tab_cells = tcfg[i].tab_cells;
       c.tab_stride = tcfg[i].tab_stride;
       c.tab_tmax = tcfg[i].tab_tmax;
       c.tab_pmax = tcfg[i].tab_pmax;

@@ -23,6 +23,7 @@ void fill_sim_ops(SimConfig& c, const std::vector<OperatorDescriptor>& ops, cons
   c.tab_tmax = 0;
   c.tab_pmax = 0;
   c.tab_stride = 0;
+  c.tab_cells = 0;
   c.idx_pre = c.idx_dec = -1;
   c.ncomm = 0;
   c.qb_fixed = c.qb_pre = c.qb_dec = 0;
@@ -165,16 +166,25 @@ void build_token_tables(std::vector<SimConfig>& cfgs, const std::vector<SsgEstVi
       if (cfgs[i].ops[k].cls == SSG_CLS_TOKEN && cfgs[i].ops[k].slot >= 0)
         up = std::min(up, de.host_models[cfgs[i].ops[k].slot].upper[0]);
     cap.push_back(static_cast<int32_t>(std::min(up, 1.0e6)));
+    // axis-0 cell rows need both attention models to be 2-D interpolators
+    auto interp2 = [&](int32_t idx) {
+      if (idx < 0) return false;
+      const int32_t slot = cfgs[i].ops[idx].slot;
+      if (slot < 0) return false;
+      const SsgModelDesc& md = de.host_models[slot];
+      return md.kind == SSG_KIND_INTERP && md.nf == 2;
+    };
     reps.push_back(cfgs[i]);
+    reps.back().tab_cells = interp2(cfgs[i].idx_pre) && interp2(cfgs[i].idx_dec) ? 1 : 0;
   }
   int32_t stride = 2;
   for (auto c : cap) stride = std::max(stride, c + 1);
   const int32_t n = static_cast<int32_t>(reps.size());
   for (int32_t t = 0; t < n; ++t) {
-    reps[t].tab_off = static_cast<int64_t>(t) * 7 * stride;
+    reps[t].tab_off = static_cast<int64_t>(t) * SSG_TAB_ROWS * stride;
     reps[t].tab_stride = stride;
   }
-  pool.resize(static_cast<std::size_t>(n) * 7 * stride);
+  pool.resize(static_cast<std::size_t>(n) * SSG_TAB_ROWS * stride);
   DeviceBuffer<SimConfig> d_cfg;
   DeviceBuffer<SsgEstView> d_est;
   DeviceBuffer<uint8_t> d_valid(static_cast<std::size_t>(n) * stride);
@@ -197,6 +207,7 @@ void build_token_tables(std::vector<SimConfig>& cfgs, const std::vector<SsgEstVi
     cfgs[i].tab_stride = r.tab_stride;
     cfgs[i].tab_tmax = r.tab_tmax;
     cfgs[i].tab_pmax = r.tab_pmax;
+    cfgs[i].tab_cells = r.tab_off >= 0 && r.tab_tmax >= 1 ? r.tab_cells : 0;
   }
 }
 

@@ -31,6 +31,8 @@
 #define SSG_UF_BATCH_LOG 2  // record every scheduled batch (SimObserver payload)
 #define SSG_UF_ABORT 4      // capacity probe: stop once late schedules exceed the bound
 
+#define SSG_TAB_ROWS 11     // token-table rows per table (see SimConfig)
+
 // One operator of the per-stage operator set, with everything predict_batch /
 // batch_device_flops need (estimator.hpp:294-380, op_cost.hpp:21-73).
 struct SimOp {
@@ -57,14 +59,19 @@ struct SimConfig {
   //   S6[t] = fp64 sum of count*pred over the token-level ops, in op order
   //   F6[t] = same for their flops;  C_k[t] = count*pred of the k-th comm op
   //   P0[t], P0F[t] = prefill attention at n_eq = t with no prior context
-  // Layout at `tab_off` in the table pool: S6 | F6 | C0 | C1 | C2 | P0 | P0F,
-  // each tab_stride doubles.  tab_off < 0: no tables (full path).
+  //   DF[t], DL[t] / PF[t], PL[t] = the interp cell (clamped fraction, lower
+  //     index as a double) along axis 0 of the decode / prefill attention model
+  //     at v0 = t, i.e. ssg_axis_cell(log1p(t)) -- only when tab_cells is set
+  // Layout at `tab_off` in the table pool: S6 | F6 | C0 | C1 | C2 | P0 | P0F |
+  // DF | DL | PF | PL, each tab_stride doubles.  tab_off < 0: no tables (full path).
   int64_t tab_off;
   int32_t tab_tmax;   // every token op and comm op is valid for t <= tab_tmax
   int32_t tab_pmax;   // prefill attention at prior 0 is valid for n_eq <= tab_pmax
   // derived once on the host (fill_sim_ops) so the per-batch path never scans ops
   int32_t idx_pre, idx_dec;  // op indices of attention prefill / decode (-1 if absent)
   int32_t ncomm, bs_shift;   // comm ops (<= 3); log2(block_size) if a power of two, else -1
+  int32_t tab_cells;         // DF/DL/PF/PL rows valid: both attention models are 2-D interp
+  int32_t tab_pad;
   int64_t qb_fixed;          // qbytes of token + comm ops (queried every non-empty microbatch)
   int64_t qb_pre, qb_dec;    // qbytes of the attention queries
   SimOp ops[SSG_MAX_OPS];
