@@ -442,7 +442,7 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, double next_
       } else {
         int32_t lo1;
         double f1;
-        ssg_axis_cell(ax1, n1, ssg_log1p(v1, FMA), &lo1, &f1);
+        ssg_axis_cell_hint(ax1, n1, ssg_log1p(v1, FMA), &U.ax1_hint, &lo1, &f1);
         const int32_t h1 = n1 == 1 ? 0 : 1;
         const double g1 = __dsub_rn(1.0, f1);
         const double w1lo = g1, w1hi = h1 ? f1 : g1;

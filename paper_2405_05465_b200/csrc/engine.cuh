@@ -130,7 +130,10 @@ __device__ __forceinline__ bool failed(Unit& U) { return U.out->code != SSG_OK; 
 __device__ __forceinline__ int64_t units_for(const SimConfig& c, int64_t tokens) {
   if (c.token_granular) return tokens;
   const int64_t t = tokens + c.block_size - 1;  // ceil(tokens / block_size), tokens >= 0
-  return c.bs_shift >= 0 ? (t >> c.bs_shift) : t / c.block_size;
+  // t < 2^32 (tokens < 2^31, block_size < 2^31, both checked on the host):
+  // floor(t / b) = mulhi(t, ceil(2^64 / b)) exactly; inlined at every
+  // block-accounting site, so no division sequence is
+  return c.bs_shift >= 0 ? (t >> c.bs_shift) : (int64_t)__umul64hi((uint64_t)t, c.bs_magic);
 }
 __device__ __forceinline__ int64_t shortfall_held(const SimConfig& c, int32_t held, int64_t tokens) {
   int64_t s = units_for(c, tokens) - (int64_t)held;
@@ -702,24 +705,10 @@ __device__ __forceinline__ int ssg_attn_interp(const SsgEstView& E, const SsgMod
     *bad_feature = 1;
     return SSG_ERR_BBOX;
   }
-  const double x1 = ssg_log1p(v1, FMA);
-  const double* ax = E.dpool + m.axis_off[1];
   const int32_t n1 = m.axis_len[1];
-  int32_t lo1 = 0;
-  double f1 = 0.0;
-  if (n1 > 1) {
-    int32_t h = hint < 0 ? 0 : (hint > n1 - 2 ? n1 - 2 : hint);
-    const double a = __ldg(ax + h), b = __ldg(ax + h + 1);
-    // upper_bound(x) - 1 clamped to [0, n1 - 2] equals h  <=>
-    //   (h == 0 || ax[h] <= x) && (h == n1 - 2 || x < ax[h + 1])
-    if ((h == 0 || !(x1 < a)) && (h == n1 - 2 || x1 < b)) {
-      lo1 = h;
-      f1 = ssg_clamp((x1 - a) / (b - a), 0.0, 1.0);
-    } else {
-      ssg_axis_cell(ax, n1, x1, &lo1, &f1);
-    }
-    hint = lo1;
-  }
+  int32_t lo1;
+  double f1;
+  ssg_axis_cell_hint(E.dpool + m.axis_off[1], n1, ssg_log1p(v1, FMA), &hint, &lo1, &f1);
   const int32_t n0 = m.axis_len[0];
   const double* vals = E.dpool + m.values_off;
   const int32_t h0 = n0 == 1 ? 0 : 1;
@@ -745,8 +734,8 @@ __device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, doubl
   const int32_t total = S.np + S.nd;
   for (int m = 0; m < pp; ++m) {
     int64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0;
-    for (int32_t k = U.lane; k < total; k += 32) {
-      if (k % pp != m) continue;
+    // entry k belongs to microbatch k mod pp (split_microbatches, sim.hpp:118-130)
+    for (int32_t k = m + U.lane * pp; k < total; k += 32 * pp) {
       if (k < S.np) {
         const int64_t ch = P_CHUNK(U, r)[k];
         a0 += 1;

@@ -57,6 +57,30 @@ __device__ __forceinline__ void ssg_axis_cell(const double* __restrict__ ax, int
   *frac = ssg_clamp((x - a) / (b - a), 0.0, 1.0);
 }
 
+// ssg_axis_cell starting from a guess: the bracket test holds exactly when
+// std::upper_bound(x) - 1, clamped to [0, n - 2], equals the guess
+//   (h == 0 || ax[h] <= x) && (h == n - 2 || x < ax[h + 1])
+// so the cell and fraction are ssg_axis_cell's; otherwise the full search runs.
+// *hint receives the cell (simulations query neighbouring cells iteration
+// after iteration: the context sum grows by one token per decode).
+__device__ __forceinline__ void ssg_axis_cell_hint(const double* __restrict__ ax, int32_t n, double x,
+                                                   int32_t* hint, int32_t* lo, double* frac) {
+  if (n == 1) {
+    *lo = 0;
+    *frac = 0.0;
+    return;
+  }
+  const int32_t h = *hint < 0 ? 0 : (*hint > n - 2 ? n - 2 : *hint);
+  const double a = __ldg(ax + h), b = __ldg(ax + h + 1);
+  if ((h == 0 || !(x < a)) && (h == n - 2 || x < b)) {
+    *lo = h;
+    *frac = ssg_clamp((x - a) / (b - a), 0.0, 1.0);
+  } else {
+    ssg_axis_cell(ax, n, x, lo, frac);
+  }
+  *hint = *lo;
+}
+
 // Multilinear interpolation (regressor.hpp:308-341), unrolled for the one- and
 // two-feature models the estimator trains.  Corner order (mask 0..2^nf-1),
 // weight product order (feature nf-1 down to 0, from 1.0) and the fp64

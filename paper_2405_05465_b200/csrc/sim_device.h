@@ -72,6 +72,7 @@ struct SimConfig {
   int32_t ncomm, bs_shift;   // comm ops (<= 3); log2(block_size) if a power of two, else -1
   int32_t tab_cells;         // DF/DL/PF/PL rows valid: both attention models are 2-D interp
   int32_t tab_pad;
+  uint64_t bs_magic;         // ceil(2^64 / block_size) when it is not a power of two
   int64_t qb_fixed;          // qbytes of token + comm ops (queried every non-empty microbatch)
   int64_t qb_pre, qb_dec;    // qbytes of the attention queries
   SimOp ops[SSG_MAX_OPS];

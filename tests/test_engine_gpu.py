@@ -121,6 +121,20 @@ def test_cfg2_sarathi_70b_zipf_10k(ssg, ref, qps):
 TIGHT = dict(catalog.DEVICES["a100_80g"], device_mem=30e9)
 
 
+@pytest.mark.parametrize("policy,block_size", [("vllm", 24), ("sarathi_serve", 7), ("orca_plus", 1),
+                                                ("vllm", 32)])
+def test_block_sizes(ssg, ref, policy, block_size):
+    """Block accounting for power-of-two and other block sizes (the device divides
+    by a non-power-of-two block size with a 64-bit multiply-high), under memory
+    pressure so shortfalls, watermarks and preemptions depend on the rounding."""
+    m, t = estimators(ssg, ref, "llama2_7b", "a100_80g", [1])
+    extra = {"chunk_size": 384} if policy == "sarathi_serve" else {}
+    cluster = catalog.cluster_doc("llama2_7b", TIGHT, policy=policy, max_batch_size=64,
+                                  block_size=block_size, **extra)
+    mine, theirs = run_both(ssg, m, t, cluster, trace_fixture(500, 8.0, 3))
+    assert_same(mine, theirs)
+
+
 @pytest.mark.parametrize("policy,extra", [
     ("vllm", {}), ("orca_plus", {}), ("lightllm", {}),
     ("sarathi_serve", {"chunk_size": 512}), ("faster_transformer", {}),
