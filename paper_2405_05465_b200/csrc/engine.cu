@@ -606,6 +606,7 @@ __device__ void run_unit(Unit& U) {
   U.seq = (uint64_t)u.n;
   U.serial = 0;
   U.qbytes = 0;
+  U.qb_lane = 0;
   U.iters = 0;
   U.entries = 0;
   int32_t next_arrival = 0;
@@ -766,6 +767,7 @@ __device__ void run_unit(Unit& U) {
     }
   }
   if (reg1) store_rep(U, 0, S1);
+  U.qbytes += warp_sum64(U.qb_lane);
   if (U.lane == 0) {
     U.out->span = U.clock;
     U.out->events = events;
@@ -871,6 +873,7 @@ __global__ void __launch_bounds__(SSG_SIM_WARPS * 32)
   U.ax1_hint = 0;
   U.clock = 0.0;
   U.qbytes = 0;
+  U.qb_lane = 0;
   if (U.lane == 0) {
     SimUnitOut o;
     memset(&o, 0, sizeof o);

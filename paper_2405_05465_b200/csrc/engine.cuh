@@ -67,6 +67,7 @@ struct Unit {
   double clock;
   uint64_t seq;
   int32_t ax1_hint;    // per lane: last axis-1 interp cell of this lane's attention query
+  int64_t qb_lane;     // per lane: predictor bytes of the microbatches this lane summed
 };
 
 // ---------------------------------------------------------------- workspace
@@ -732,25 +733,30 @@ __device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, doubl
   const int pp = c.pp;
   int64_t* st = U.smem_stats;  // [pp][6]: prefills, tokens, sum p^2, sum prior, decodes, sum ctx
   const int32_t total = S.np + S.nd;
-  for (int m = 0; m < pp; ++m) {
-    int64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0;
-    // entry k belongs to microbatch k mod pp (split_microbatches, sim.hpp:118-130)
-    for (int32_t k = m + U.lane * pp; k < total; k += 32 * pp) {
-      if (k < S.np) {
-        const int64_t ch = P_CHUNK(U, r)[k];
-        a0 += 1;
-        a1 += ch;
-        a2 += ch * ch;
-        a3 += P_PRIOR(U, r)[k];
-      } else {
-        a1 += 1;
-        a4 += 1;
-        a5 += D_CTX(U, r)[k - S.np];
-      }
+  // per-microbatch sums: prefills, tokens, sum p^2, sum prior, decodes, sum ctx
+  auto accumulate = [&](int32_t k, int64_t& a0, int64_t& a1, int64_t& a2, int64_t& a3, int64_t& a4,
+                        int64_t& a5) {
+    if (k < S.np) {
+      const int64_t ch = P_CHUNK(U, r)[k];
+      a0 += 1;
+      a1 += ch;
+      a2 += ch * ch;
+      a3 += P_PRIOR(U, r)[k];
+    } else {
+      a1 += 1;
+      a4 += 1;
+      a5 += D_CTX(U, r)[k - S.np];
     }
+  };
+  if ((32 % pp) == 0) {
+    // entry k belongs to microbatch k mod pp (split_microbatches, sim.hpp:118-130);
+    // with pp | 32 lane l only sees entries of microbatch l mod pp, so one pass
+    // and a reduction over the lanes sharing l mod pp give every microbatch
+    int64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0;
+    for (int32_t k = U.lane; k < total; k += 32) accumulate(k, a0, a1, a2, a3, a4, a5);
     // 32-lane sums of values below 2^26 fit in 31 bits: one REDUX each
     const bool small = ((a1 | a2 | a3 | a5) >> 26) == 0;
-    if (__all_sync(SSG_FULL, small)) {
+    if (pp == 1 && __all_sync(SSG_FULL, small)) {
       a0 = __reduce_add_sync(SSG_FULL, (unsigned)a0);
       a1 = __reduce_add_sync(SSG_FULL, (unsigned)a1);
       a2 = __reduce_add_sync(SSG_FULL, (unsigned)a2);
@@ -758,8 +764,7 @@ __device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, doubl
       a4 = __reduce_add_sync(SSG_FULL, (unsigned)a4);
       a5 = __reduce_add_sync(SSG_FULL, (unsigned)a5);
     } else {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
+      for (int o = 16; o >= pp; o >>= 1) {
         a0 += __shfl_xor_sync(SSG_FULL, a0, o);
         a1 += __shfl_xor_sync(SSG_FULL, a1, o);
         a2 += __shfl_xor_sync(SSG_FULL, a2, o);
@@ -768,13 +773,35 @@ __device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, doubl
         a5 += __shfl_xor_sync(SSG_FULL, a5, o);
       }
     }
-    if (U.lane == 0) {
-      st[m * 6 + 0] = a0;
-      st[m * 6 + 1] = a1;
-      st[m * 6 + 2] = a2;
-      st[m * 6 + 3] = a3;
-      st[m * 6 + 4] = a4;
-      st[m * 6 + 5] = a5;
+    __syncwarp();
+    if (U.lane < pp) {
+      int64_t* s6 = st + U.lane * 6;
+      s6[0] = a0;
+      s6[1] = a1;
+      s6[2] = a2;
+      s6[3] = a3;
+      s6[4] = a4;
+      s6[5] = a5;
+    }
+  } else {
+    for (int m = 0; m < pp; ++m) {
+      int64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0;
+      for (int32_t k = m + U.lane * pp; k < total; k += 32 * pp) accumulate(k, a0, a1, a2, a3, a4, a5);
+      a0 = warp_sum64(a0);
+      a1 = warp_sum64(a1);
+      a2 = warp_sum64(a2);
+      a3 = warp_sum64(a3);
+      a4 = warp_sum64(a4);
+      a5 = warp_sum64(a5);
+      if (U.lane == 0) {
+        st[m * 6 + 0] = a0;
+        st[m * 6 + 1] = a1;
+        st[m * 6 + 2] = a2;
+        st[m * 6 + 3] = a3;
+        st[m * 6 + 4] = a4;
+        st[m * 6 + 5] = a5;
+      }
+      __syncwarp();
     }
   }
   __syncwarp();
@@ -785,9 +812,8 @@ __device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, doubl
   double err_val = 0.0;
   int64_t qb = 0;
   // token-table fast path: every non-empty microbatch within the tables' range
-  bool use_tab = c.tab_off >= 0;
-  for (int m = 0; m < pp && use_tab; ++m)
-    if (st[m * 6 + 1] > c.tab_tmax) use_tab = false;
+  const bool use_tab =
+      c.tab_off >= 0 && !__any_sync(SSG_FULL, U.lane < pp && st[U.lane * 6 + 1] > c.tab_tmax);
   if (use_tab) {
     const int T1 = c.tab_stride;
     const double* tab = U.tables + c.tab_off;
@@ -848,24 +874,22 @@ __device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, doubl
       err_val = __shfl_sync(SSG_FULL, bad ? v1 : v0, src);
       err_task = __shfl_sync(SSG_FULL, op_index, src);  // op index within microbatch 0's numbering
     }
-    // algorithmic bytes: every query the reference makes, however it is served
-    for (int mm = 0; mm < pp; ++mm) {
-      const int64_t* s6 = st + mm * 6;
-      if (s6[1] == 0) continue;
-      qb += c.qb_fixed + (s6[0] > 0 ? c.qb_pre : 0) + (s6[4] > 0 ? c.qb_dec : 0);
-    }
-    U.qbytes += qb;
-    for (int mm = 0; mm < pp; ++mm) {
-      const double pp_pred = __shfl_sync(SSG_FULL, pred, 2 * mm);
-      const double pp_fl = __shfl_sync(SSG_FULL, fl, 2 * mm);
-      const int pp_act = __shfl_sync(SSG_FULL, (int)active, 2 * mm);
-      const double dd_pred = __shfl_sync(SSG_FULL, pred, 2 * mm + 1);
-      const double dd_fl = __shfl_sync(SSG_FULL, fl, 2 * mm + 1);
-      const int dd_act = __shfl_sync(SSG_FULL, (int)active, 2 * mm + 1);
-      const int64_t t = st[mm * 6 + 1];
+    // microbatch mm's operator-order sum on lane mm: token-level ops (table),
+    // prefill attention (lane 2mm), decode attention (lane 2mm + 1), comm ops
+    const double pp_pred = __shfl_sync(SSG_FULL, pred, (2 * U.lane) & 31);
+    const double pp_fl = __shfl_sync(SSG_FULL, fl, (2 * U.lane) & 31);
+    const int pp_act = __shfl_sync(SSG_FULL, (int)active, (2 * U.lane) & 31);
+    const double dd_pred = __shfl_sync(SSG_FULL, pred, (2 * U.lane + 1) & 31);
+    const double dd_fl = __shfl_sync(SSG_FULL, fl, (2 * U.lane + 1) & 31);
+    const int dd_act = __shfl_sync(SSG_FULL, (int)active, (2 * U.lane + 1) & 31);
+    if (U.lane < pp) {
+      const int64_t* s6 = st + U.lane * 6;
+      const int64_t t = s6[1];
       double acc_s = 0.0, acc_f = 0.0;
       if (t > 0) {
-        acc_s = tab[t];                 // token-level ops, op order
+        // algorithmic bytes: every query the reference makes, however it is served
+        U.qb_lane += c.qb_fixed + (s6[0] > 0 ? c.qb_pre : 0) + (s6[4] > 0 ? c.qb_dec : 0);
+        acc_s = tab[t];
         acc_f = tab[(int64_t)T1 + t];
         if (pp_act) {
           acc_s = __dadd_rn(acc_s, pp_pred);
@@ -877,10 +901,8 @@ __device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, doubl
         }
         for (int k = 0; k < c.ncomm; ++k) acc_s = __dadd_rn(acc_s, tab[(int64_t)(2 + k) * T1 + t]);
       }
-      if (U.lane == 0) {
-        secs_part[mm] = acc_s;
-        flop_part[mm] = acc_f;
-      }
+      secs_part[U.lane] = acc_s;
+      flop_part[U.lane] = acc_f;
     }
     __syncwarp();
   } else {
