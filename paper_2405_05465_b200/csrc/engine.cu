@@ -618,11 +618,21 @@ __device__ void run_unit(Unit& U) {
   const bool reg1 = R == 1 && c.routing != SSG_ROUTE_DEFERRED;
   RepState S1;
   memset(&S1, 0, sizeof S1);
+  // a lone replica's BatchStart queued by BatchComplete at the same clock is the
+  // next event unless an arrival is due at or before it (arrivals carry lower
+  // seq numbers): then the event selection is skipped (one call site each)
+  bool direct = false;
   while (true) {
     // ---- next event: (time, seq) argmin over the arrival head and replica slots
     double bt = INFINITY;
     uint64_t bs = ~0ull;
     int bw = -2;  // -1 arrival, r >= 0 replica
+    if (direct) {
+      direct = false;
+      bt = U.clock;
+      bw = 0;
+      goto replica_event;
+    }
     if (next_arrival < u.n) {
       bt = next_arrival_time;
       bs = (uint64_t)next_arrival;
@@ -668,6 +678,7 @@ __device__ void run_unit(Unit& U) {
       }
     }
     if (bw == -2) break;
+  replica_event:
     if (bt < U.clock) {
       set_error(U, SSG_ERR_INTERNAL, 6, 0, 0, bt);  // event time regression
       break;
@@ -759,6 +770,7 @@ __device__ void run_unit(Unit& U) {
       start_if_idle(U, S);
       if (reg1) {
         S1 = S;
+        direct = !FAST && S.ev_kind == 1 && !(next_arrival < u.n && next_arrival_time <= U.clock);
       } else {
         store_rep(U, r, S);
         drain_pool(U);
@@ -793,11 +805,14 @@ __device__ void run_unit(Unit& U) {
   }
 }
 
+#ifndef SSG_SIM_FAST_MINB
+#define SSG_SIM_FAST_MINB 1  // fast-forward kernels run lone simulations: registers over occupancy
+#endif
 #ifndef SSG_SIM_MINB
 #define SSG_SIM_MINB 6  // 6 blocks x 2 warps per SM: <= 168 registers (measured best, DESIGN 6.4)
 #endif
 template <int FMA, int FOREST, int FAST>
-__global__ void __launch_bounds__(SSG_SIM_WARPS * 32, FAST ? 1 : SSG_SIM_MINB)
+__global__ void __launch_bounds__(SSG_SIM_WARPS * 32, FAST ? SSG_SIM_FAST_MINB : SSG_SIM_MINB)
     k_simulate(SimLaunch L) {
   __shared__ int64_t stats[SSG_SIM_WARPS][SSG_MAX_PP * 6];
   __shared__ double part[SSG_SIM_WARPS][4 * SSG_MAX_PP];
