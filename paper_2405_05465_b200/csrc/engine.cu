@@ -194,6 +194,8 @@ __device__ bool batch_start(Unit& U, RepState& S, int r) {
   U.serial += 1;
   S.np = 0;
   S.nd = 0;
+  U.plan_tokens = 0;
+  U.plan_late = 0;
   switch (c.policy) {
     case SSG_POL_FT: schedule_ft(U, S, r); break;
     case SSG_POL_VLLM: schedule_vllm(U, S, r); break;
@@ -207,10 +209,7 @@ __device__ bool batch_start(Unit& U, RepState& S, int r) {
     S.ev_kind = 0;
     return true;
   }
-  int32_t tokens = 0;
-  for (int32_t k = U.lane; k < S.np; k += 32) tokens += P_CHUNK(U, r)[k];
-  tokens = (int32_t)warp_sum64(tokens);
-  tokens += S.nd;
+  const int32_t tokens = U.plan_tokens + S.nd;
   if (c.policy == SSG_POL_SARATHI && tokens > c.chunk) {
     set_error(U, SSG_ERR_INTERNAL, 5, tokens, 0, 0.0);  // sarathi: token budget exceeded
     return false;
@@ -247,13 +246,7 @@ __device__ bool batch_start(Unit& U, RepState& S, int r) {
   }
   // capacity-probe abort (sim.hpp:231-240)
   if (U.u->flags & SSG_UF_ABORT) {
-    int late = 0;
-    for (int32_t k = U.lane; k < S.np + S.nd; k += 32) {
-      const int32_t j = k < S.np ? P_IDX(U, r)[k] : D_IDX(U, r)[k - S.np];
-      const ReqTimes t = U.tm[j];
-      if (t.first_sched == U.clock && U.clock - t.arrival > U.u->abort_thr) ++late;
-    }
-    late = (int)__reduce_add_sync(SSG_FULL, (unsigned)late);
+    const int late = U.plan_late;
     if (late) {
       const int total = U.out->late + late;
       wput(U, &U.out->late, total);

@@ -68,6 +68,9 @@ struct Unit {
   uint64_t seq;
   int32_t ax1_hint;    // per lane: last axis-1 interp cell of this lane's attention query
   int64_t qb_lane;     // per lane: predictor bytes of the microbatches this lane summed
+  // counted while the scheduler forms a batch (reset by batch_start):
+  int32_t plan_tokens; // prefill chunk tokens pushed
+  int32_t plan_late;   // requests first scheduled now, later than the abort threshold
 };
 
 // ---------------------------------------------------------------- workspace
@@ -272,7 +275,13 @@ __device__ __forceinline__ bool prefill_complete(const ReqHot& h) { return h.don
 
 // mark_scheduled (scheduler.hpp:262-265)
 __device__ __forceinline__ void mark_scheduled(Unit& U, int32_t j) {
-  const bool first = U.tm[j].first_sched < 0;
+  const ReqTimes t = U.tm[j];
+  const bool first = t.first_sched < 0;
+  // the probe abort counts batch entries with first_scheduled == clock that
+  // waited past the threshold (sim.hpp:231-239); a request is marked at most
+  // once per schedule, is in the batch iff marked, and gets first_scheduled ==
+  // clock only here -- so the count can be taken as it happens
+  if (first && U.clock - t.arrival > U.u->abort_thr) U.plan_late += 1;
   WSTORE_BEGIN(U)
   if (first) U.tm[j].first_sched = U.clock;
   U.hot[j].planned = U.serial;
@@ -334,6 +343,7 @@ __device__ __forceinline__ void push_prefill(Unit& U, RepState& S, int r, int32_
   P_PRIOR(U, r)[S.np] = prior;
   WSTORE_END
   S.np += 1;
+  U.plan_tokens += chunk;
 }
 
 // schedule_decodes (scheduler.hpp:449-472).  Fast path: a 32-entry window of
@@ -392,14 +402,20 @@ __device__ void schedule_decodes(Unit& U, RepState& S, int r, int32_t max_entrie
     const bool take = elig && U.lane < first_stop;
     const unsigned tm = __ballot_sync(SSG_FULL, take);
     const int ntake = __popc(tm);
+    bool late_first = false;
     if (take) {
       ReqHot& h = U.hot[j];
       h.held += (int32_t)need;  // distinct requests per lane
-      if (U.tm[j].first_sched < 0) U.tm[j].first_sched = U.clock;
+      const ReqTimes t = U.tm[j];
+      if (t.first_sched < 0) {
+        U.tm[j].first_sched = U.clock;
+        late_first = U.clock - t.arrival > U.u->abort_thr;
+      }
       h.planned = U.serial;
       D_IDX(U, r)[S.nd + before] = j;
       D_CTX(U, r)[S.nd + before] = h.kv + 1;
     }
+    U.plan_late += __popc(__ballot_sync(SSG_FULL, late_first));
     __syncwarp();
     int64_t taken_need = __shfl_sync(SSG_FULL, incl, first_stop == 0 ? 0 : first_stop - 1);
     // inclusive prefix at the last taken lane (non-eligible lanes add 0)
@@ -569,13 +585,19 @@ __device__ SSG_COLD void schedule_ft(Unit& U, RepState& S, int r) {
       live = !finished(U.hot[j]);
     }
     const unsigned m = __ballot_sync(SSG_FULL, live);
+    bool late_first = false;
     if (live) {
       const int32_t slot = S.nd + __popc(m & ((1u << U.lane) - 1u));
-      if (U.tm[j].first_sched < 0) U.tm[j].first_sched = U.clock;
+      const ReqTimes t = U.tm[j];
+      if (t.first_sched < 0) {
+        U.tm[j].first_sched = U.clock;
+        late_first = U.clock - t.arrival > U.u->abort_thr;
+      }
       U.hot[j].planned = U.serial;
       D_IDX(U, r)[slot] = j;
       D_CTX(U, r)[slot] = U.hot[j].kv + 1;
     }
+    U.plan_late += __popc(__ballot_sync(SSG_FULL, late_first));
     __syncwarp();
     S.nd += __popc(m);
   }
