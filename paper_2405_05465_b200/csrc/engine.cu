@@ -146,6 +146,11 @@ __device__ void complete_batch(Unit& U, RepState& S, int r) {
   }
   newly_finished = (int)__reduce_add_sync(SSG_FULL, (unsigned)newly_finished);
   S.outstanding -= newly_finished;
+  // only a request that just emitted its last token holds KV and sits in the
+  // running queue while finished (earlier finishers were released and dropped,
+  // or -- FT -- released with held = 0 and still unfinished members remain):
+  // with none, the release/compaction pass below changes nothing
+  if (newly_finished == 0) return;
   // release finished runners; drop them from running unless FT froze membership
   int32_t* a = RUN(U, r);
   int32_t write = 0;
