@@ -28,7 +28,8 @@ struct ssg_estimator {
 namespace ssg {
 void launch_predict(const DeviceEstimator& de, int64_t n, const int32_t* slots, int32_t uniform,
                     const double* f0, const double* f1, double* out,
-                    unsigned long long* first_error, cudaStream_t s);
+                    unsigned long long* first_error, cudaStream_t s,
+                    unsigned long long* invalid = nullptr, unsigned long long* flag_f1 = nullptr);
 [[noreturn]] void raise_predict_error(const EstimatorModel& est, unsigned long long word,
                                       const int32_t* slots_host, int32_t uniform,
                                       const double* f0_host, const double* f1_host);
@@ -77,31 +78,93 @@ struct Staging {
   ssg::DeviceBuffer<int32_t> slots;
   ssg::DeviceBuffer<double> f0, f1, out;
   ssg::DeviceBuffer<unsigned long long> err;
+  cudaStream_t side[2] = {nullptr, nullptr};  // chunk streams besides the context stream
+  cudaEvent_t ready = nullptr;
 };
 Staging& staging() {
   static Staging s;
   return s;
 }
 
+bool pinned(const void* p) {
+  if (!p) return true;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// Host-buffer predictions.  From pinned host memory the queries stream through
+// in chunks on three streams, so chunk k's copy-in, chunk k-1's kernel and
+// chunk k-2's copy-out overlap (PCIe both ways and the SMs at once); pageable
+// buffers take one copy-in, one launch, one copy-out.  Slot validation runs in
+// the kernel (validate), and errors are raised in the reference's order: an
+// invalid slot first, then a missing second feature, then the first failing
+// query.
 void predict_host(const EstimatorModel& est, size_t n, const int32_t* slots, int32_t uniform,
-                  const double* f0, const double* f1, double* out) {
+                  const double* f0, const double* f1, double* out, bool validate) {
   if (n == 0) return;
   const auto& de = est.device();
   auto& ctx = ssg::context();
   auto& S = staging();
-  cudaStream_t s = ctx.stream;
-  if (slots) S.slots.upload(slots, n, s);
-  S.f0.upload(f0, n, s);
-  if (f1) S.f1.upload(f1, n, s);
+  if (!S.ready) {
+    for (auto& x : S.side)
+      ssg::cuda_check(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking), "predict stream");
+    ssg::cuda_check(cudaEventCreateWithFlags(&S.ready, cudaEventDisableTiming), "event");
+  }
+  const bool chunked = n > (1u << 20) && pinned(f0) && pinned(f1) && pinned(out) && pinned(slots);
+  const size_t chunk = chunked ? (size_t(1) << 20) : n;
+  const size_t nch = (n + chunk - 1) / chunk;
+  cudaStream_t s0 = ctx.stream;
+  if (slots) S.slots.resize(n);
+  S.f0.resize(n);
+  if (f1) S.f1.resize(n);
   S.out.resize(n);
-  unsigned long long none = SSG_NO_ERROR, word = 0;
-  S.err.upload(&none, 1, s);
-  ssg::launch_predict(de, static_cast<int64_t>(n), slots ? S.slots.ptr : nullptr, uniform, S.f0.ptr,
-                      f1 ? S.f1.ptr : nullptr, S.out.ptr, S.err.ptr, s);
-  S.out.download(out, n, s);
-  S.err.download(&word, 1, s);
-  ssg::cuda_check(cudaStreamSynchronize(s), "predict");
-  if (word != SSG_NO_ERROR) ssg::raise_predict_error(est, word, slots, uniform, f0, f1);
+  // per chunk: first failing query, first invalid slot; then the missing-f1 flag
+  S.err.resize(2 * nch + 1);
+  ssg::cuda_check(cudaMemsetAsync(S.err.ptr, 0xff, 2 * nch * sizeof(unsigned long long), s0), "memset");
+  ssg::cuda_check(cudaMemsetAsync(S.err.ptr + 2 * nch, 0, sizeof(unsigned long long), s0), "memset");
+  ssg::cuda_check(cudaEventRecord(S.ready, s0), "event");
+  cudaStream_t streams[3] = {s0, S.side[0], S.side[1]};
+  for (int k = 1; k < 3; ++k) ssg::cuda_check(cudaStreamWaitEvent(streams[k], S.ready, 0), "wait");
+  auto h2d = [&](void* d, const void* h, size_t bytes, cudaStream_t st) {
+    ssg::cuda_check(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st), "H2D");
+    ssg::stats().h2d_bytes += static_cast<int64_t>(bytes);
+  };
+  for (size_t c = 0; c < nch; ++c) {
+    cudaStream_t st = streams[c % 3];
+    const size_t b = c * chunk, m = std::min(chunk, n - b);
+    if (slots) h2d(S.slots.ptr + b, slots + b, m * sizeof(int32_t), st);
+    h2d(S.f0.ptr + b, f0 + b, m * sizeof(double), st);
+    if (f1) h2d(S.f1.ptr + b, f1 + b, m * sizeof(double), st);
+    ssg::launch_predict(de, static_cast<int64_t>(m), slots ? S.slots.ptr + b : nullptr, uniform,
+                        S.f0.ptr + b, f1 ? S.f1.ptr + b : nullptr, S.out.ptr + b, S.err.ptr + c, st,
+                        validate ? S.err.ptr + nch + c : nullptr, S.err.ptr + 2 * nch);
+    ssg::cuda_check(cudaMemcpyAsync(out + b, S.out.ptr + b, m * sizeof(double), cudaMemcpyDeviceToHost, st),
+                    "D2H");
+    ssg::stats().d2h_bytes += static_cast<int64_t>(m * sizeof(double));
+  }
+  std::vector<unsigned long long> words(2 * nch + 1);
+  for (int k = 1; k < 3; ++k) {
+    ssg::cuda_check(cudaEventRecord(S.ready, streams[k]), "event");
+    ssg::cuda_check(cudaStreamWaitEvent(s0, S.ready, 0), "wait");
+  }
+  ssg::cuda_check(cudaMemcpyAsync(words.data(), S.err.ptr, words.size() * sizeof(unsigned long long),
+                                  cudaMemcpyDeviceToHost, s0), "D2H");
+  ssg::cuda_check(cudaStreamSynchronize(s0), "predict");
+  for (size_t c = 0; validate && c < nch; ++c)  // chunk-local index, re-based
+    if (words[nch + c] != SSG_NO_ERROR)
+      throw Error("predict: query " + std::to_string(words[nch + c] + c * chunk) +
+                  " has no trained model slot");
+  if (validate && words[2 * nch] != 0) throw Error("predict: two-feature models need f1");
+  for (size_t c = 0; c < nch; ++c) {
+    if (words[c] == SSG_NO_ERROR) continue;
+    // re-base the chunk-local query index
+    const unsigned long long word = ((words[c] >> 8) + c * chunk) << 8 | (words[c] & 0xff);
+    ssg::raise_predict_error(est, word, slots, uniform, f0, f1);
+  }
 }
 
 }  // namespace
@@ -179,22 +242,14 @@ int ssg_predict(const ssg_estimator* e, int32_t op, int64_t tp, size_t n, const 
             "estimator: query for " + to_string(OpModelKey{static_cast<OpName>(op), tp}) +
                 " missing feature " + m.schema.back());
     const int32_t slot = e->model.device().slot(static_cast<OpName>(op), tp);
-    predict_host(e->model, n, nullptr, slot, f0, m.schema.size() > 1 ? f1 : nullptr, out);
+    predict_host(e->model, n, nullptr, slot, f0, m.schema.size() > 1 ? f1 : nullptr, out, false);
   });
 }
 
 int ssg_predict_mixed(const ssg_estimator* e, size_t n, const int32_t* slots, const double* f0,
                       const double* f1, double* out, ssg_status* st) {
   return guarded(st, [&] {
-    const auto& de = e->model.device();
-    bool needs_f1 = false;
-    for (size_t i = 0; i < n; ++i) {
-      if (slots[i] < 0 || slots[i] >= de.view.nmodels)  // message built only on failure
-        throw Error("predict: query " + std::to_string(i) + " has no trained model slot");
-      needs_f1 |= de.host_models[slots[i]].nf > 1;
-    }
-    require(f1 != nullptr || !needs_f1, "predict: two-feature models need f1");
-    predict_host(e->model, n, slots, 0, f0, f1, out);
+    predict_host(e->model, n, slots, 0, f0, f1, out, true);
   });
 }
 
@@ -428,6 +483,7 @@ nlohmann::json outcome_json(const SearchOutcome& o, const std::string& objective
 int ssg_search(const char* config_path, int shard, int num_shards, char** out, ssg_status* st) {
   return guarded(st, [&] {
     require(num_shards >= 1 && shard >= 0 && shard < num_shards, "ssg_search: bad shard");
+    ssg::PhaseTimer timer("ssg_search_shard");
     auto cfg = load_search_config(config_path);
     auto results = evaluate_configs_shard(cfg.spec, cfg.workload, cfg.options, shard, num_shards);
     auto o = finalize_search(cfg.spec, cfg.options, std::move(results));

@@ -328,6 +328,7 @@ std::mutex g_dump_mu;
 
 void run_launch(SweepLane& lane, ProbeLaunch& L, const ResidentWorkload& w,
                 std::vector<SimUnitOut>& out, std::vector<double>& sel) {
+  PhaseTimer timer("search: launch");
   SweepBuffers& B = lane.B;
   cudaStream_t s = lane.stream.s;
   const int32_t np = static_cast<int32_t>(L.probes.size());
@@ -693,6 +694,7 @@ struct SearchSession::State {
 SearchSession::SearchSession(const ModelSpec& spec, const std::vector<Request>& workload,
                              const SearchOptions& opts)
     : st_(std::make_unique<State>()) {
+  PhaseTimer timer("search: session open");
   State& S = *st_;
   S.spec = spec;
   S.opts = opts;
@@ -754,6 +756,7 @@ std::vector<ConfigResult> evaluate_configs_shard(const ModelSpec& spec,
 }
 
 std::vector<ConfigResult> SearchSession::evaluate(int shard, int num_shards) {
+  PhaseTimer timer("search: evaluate");
   const State& S = *st_;
   const ModelSpec& spec = S.spec;
   const SearchOptions& opts = S.opts;
@@ -801,6 +804,7 @@ std::vector<ConfigResult> SearchSession::evaluate(int shard, int num_shards) {
       tcfg.push_back(c);
       tk.push_back(k);
     }
+    PhaseTimer t("search: token tables");
     if (std::getenv("SSG_NO_TABLES") == nullptr)
       build_token_tables(tcfg, tests, test_of, SS.tables);
     for (std::size_t i = 0; i < tk.size(); ++i) {
@@ -895,6 +899,7 @@ std::vector<ConfigResult> SearchSession::evaluate(int shard, int num_shards) {
     }
   }
 
+  PhaseTimer t_rounds("search: rounds");
   // lanes: streams + buffers; every lane waits for the token tables
   const SweepKnobs knobs = knobs_from_env();
   const std::size_t nlanes =

@@ -63,13 +63,30 @@ int32_t append_tree(const ForestTree& t, std::size_t nf, std::vector<SsgNode>& o
   return root;
 }
 
+// `invalid` (optional, host-buffer entry points): lowest query index with no
+// trained model slot; *flag_f1 set if a two-feature model got no f1 --
+// checked here instead of a host pass over every query before the copies.
 __global__ void k_predict(SsgEstView E, int64_t n, const int32_t* __restrict__ slot,
                           int32_t uniform_slot, const double* __restrict__ f0,
                           const double* __restrict__ f1, double* __restrict__ out,
-                          unsigned long long* __restrict__ first_error) {
+                          unsigned long long* __restrict__ first_error,
+                          unsigned long long* __restrict__ invalid,
+                          unsigned long long* __restrict__ flag_f1) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const int32_t m = slot ? __ldg(slot + i) : uniform_slot;
+    if (invalid) {
+      if (m < 0 || m >= E.nmodels) {
+        atomicMin(invalid, (unsigned long long)i);
+        out[i] = 0.0;
+        continue;
+      }
+      if (!f1 && E.models[m].nf > 1) {
+        *flag_f1 = 1ull;
+        out[i] = 0.0;
+        continue;
+      }
+    }
     const double v0 = __ldg(f0 + i);
     const double v1 = f1 ? __ldg(f1 + i) : 0.0;
     double r = 0.0;
@@ -215,7 +232,8 @@ using namespace servesim;
 // SSG_NO_ERROR on entry.
 void launch_predict(const DeviceEstimator& de, int64_t n, const int32_t* slots, int32_t uniform,
                     const double* f0, const double* f1, double* out,
-                    unsigned long long* first_error, cudaStream_t s) {
+                    unsigned long long* first_error, cudaStream_t s, unsigned long long* invalid,
+                    unsigned long long* flag_f1) {
   if (n <= 0) return;
   auto& ctx = context();
   const int threads = 256;
@@ -223,7 +241,7 @@ void launch_predict(const DeviceEstimator& de, int64_t n, const int32_t* slots, 
   const int64_t cap = static_cast<int64_t>(ctx.num_sms) * 8;  // 8 x 256 threads resident per SM
   if (blocks > cap) blocks = cap;
   k_predict<<<static_cast<unsigned>(blocks), threads, 0, s>>>(de.view, n, slots, uniform, f0, f1,
-                                                              out, first_error);
+                                                              out, first_error, invalid, flag_f1);
   cuda_check(cudaGetLastError(), "k_predict launch");
   stats().launches_predict += 1;
   stats().queries += n;
@@ -270,7 +288,8 @@ double EstimatorModel::predict(OpName op, std::int64_t tp, const FeatureMap& fea
   unsigned long long none = SSG_NO_ERROR;
   err.upload(&none, 1, ctx.stream);
   buf.upload(v, 2, ctx.stream);
-  ssg::launch_predict(de, 1, nullptr, slot, buf.ptr, buf.ptr + 1, buf.ptr + 2, err.ptr, ctx.stream);
+  ssg::launch_predict(de, 1, nullptr, slot, buf.ptr, buf.ptr + 1, buf.ptr + 2, err.ptr, ctx.stream,
+                      nullptr, nullptr);
   double out = 0.0;
   unsigned long long word = 0;
   cudaMemcpyAsync(&out, buf.ptr + 2, 8, cudaMemcpyDeviceToHost, ctx.stream);

@@ -92,3 +92,44 @@ def test_untrained_op_message(ssg, ref):
         mine.predict("allreduce", 2, np.array([4096.0]))
     assert str(ei.value) == ("estimator: no trained model for op allreduce@tp2 "
                              "(profile and train must cover the config's operators)")
+
+
+def test_predict_mixed_chunked_pinned(ssg, ref):
+    """Host-buffer predictions from pinned memory stream through 1M-query chunks on
+    three streams: still bit-exact, and an error in a late chunk reports its global
+    index with the reference's message; invalid slots and a missing f1 are caught
+    in the kernel and raised before any prediction error."""
+    import torch
+
+    spec, dev = catalog.MODELS["llama2_70b"], catalog.DEVICES["h100_80g"]
+    est_json = ref.train(spec, dev, [4], "interp", 3)
+    mine = ssg.Estimator.from_json(est_json)
+    theirs = ref.Estimator(est_json)
+    rng = np.random.default_rng(4)
+    n = 3 * (1 << 20) + 12345
+    ops = rng.choice([OPS.index("attn_prefill"), OPS.index("attn_decode"), OPS.index("mlp_up_proj")], n)
+    slots = np.array([mine.slot(OPS[o], 4) for o in range(len(OPS))], dtype=np.int32)[ops]
+    pin = lambda a: torch.from_numpy(a).pin_memory().numpy()  # noqa: E731
+    f0 = pin(np.floor(4096.0 ** rng.random(n)))
+    f1 = pin(np.floor((512.0 * 4096.0) ** rng.random(n)) * 1024.0)
+    slots_p = pin(slots)
+    out = pin(np.zeros(n))
+    got = mine.predict_mixed(slots_p, f0, f1, out=out)
+    sample = rng.choice(n, 200000, replace=False)
+    want, bad, _ = theirs.predict(ops[sample], 4, f0[sample], f1[sample])
+    assert bad == -1
+    assert np.array_equal(got[sample].view(np.uint64), want.view(np.uint64))
+    # a guard violation in the third chunk
+    i = 2 * (1 << 20) + 777
+    f0[i] = 1e9
+    with pytest.raises(ssg.InputError) as ei:
+        mine.predict_mixed(slots_p, f0, f1, out=out)
+    _, bad, msg = theirs.predict(ops[i:i + 1], 4, f0[i:i + 1], f1[i:i + 1])
+    assert str(ei.value) == msg
+    # an invalid slot wins over the guard violation, whatever its index
+    slots_p[i + 5] = 999
+    with pytest.raises(ssg.InputError, match="query %d has no trained model slot" % (i + 5)):
+        mine.predict_mixed(slots_p, f0, f1, out=out)
+    slots_p[i + 5] = slots[i + 5]
+    with pytest.raises(ssg.InputError, match="two-feature models need f1"):
+        mine.predict_mixed(slots_p, f0, None, out=out)
