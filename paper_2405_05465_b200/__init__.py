@@ -227,8 +227,9 @@ def search_shard(config_path: str, shard: int, num_shards: int) -> bytes:
     """This shard's ConfigResults as fixed-size records (ssg_config_record), for all-gather."""
     import math
 
-    # capacity: every config could land in one shard; the header counts them
-    cap = 1 << 16
+    # capacity: every config could land in one shard (a search is at most a few
+    # thousand configs; the library reports an error if the buffer is short)
+    cap = 1 << 14
     size = record_size()
     buf = (C.c_char * (cap * size))()
     n = C.c_size_t()

@@ -14,6 +14,7 @@
 #include "runtime.h"
 #include "servesim_b200.hpp"
 #include "sim_host.h"
+#include "sweep.h"
 
 using namespace servesim;
 
@@ -176,6 +177,7 @@ int ssg_init(int device, ssg_status* st) {
 }
 
 int ssg_shutdown(void) {
+  ssg::release_sweep_lanes();
   ssg::shutdown_context();
   return SSG_STATUS_OK;
 }

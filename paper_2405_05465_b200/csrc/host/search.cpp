@@ -326,6 +326,31 @@ struct SweepLane {
 
 std::mutex g_dump_mu;
 
+// Lanes outlive sessions: a process that opens search after search (the e2e
+// bench, a service) reuses the streams, grow-only HBM buffers and pinned
+// staging of earlier sessions instead of paying fresh allocations (+300 ms on
+// a sweep's first launch, measured).  Sessions borrow lanes and give them back.
+struct LanePool {
+  std::mutex mu;
+  std::vector<std::unique_ptr<SweepLane>> free;
+};
+LanePool& lane_pool() {
+  static LanePool* pool = new LanePool;  // never destroyed: lanes may outlive static teardown
+  return *pool;
+}
+std::unique_ptr<SweepLane> borrow_lane() {
+  LanePool& p = lane_pool();
+  {
+    std::lock_guard<std::mutex> lk(p.mu);
+    if (!p.free.empty()) {
+      auto lane = std::move(p.free.back());
+      p.free.pop_back();
+      return lane;
+    }
+  }
+  return std::make_unique<SweepLane>();
+}
+
 void run_launch(SweepLane& lane, ProbeLaunch& L, const ResidentWorkload& w,
                 std::vector<SimUnitOut>& out, std::vector<double>& sel) {
   PhaseTimer timer("search: launch");
@@ -688,7 +713,12 @@ struct SearchSession::State {
   Workload w;
   ResidentWorkload rw;
   DeviceBuffer<double> tables;                    // token tables (context stream)
-  std::vector<std::unique_ptr<SweepLane>> lanes;  // grow-only, reused across evaluations
+  std::vector<std::unique_ptr<SweepLane>> lanes;  // borrowed from the lane pool
+  ~State() {
+    LanePool& p = lane_pool();
+    std::lock_guard<std::mutex> lk(p.mu);
+    for (auto& l : lanes) p.free.push_back(std::move(l));
+  }
 };
 
 SearchSession::SearchSession(const ModelSpec& spec, const std::vector<Request>& workload,
@@ -744,6 +774,18 @@ SearchSession::SearchSession(const ModelSpec& spec, const std::vector<Request>& 
 }
 
 SearchSession::~SearchSession() = default;
+
+}  // namespace servesim
+
+namespace ssg {
+void release_sweep_lanes() {
+  servesim::LanePool& p = servesim::lane_pool();
+  std::lock_guard<std::mutex> lk(p.mu);
+  p.free.clear();
+}
+}  // namespace ssg
+
+namespace servesim {
 
 std::size_t SearchSession::num_configs() const { return st_->configs.size(); }
 
@@ -904,7 +946,7 @@ std::vector<ConfigResult> SearchSession::evaluate(int shard, int num_shards) {
   const SweepKnobs knobs = knobs_from_env();
   const std::size_t nlanes =
       makespan ? 1 : std::max<std::size_t>(1, std::min<std::size_t>(knobs.lanes, live.size()));
-  while (SS.lanes.size() < nlanes) SS.lanes.push_back(std::make_unique<SweepLane>());
+  while (SS.lanes.size() < nlanes) SS.lanes.push_back(borrow_lane());
   auto& ctx = context();
   cudaEvent_t origin;
   cuda_check(cudaEventCreate(&origin), "event");

@@ -29,6 +29,9 @@ struct ResidentWorkload {
   DeviceBuffer<uint8_t> first_emis;  // 1 at each request's first emission slot
 };
 
+// Drops the pooled sweep lanes (streams, HBM, pinned staging); ssg_shutdown.
+void release_sweep_lanes();
+
 void launch_probe_setup(const ProbeDesc* d_probes, int32_t nprobes, const SimUnit* d_units,
                         const ResidentWorkload& w, ReqHot* hot, ReqTimes* tm, int64_t* ids,
                         int64_t* emit_base, cudaStream_t s);
