@@ -342,16 +342,24 @@ def main():
         return reference_arm(a, world, rank)
     import torch
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one process per GPU; with fewer GPUs than ranks (a 1-GPU check of the
+    # multi-rank flow) ranks share devices and the gather falls back to gloo
+    ndev = torch.cuda.device_count()
+    torch.cuda.set_device(local % ndev)
+    dev = torch.device("cuda", local % ndev)
+    backend = "nccl" if world <= ndev else "gloo"
+    coll_dev = dev if backend == "nccl" else torch.device("cpu")
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     import paper_2405_05465_b200 as ssg
 
-    ssg.init(local)
+    ssg.init(local % ndev)
     tmp = tempfile.mkdtemp(prefix="ssg_bench_")
     sweeps = search_configs(tmp, a.quick, a.workload)
     cfg_path = sweeps[0][1]
@@ -370,7 +378,7 @@ def main():
                 recs = ssg.search_shard(path, rank, world)
             else:
                 recs = session.run(rank, world)
-            allrecs = gather_records(recs, count, rank, world, rec_size, device=dev)
+            allrecs = gather_records(recs, count, rank, world, rec_size, device=coll_dev)
             outs.append(ssg.search_finalize(path, allrecs) if rank == 0 else None)
         return outs
 
@@ -391,7 +399,7 @@ def main():
             barrier()
             t = e0.elapsed_time(e1) / 1e3
             if dist is not None:
-                tt = torch.tensor([t], dtype=torch.float64, device=dev)
+                tt = torch.tensor([t], dtype=torch.float64, device=coll_dev)
                 dist.all_reduce(tt, op=dist.ReduceOp.MAX)
                 t = float(tt.item())
             times.append(t)
@@ -399,7 +407,7 @@ def main():
 
     for _ in range(a.warmup):
         step(False)
-    clocks = Clocks(local)
+    clocks = Clocks(local % ndev)
     clocks.start()
     ssg.stats_reset()
     times, outcome = timed(False, a.steps)
@@ -435,7 +443,8 @@ def main():
                                 "(A100/H100 x tp,pp in {1,2,4} x vLLM/Orca+/Sarathi x bs x cs), "
                                 "2000 probe requests, tol 0.02, interp estimator" % n_configs),
                    "configs": n_configs, "sweeps": len(sweeps),
-                   "parallelism": "config shards x%d + 1 NCCL all_gather per sweep" % world,
+                   "parallelism": "config shards x%d + 1 %s all_gather per sweep"
+                                  % (world, "NCCL" if backend == "nccl" else "gloo (ranks share GPUs)"),
                    "l2": "flushed (512 MB write) before every timed step"},
         "e2e": {"value": n_configs / (sum(e2e_times) / len(e2e_times)), "unit": UNIT,
                 "h2d_bytes_per_step": st_e2e["h2d_bytes"] // e2e_steps,
