@@ -211,7 +211,13 @@ int ssg_estimator_train(const char* model_spec_json, const char* device_json, co
     TrainConfig cfg;
     cfg.seed = seed;
     cfg.regressor = regressor ? regressor : "interp";
-    auto* e = new ssg_estimator{train(generate_synthetic_profile(spec, dev, tp), cfg)};
+    std::vector<ProfileRecord> profile;
+    {
+      ssg::PhaseTimer t("train: synthetic profile");
+      profile = generate_synthetic_profile(spec, dev, tp);
+    }
+    ssg::PhaseTimer t("train: fit");
+    auto* e = new ssg_estimator{train(profile, cfg)};
     *out = e;
   });
 }

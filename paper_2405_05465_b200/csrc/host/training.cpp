@@ -9,10 +9,14 @@
 // reference: op_cost.hpp:21-98, profiler.hpp:54-347, regressor.hpp:26-386,
 //            estimator.hpp:137-275
 #include <algorithm>
+#include <cstdlib>
+#include <exception>
+#include <thread>
 #include <cmath>
 #include <random>
 
 #include "json.hpp"
+#include "runtime.h"
 #include "servesim_b200.hpp"
 
 namespace servesim {
@@ -449,6 +453,7 @@ struct ForestBuilder {
 };
 
 RegressorData fit_forest(const Rows& x, const std::vector<double>& y, const ForestConfig& cfg) {
+  ssg::PhaseTimer timer("train: fit_forest");
   require(!x.empty() && x.size() == y.size(), "forest train: empty or mismatched data");
   RegressorData f;
   f.type = "forest";
@@ -461,14 +466,39 @@ RegressorData fit_forest(const Rows& x, const std::vector<double>& y, const Fore
   std::size_t min_leaf = cfg.min_samples_leaf > 0 ? static_cast<std::size_t>(cfg.min_samples_leaf)
                          : f.num_features <= 1    ? 2
                                                   : f.num_features + 2;
-  ForestBuilder fb{x, y, cfg, f.num_features, min_leaf};
   std::vector<std::size_t> all(x.size());
   for (std::size_t i = 0; i < all.size(); ++i) all[i] = i;
-  for (int t = 0; t < cfg.num_trees; ++t) {
-    std::mt19937_64 rng(cfg.seed * 0x9e3779b97f4a7c15ULL + static_cast<std::uint64_t>(t) + 1);
-    ForestTree tree;
-    fb.grow(tree, all, 0, rng);
-    f.trees.push_back(std::move(tree));
+  // Every tree draws from its own mt19937_64 seeded by (seed, t)
+  // (regressor.hpp:93-96), so trees are independent: grow them on host
+  // threads, each into its own slot -- the forest is the same for any thread count.
+  const int nt = cfg.num_trees;
+  f.trees.resize(static_cast<std::size_t>(std::max(0, nt)));
+  auto grow_range = [&](int t0, int t1) {
+    ForestBuilder fb{x, y, cfg, f.num_features, min_leaf};
+    for (int t = t0; t < t1; ++t) {
+      std::mt19937_64 rng(cfg.seed * 0x9e3779b97f4a7c15ULL + static_cast<std::uint64_t>(t) + 1);
+      fb.grow(f.trees[static_cast<std::size_t>(t)], all, 0, rng);
+    }
+  };
+  const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+  int workers = std::max(1, std::min({nt, hw, 16}));
+  if (const char* e = std::getenv("SSG_TRAIN_THREADS")) workers = std::max(1, std::min(nt, std::atoi(e)));
+  if (workers <= 1) {
+    grow_range(0, nt);
+  } else {
+    std::vector<std::thread> pool;
+    std::vector<std::exception_ptr> err(static_cast<std::size_t>(workers));
+    for (int w = 0; w < workers; ++w)
+      pool.emplace_back([&, w] {
+        try {
+          grow_range(nt * w / workers, nt * (w + 1) / workers);
+        } catch (...) {
+          err[static_cast<std::size_t>(w)] = std::current_exception();
+        }
+      });
+    for (auto& th : pool) th.join();
+    for (auto& e : err)
+      if (e) std::rethrow_exception(e);
   }
   return f;
 }
