@@ -414,7 +414,17 @@ void run_launch(SweepLane& lane, ProbeLaunch& L, const ResidentWorkload& w,
   K.log = nullptr;
   K.out = B.out.ptr;
   K.tables = lane.tables;
-  K.fast_forward = sweep_fast_forward_enabled();
+  // decode fast-forward only for launches too small to fill the device (its
+  // larger body costs I-cache misses when many warps share an SM, and saves
+  // half the work of a lone warp's decode stretches)
+  // (measured on cfg #4 shards: threshold 16 units per SM is the best of
+  // 6/8/12/16 for 1, 2, 4 and 8 shards; a 1/8 shard goes 0.91 -> 0.68 s)
+  const int64_t ff_units = [] {
+    const char* e = std::getenv("SSG_FF_UNITS");
+    return e ? std::atoll(e) : 16LL * context().num_sms;
+  }();
+  K.fast_forward = sweep_fast_forward_enabled() ||
+                   static_cast<int64_t>(L.units.size()) <= ff_units ? 1 : 0;
   K.has_forest = L.has_forest ? 1 : 0;
   cudaEvent_t e0, e1;
   cuda_check(cudaEventCreate(&e0), "event");

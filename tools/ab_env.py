@@ -10,16 +10,18 @@ ssg.init(0)
 path = catalog.write_search_config(tempfile.mkdtemp())
 s = ssg.SearchSession(path)
 settings = sys.argv[1].split()
+# AB_SHARD="r/N": time one rank's shard of an N-GPU run (records hash per shard)
+shard, nsh = (int(x) for x in os.environ.get("AB_SHARD", "0/1").split("/"))
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 ref = None
-s.run()
+s.run(shard, nsh)
 for st in settings:
     env = dict(kv.split("=") for kv in st.split(","))
     old = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
     ts = []
     for r in range(reps):
-        ssg.stats_reset(); t0 = time.perf_counter(); recs = s.run(); ts.append(time.perf_counter() - t0)
+        ssg.stats_reset(); t0 = time.perf_counter(); recs = s.run(shard, nsh); ts.append(time.perf_counter() - t0)
         h = hashlib.sha256(recs).hexdigest()[:16]
         ref = ref or h
         assert h == ref, ("records differ", st, h, ref)
