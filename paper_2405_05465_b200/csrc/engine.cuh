@@ -921,7 +921,11 @@ __device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, doubl
           acc_s = __dadd_rn(acc_s, dd_pred);
           acc_f = __dadd_rn(acc_f, dd_fl);
         }
-        for (int k = 0; k < c.ncomm; ++k) acc_s = __dadd_rn(acc_s, tab[(int64_t)(2 + k) * T1 + t]);
+        // comm ops (at most 3), op order
+        const double* comm = tab + 2 * (int64_t)T1 + t;
+        if (c.ncomm > 0) acc_s = __dadd_rn(acc_s, comm[0]);
+        if (c.ncomm > 1) acc_s = __dadd_rn(acc_s, comm[T1]);
+        if (c.ncomm > 2) acc_s = __dadd_rn(acc_s, comm[2 * (int64_t)T1]);
       }
       secs_part[U.lane] = acc_s;
       flop_part[U.lane] = acc_f;
@@ -943,6 +947,45 @@ __device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, doubl
       return SSG_ERR_INTERNAL;
     }
     flops = __dmul_rn(flop_part[0], (double)c.tp);
+  } else if (pp <= 4) {
+    // pipeline_makespan (scheduler.hpp:566-579) over the non-empty microbatches
+    // in order, in registers: stage after stage, each microbatch starts when it
+    // and its predecessor are both done
+    double tim[4], fin[4];
+    bool ne[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      ne[m] = m < pp && st[m * 6 + 1] != 0;
+      tim[m] = ne[m] ? secs_part[m] : 0.0;
+      fin[m] = 0.0;
+    }
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      if (!ne[m]) continue;
+      if (!(tim[m] > 0.0)) {
+        set_error(U, SSG_ERR_INTERNAL, 2, 0, 0, tim[m]);
+        return SSG_ERR_INTERNAL;
+      }
+      flops = __dadd_rn(flops, __dmul_rn(flop_part[m], (double)(c.tp * c.pp)));
+    }
+#pragma unroll
+    for (int st_i = 0; st_i < 4; ++st_i) {
+      if (st_i >= pp) break;
+      double prev = 0.0;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        if (!ne[m]) continue;
+        const double f = fin[m];
+        const double start = f < prev ? prev : f;
+        prev = __dadd_rn(start, tim[m]);
+        fin[m] = prev;
+      }
+    }
+    lat = 0.0;
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+      if (ne[m]) lat = fin[m];  // the last non-empty microbatch
+    __syncwarp();
   } else {
     // compact the non-empty microbatches' times into part[2*MAX..]; makespan
     double* times = U.smem_part + 2 * SSG_MAX_PP;
