@@ -377,7 +377,11 @@ __device__ void schedule_decodes(Unit& U, RepState& S, int r, int32_t max_entrie
     // (32-bit scan when every need is small -- the common case: 0 or 1 block)
     const int before = __popc(em & ((1u << U.lane) - 1u));
     int64_t incl = need;
-    if (__all_sync(SSG_FULL, need < (1 << 25))) {
+    const unsigned ones = __ballot_sync(SSG_FULL, need == 1);
+    if (__all_sync(SSG_FULL, need <= 1)) {
+      // the usual case: a decode needs no new block or exactly one
+      incl = __popc(ones & ((2u << U.lane) - 1u));
+    } else if (__all_sync(SSG_FULL, need < (1 << 25))) {
       int32_t inc32 = (int32_t)need;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
