@@ -267,3 +267,47 @@ def test_simulate_run_binary_outputs(ssg, ref):
     assert rep["preemptions"] == theirs["report"]["preemptions"]
     timed = ref.simulate_timed(t, cluster, ids, arr, pre, dec)
     assert np.array_equal(timed["completion"], run.completion)
+
+
+def test_sarathi_chunk_sequence_known_answer(ssg, ref):
+    """test_scheduler.cpp:172-191 through the engine: a lone 1300-token prompt under
+    Sarathi chunk 512 runs as chunks 512 / 512 / 276 with prior context 0 / 512 /
+    1024, then decodes; identical batch log to the reference."""
+    m, t = estimators(ssg, ref, "llama2_7b", "a100_80g", [1])
+    cluster = catalog.cluster_doc("llama2_7b", "a100_80g", policy="sarathi_serve", max_batch_size=8,
+                                  chunk_size=512)
+    trace = (np.array([0], dtype=np.int64), np.array([0.0]), np.array([1300], dtype=np.int64),
+             np.array([3], dtype=np.int64))
+    mine, theirs = run_both(ssg, m, t, cluster, trace)
+    assert_same(mine, theirs)
+    # entries are [is_prefill, request id, tokens, context]
+    chunks = [b["entries"][0] for b in mine["batches"][:3]]
+    assert [(e[0], e[2], e[3]) for e in chunks] == [(1, 512, 0), (1, 512, 512), (1, 276, 1024)]
+    assert [len(b["entries"]) for b in mine["batches"][3:]] == [1, 1]  # two decodes remain
+
+
+def test_sarathi_hybrid_batches_fill_the_budget(ssg, ref):
+    """test_scheduler.cpp:152-170 as a property of whole runs: decodes are scheduled
+    first and a prefill chunk tops the batch up to the 512-token budget whenever a
+    long prompt is still being chunked, never beyond it; identical to the reference."""
+    m, t = estimators(ssg, ref, "llama2_7b", "a100_80g", [1])
+    cluster = catalog.cluster_doc("llama2_7b", "a100_80g", policy="sarathi_serve", max_batch_size=128,
+                                  chunk_size=512)
+    n = 11
+    ids = np.arange(n, dtype=np.int64)
+    arr = np.array([i * 0.1 for i in range(10)] + [1.5])
+    pre = np.array([1] * 10 + [2000], dtype=np.int64)
+    dec = np.array([400] * 10 + [5], dtype=np.int64)  # still decoding at 1.5 s
+    mine, theirs = run_both(ssg, m, t, cluster, (ids, arr, pre, dec))
+    assert_same(mine, theirs)
+    hybrid = 0
+    for b in mine["batches"]:
+        total = sum(e[2] for e in b["entries"])
+        assert total <= 512
+        kinds = [e[0] for e in b["entries"]]
+        assert kinds == sorted(kinds, reverse=True)  # the log lists prefills, then decodes
+        big = [e for e in b["entries"] if e[0] == 1 and e[1] == 10]
+        if big and any(e[0] == 0 for e in b["entries"]) and big[0][2] + big[0][3] < 2000:
+            assert total == 512  # the chunk fills the budget left by the decodes
+            hybrid += 1
+    assert hybrid >= 1
