@@ -70,34 +70,38 @@ __device__ SSG_COLD void drain_pool(Unit& U) {
   int32_t head = ph[0], size = ph[1];
   if (size == 0) return;
   const int R = U.u->R;
-  // counts snapshot, one lane per replica
-  int64_t cnt = INT64_MAX;
-  if (U.lane < R) cnt = U.reps[U.lane].outstanding;
   const int mask = U.WC - 1;
-  // assignments are decided first, then applied in order
-  int32_t assigned = 0;
+  // The reference snapshots outstanding counts and bumps counts[best] per
+  // assignment; each assignment's enqueue bumps the replica's outstanding count
+  // too, so the live counts equal the snapshot throughout -- read them live,
+  // 32 replicas per pass (any replica count).
   while (size > 0) {
     // best = lowest index among counts < threshold with the smallest count
-    int64_t key = (U.lane < R && cnt < c.defer_threshold) ? ((cnt << 8) | U.lane) : INT64_MAX;
+    int64_t key = INT64_MAX;
+    for (int r0 = 0; r0 < R; r0 += 32) {
+      const int r = r0 + U.lane;
+      int64_t k2 = INT64_MAX;
+      if (r < R) {
+        const int64_t cnt = U.reps[r].outstanding;
+        if (cnt < c.defer_threshold) k2 = (cnt << 16) | r;
+      }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      int64_t t = __shfl_xor_sync(SSG_FULL, key, o);
-      key = t < key ? t : key;
+      for (int o = 16; o > 0; o >>= 1) {
+        const int64_t t = __shfl_xor_sync(SSG_FULL, k2, o);
+        k2 = t < k2 ? t : k2;
+      }
+      key = k2 < key ? k2 : key;
     }
     if (key == INT64_MAX) break;
-    const int best = (int)(key & 0xff);
+    const int best = (int)(key & 0xffff);
     const int32_t j = pool[head & mask];
     head = (head + 1) & mask;
     size -= 1;
-    if (U.lane == best) cnt += 1;
-    // stash the decision in the drained slot: pool[(head-1)] = j | best<<24 is
-    // not needed -- apply immediately, outstanding counts were snapshotted
     RepState S = load_rep(U, best);
     const bool ok = enqueue(U, S, best, j);
     if (ok) start_if_idle(U, S);
     store_rep(U, best, S);
     if (!ok) break;
-    ++assigned;
   }
   wput(U, &ph[0], head);
   wput(U, &ph[1], size);

@@ -149,13 +149,18 @@ def test_policies_under_memory_pressure(ssg, ref, policy, extra):
         assert theirs["report"]["preemptions"] > 0
 
 
-@pytest.mark.parametrize("routing,replicas", [("round_robin", 3), ("least_outstanding", 3),
-                                              ("deferred", 4)])
-def test_routing(ssg, ref, routing, replicas):
+@pytest.mark.parametrize("routing,replicas,n,qps", [("round_robin", 3, 900, 14.0),
+                                                    ("least_outstanding", 3, 900, 14.0),
+                                                    ("deferred", 4, 900, 14.0),
+                                                    ("least_outstanding", 40, 3000, 400.0),
+                                                    ("deferred", 40, 3000, 400.0)])
+def test_routing(ssg, ref, routing, replicas, n, qps):
+    """Routers, including more replicas than a warp has lanes (argmins run 32
+    replicas per pass)."""
     m, t = estimators(ssg, ref, "llama2_7b", "a100_80g", [1])
     cluster = catalog.cluster_doc("llama2_7b", "a100_80g", replicas=replicas, routing=routing,
                                   policy="vllm", max_batch_size=32)
-    mine, theirs = run_both(ssg, m, t, cluster, trace_fixture(900, 14.0, 2))
+    mine, theirs = run_both(ssg, m, t, cluster, trace_fixture(n, qps, 2))
     assert_same(mine, theirs)
 
 
