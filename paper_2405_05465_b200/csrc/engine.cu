@@ -364,11 +364,13 @@ __global__ void k_build_tables(const SimConfig* __restrict__ cfgs, int32_t n, in
 // those quantities; it stops *before* any iteration that would break a
 // condition (or raise) and hands it to the normal path, so every decision,
 // clock value and counter stays identical.  Returns iterations executed.
+#define SSG_FF_MAX_PP 8  // the fast-forward keeps per-microbatch state in registers
 template <int FMA>
 __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, double next_arrival_time,
                                               double* flops_acc) {
   const SimConfig& c = *U.cfg;
   const int nd = S.run_n, pp = c.pp;
+  if (pp > SSG_FF_MAX_PP) return 0;  // deeper pipelines take the normal path
   const int nm = nd < pp ? nd : pp;  // non-empty microbatches
   const int lane = U.lane;
   const bool mine = lane < nd;
@@ -473,11 +475,11 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, double next_
       lat = __shfl_sync(SSG_FULL, acc, 0);
       fl_tot = __dmul_rn(__shfl_sync(SSG_FULL, fl, 0), (double)c.tp);
     } else {
-      double fin[SSG_MAX_PP];
-      double tim[SSG_MAX_PP];
+      double fin[SSG_FF_MAX_PP];
+      double tim[SSG_FF_MAX_PP];
       fl_tot = 0.0;
 #pragma unroll
-      for (int m = 0; m < SSG_MAX_PP; ++m) {
+      for (int m = 0; m < SSG_FF_MAX_PP; ++m) {
         tim[m] = __shfl_sync(SSG_FULL, acc, m);
         const double fm = __shfl_sync(SSG_FULL, fl, m);
         fin[m] = 0.0;
@@ -486,7 +488,7 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, double next_
       for (int st = 0; st < pp; ++st) {
         double prev = 0.0;
 #pragma unroll
-        for (int m = 0; m < SSG_MAX_PP; ++m) {
+        for (int m = 0; m < SSG_FF_MAX_PP; ++m) {
           if (m < nm) {
             const double start = fin[m] < prev ? prev : fin[m];
             prev = __dadd_rn(start, tim[m]);
@@ -496,7 +498,7 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, double next_
       }
       lat = 0.0;
 #pragma unroll
-      for (int m = 0; m < SSG_MAX_PP; ++m)
+      for (int m = 0; m < SSG_FF_MAX_PP; ++m)
         if (m == nm - 1) lat = fin[m];
     }
     lat = __dadd_rn(lat, c.cpu_overhead);

@@ -24,7 +24,7 @@
 #define SSG_CLS_COMM 2
 
 #define SSG_MAX_OPS 11
-#define SSG_MAX_PP 8
+#define SSG_MAX_PP 16  // microbatch m uses lanes 2m, 2m + 1 of the batch-latency step
 
 // Unit flags
 #define SSG_UF_EMISSIONS 1  // write per-token emission times (CSR)

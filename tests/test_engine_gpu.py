@@ -164,7 +164,8 @@ def test_routing(ssg, ref, routing, replicas, n, qps):
     assert_same(mine, theirs)
 
 
-@pytest.mark.parametrize("tp,pp,policy", [(4, 1, "sarathi_serve"), (2, 2, "vllm"), (1, 4, "orca_plus")])
+@pytest.mark.parametrize("tp,pp,policy", [(4, 1, "sarathi_serve"), (2, 2, "vllm"), (1, 4, "orca_plus"),
+                                         (1, 5, "sarathi_serve"), (1, 16, "vllm")])
 def test_70b_parallelism(ssg, ref, tp, pp, policy):
     """cfg #2 shape (70B, Sarathi cs512) plus pipeline microbatching."""
     m, t = estimators(ssg, ref, "llama2_70b", "h100_80g", [1, 2, 4])
