@@ -546,6 +546,8 @@ void fail(Candidate& C, const SimUnitOut& o) {
 struct SweepKnobs {
   int ladder = 4;  // doubling rates probed per round
   int depth = 3;   // bisection levels probed per round (2^depth - 1 rates)
+  int crit_extra = 2;  // extra levels for the candidates with the longest probes
+  int crit_pct = 95;   // "longest": probes within this % of the group's longest (A/B: DESIGN 6.4)
   int lanes = 1;   // candidate groups advancing independently (streams); measured: no gain
                    // (the sweep is issue-bound, not tail-bound), so one lane by default
   bool block = false;  // groups = contiguous blocks of the capacity order (else dealt)
@@ -555,6 +557,8 @@ SweepKnobs knobs_from_env() {
   SweepKnobs k;
   if (const char* s = std::getenv("SSG_SPEC_LADDER")) k.ladder = std::max(1, std::atoi(s));
   if (const char* s = std::getenv("SSG_SPEC_DEPTH")) k.depth = std::max(1, std::atoi(s));
+  if (const char* s = std::getenv("SSG_SPEC_CRIT")) k.crit_extra = std::max(0, std::atoi(s));
+  if (const char* s = std::getenv("SSG_SPEC_CRIT_PCT")) k.crit_pct = std::max(0, std::atoi(s));
   if (const char* s = std::getenv("SSG_LANES")) k.lanes = std::max(1, std::atoi(s));
   if (const char* s = std::getenv("SSG_LANE_BLOCK")) k.block = s[0] == '1';
   return k;
@@ -676,9 +680,9 @@ void run_group(SweepLane& lane, std::vector<Candidate>& cands, const std::vector
         } catch (const NeedProbe& need) {
           // candidates on the critical path (longest probes) speculate deeper,
           // so their bisection finishes in one round
-          const bool critical = C.probe_iters * 10 >= longest * 9;
+          const bool critical = C.probe_iters * 100 >= longest * knobs.crit_pct;
           std::vector<double> qs;
-          speculate(need, C.copts, knobs.ladder, critical ? knobs.depth + 3 : knobs.depth, qs);
+          speculate(need, C.copts, knobs.ladder, critical ? knobs.depth + knobs.crit_extra : knobs.depth, qs);
           std::vector<double> fresh;
           for (double q : qs)
             if (!C.memo.count(q) && std::find(fresh.begin(), fresh.end(), q) == fresh.end())
