@@ -375,13 +375,26 @@ def main():
 
     from paper_2405_05465_b200.shard import gather_records
 
+    def run_one(i: int, e2e: bool) -> bytes:
+        return ssg.search_shard(sweeps[i][1], rank, world) if e2e else sessions[i].run(rank, world)
+
+    # several sweeps (cfg #5) run concurrently on host threads -- the library's
+    # sessions are thread-safe and each borrows its own streams, so the device
+    # overlaps one sweep's sequential probe chains with the others' work; the
+    # collectives then run one sweep at a time from this thread
+    pool = None
+    if len(sweeps) > 1:
+        from concurrent.futures import ThreadPoolExecutor
+
+        pool = ThreadPoolExecutor(max_workers=len(sweeps))
+
     def step(e2e: bool):
+        if pool is None:
+            shard_recs = [run_one(i, e2e) for i in range(len(sweeps))]
+        else:
+            shard_recs = list(pool.map(lambda i: run_one(i, e2e), range(len(sweeps))))
         outs = []
-        for (name, path), session, count in zip(sweeps, sessions, counts):
-            if e2e:
-                recs = ssg.search_shard(path, rank, world)
-            else:
-                recs = session.run(rank, world)
+        for (name, path), recs, count in zip(sweeps, shard_recs, counts):
             allrecs = gather_records(recs, count, rank, world, rec_size, device=coll_dev)
             outs.append(ssg.search_finalize(path, allrecs) if rank == 0 else None)
         return outs

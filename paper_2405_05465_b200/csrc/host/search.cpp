@@ -738,6 +738,7 @@ struct SearchSession::State {
 SearchSession::SearchSession(const ModelSpec& spec, const std::vector<Request>& workload,
                              const SearchOptions& opts)
     : st_(std::make_unique<State>()) {
+  StatsScope stats_scope;  // sessions may be opened and run on several host threads at once
   PhaseTimer timer("search: session open");
   State& S = *st_;
   S.spec = spec;
@@ -812,6 +813,7 @@ std::vector<ConfigResult> evaluate_configs_shard(const ModelSpec& spec,
 }
 
 std::vector<ConfigResult> SearchSession::evaluate(int shard, int num_shards) {
+  StatsScope stats_scope;  // counters merge into the process totals when the evaluation ends
   PhaseTimer timer("search: evaluate");
   const State& S = *st_;
   const ModelSpec& spec = S.spec;

@@ -67,3 +67,29 @@ def test_sharded_search_equals_whole(ssg, tmp_path):
     whole = ssg.search(path)
     recs = b"".join(ssg.search_shard(path, s, 3) for s in range(3))
     compare(ssg.search_finalize(path, recs), whole)
+
+
+def test_concurrent_sessions_equal_sequential(ssg, tmp_path):
+    """Sweeps run on several host threads at once (the cfg #5 bench does this):
+    each session borrows its own streams and buffers, and every session's records
+    are byte-identical to running them one after another."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    paths = [catalog.write_search_config(
+        str(tmp_path / ("s%d" % i)), model=m, workload=w, skus=("a100_80g",), tp=(1, 2), pp=(1, 2),
+        schedulers=("vllm", "sarathi_serve", "orca_plus"), batch_sizes=(32, 128), chunk_sizes=(512,),
+        max_gpus_total=8, probe_requests=600, num_requests=600)
+        for i, (m, w) in enumerate([("llama2_7b", "chat_like"), ("llama2_70b", "bwb_like"),
+                                    ("qwen_72b", "arxiv_like")])]
+    sessions = [ssg.SearchSession(p) for p in paths]
+    sequential = [s.run() for s in sessions]
+    with ThreadPoolExecutor(len(sessions)) as ex:
+        concurrent = list(ex.map(lambda s: s.run(), sessions))
+    for a, b in zip(sequential, concurrent):
+        assert a == b
+    with ThreadPoolExecutor(len(paths)) as ex:  # one-call form, fresh sessions per thread
+        fresh = list(ex.map(lambda p: ssg.search_shard(p, 0, 1), paths))
+    for a, b in zip(sequential, fresh):
+        assert a == b
+    for s in sessions:
+        s.close()
