@@ -537,7 +537,13 @@ def reference_arm(a, world: int, rank: int):
             "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": 1e3 * sum(s for _, s in times) / len(times),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": "cfg #4 sample, %d configs/step" % k},
+            "data": "synthetic (chat_like lognormal lengths, synth seed 7; Poisson probes seed 1)",
+            "config": {"workload": "cfg #4: LLaMA2-70B Vidur-Search capacity sweep, %d configs "
+                                   "(A100/H100 x tp,pp in {1,2,4} x vLLM/Orca+/Sarathi x bs x cs), "
+                                   "2000 probe requests, tol 0.02, interp estimator" % n_configs,
+                       "configs": n_configs,
+                       "sample": "%d strided configs per step (evaluate_config, the reference's "
+                                 "per-config unit of run_search)" % k},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
                              "sample": "%d strided configs per step, evaluate_config" % k},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
