@@ -351,9 +351,10 @@ __global__ void k_build_tables(const SimConfig* __restrict__ cfgs, int32_t n, in
 
 // ---------------------------------------------------------------- fast-forward
 // Pure-decode stretches of a lone replica (vLLM / Orca+ / LightLLM / Sarathi).
-// While nothing can change the batch -- no request waits (so admission cannot
-// run), every runner is past its prefill and stays unfinished, its block
-// shortfalls fit in free memory (so nothing is preempted), the token budget
+// While nothing can change the batch -- no request waits, or the batch is
+// full (either way admission cannot run), every runner is past its prefill and
+// stays unfinished, its block shortfalls fit in free memory (so nothing is
+// preempted), the token budget
 // covers one decode per runner, and no arrival lands before the batch
 // completes -- each reference iteration is: every runner decodes (in running
 // order), reserves kv+1 tokens, the batch costs predict_batch(...) and
@@ -565,7 +566,12 @@ __device__ SSG_FFWD int fast_forward(Unit& U, RepState& S, double next_arrival_t
   if (c.policy != SSG_POL_VLLM && c.policy != SSG_POL_ORCA && c.policy != SSG_POL_LIGHTLLM &&
       c.policy != SSG_POL_SARATHI)
     return 0;
-  if (S.wait_n != 0 || S.run_n < 1 || S.run_n > 32 || c.tab_off < 0 || c.idx_dec < 0) return 0;
+  // requests may wait only while the batch is full: every policy's admission
+  // loop requires running < max_batch_size before it looks at the queue
+  // (scheduler.hpp:360-361, 387-388, 425-427)
+  if ((S.wait_n != 0 && S.run_n < c.max_batch) || S.run_n < 1 || S.run_n > 32 || c.tab_off < 0 ||
+      c.idx_dec < 0)
+    return 0;
   const int nd = S.run_n, pp = c.pp;
   if (c.policy == SSG_POL_SARATHI ? nd > c.chunk : nd > c.max_tokens) return 0;
   if (nd > c.max_batch || (nd + pp - 1) / pp > c.tab_tmax) return 0;
@@ -735,7 +741,8 @@ __device__ void run_unit(Unit& U) {
     }
     const int r = bw;
     RepState S = reg1 ? S1 : load_rep(U, r);
-    if (FAST && S.ev_kind == 1 && reg1 && S.wait_n == 0 && S.run_n >= 1 && S.run_n <= 32) {
+    if (FAST && S.ev_kind == 1 && reg1 && (S.wait_n == 0 || S.run_n >= c.max_batch) &&
+        S.run_n >= 1 && S.run_n <= 32) {
       // pure-decode stretch: iterations that end at the same state the event
       // loop would reach; afterwards the replica is again "BatchStart at clock"
       double fl = U.out->flops;

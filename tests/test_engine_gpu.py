@@ -317,3 +317,15 @@ def test_sarathi_hybrid_batches_fill_the_budget(ssg, ref):
             assert total == 512  # the chunk fills the budget left by the decodes
             hybrid += 1
     assert hybrid >= 1
+
+
+@pytest.mark.parametrize("policy,extra", [("vllm", {}), ("orca_plus", {}), ("lightllm", {}),
+                                          ("sarathi_serve", {"chunk_size": 256})])
+def test_full_batches_with_a_queue(ssg, ref, policy, extra):
+    """A lone replica saturated at max_batch_size 16: requests wait while the batch
+    is full, which the decode fast-forward treats as a pure-decode stretch (no
+    admission can run); identical to the reference."""
+    m, t = estimators(ssg, ref, "llama2_7b", "a100_80g", [1])
+    cluster = catalog.cluster_doc("llama2_7b", "a100_80g", policy=policy, max_batch_size=16, **extra)
+    mine, theirs = run_both(ssg, m, t, cluster, trace_fixture(500, 30.0, 8))
+    assert_same(mine, theirs)
