@@ -22,6 +22,11 @@
 #include "sim_host.h"
 
 namespace ssgk {
+#ifdef SSG_FF_STATS
+// diagnostics build only: fast-forward calls, committed iterations, histogram
+// of stretch lengths (0, 1, 2-3, 4-7, 8-15, 16-31, 32+), event-loop iterations
+__device__ unsigned long long g_ff_stats[16];
+#endif
 
 // ---------------------------------------------------------------- helpers
 __device__ __forceinline__ RepState load_rep(Unit& U, int r) {
@@ -366,6 +371,18 @@ __global__ void k_build_tables(const SimConfig* __restrict__ cfgs, int32_t n, in
 // condition (or raise) and hands it to the normal path, so every decision,
 // clock value and counter stays identical.  Returns iterations executed.
 #define SSG_FF_MAX_PP 8  // the fast-forward keeps per-microbatch state in registers
+//
+// Lane-parallel over iterations.  Inside a stretch, iteration k's schedule and
+// cost are functions of k alone: runner r reserves kv_r+k+1 tokens holding
+// max(held_r, units(kv_r+k)) (k >= 1), microbatch m's context sum is
+// ctx_m + k*nd_m.  So lane i evaluates iteration done+i of a 32-iteration
+// chunk -- block needs, the decode-attention interpolation per microbatch,
+// the makespan -- all at once; only the order-dependent parts are chained:
+// the allocation (an exact integer prefix scan), and the clock, busy time and
+// flops (fp64 adds performed one iteration after the other, in iteration
+// order, as the reference does).  The committed prefix ends before the first
+// iteration that breaks a condition, exactly where the one-iteration loop
+// stopped.
 template <int FMA>
 __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, double next_arrival_time,
                                               double* flops_acc) {
@@ -373,6 +390,15 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, double next_
   const int nd = S.run_n, pp = c.pp;
   if (pp > SSG_FF_MAX_PP) return 0;  // deeper pipelines take the normal path
   const int nm = nd < pp ? nd : pp;  // non-empty microbatches
+  {
+    // cheapest exit first: iteration 0 completes no earlier than
+    // clock + S6[size of microbatch 0] + cpu overhead (every further term of
+    // the latency is a non-negative prediction, and round-to-nearest adds of
+    // non-negative terms never decrease), so an arrival at or before that
+    // point stops the stretch before it starts
+    const double lb = __dadd_rn(U.tables[c.tab_off + (nd + pp - 1) / pp], c.cpu_overhead);
+    if (next_arrival_time <= __dadd_rn(U.clock, lb)) return 0;
+  }
   const int lane = U.lane;
   const bool mine = lane < nd;
   // runner state, one per lane (running order == decode entry order)
@@ -406,7 +432,7 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, double next_
   const int nd_m = lane < nm ? (nd - lane + pp - 1) / pp : 0;
   const double* tab = U.tables + c.tab_off;
   const int T1 = c.tab_stride;
-  double tok_s = 0.0, tok_f = 0.0, comm_s[3] = {0.0, 0.0, 0.0};
+  double tok_s = 0.0, tok_f = 0.0, comm_sum[3] = {0.0, 0.0, 0.0};
   int32_t lo0 = 0;
   double f0 = 0.0;
   bool ok = true;
@@ -415,7 +441,7 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, double next_
     tok_f = tab[(int64_t)T1 + nd_m];
 #pragma unroll
     for (int k = 0; k < 3; ++k)
-      if (k < c.ncomm) comm_s[k] = tab[(int64_t)(2 + k) * T1 + nd_m];
+      if (k < c.ncomm) comm_sum[k] = tab[(int64_t)(2 + k) * T1 + nd_m];
     const double v0 = (double)nd_m;
     ok = v0 >= md.lower[0] && v0 <= md.upper[0];
     ssg_axis_cell(U.E.dpool + md.axis_off[0], md.axis_len[0], ssg_log1p(v0, FMA), &lo0, &f0);
@@ -423,69 +449,93 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, double next_
   if (!__all_sync(SSG_FULL, ok)) return 0;
   const int32_t n1 = md.axis_len[1];
   const int32_t h0 = md.axis_len[0] == 1 ? 0 : 1;
-  const double g0 = __dsub_rn(1.0, f0);
-  const double w0lo = g0, w0hi = h0 ? f0 : g0;
   const double* vals = U.E.dpool + md.values_off;
   const double* ax1 = U.E.dpool + md.axis_off[1];
-  const int64_t r0 = (int64_t)lo0 * n1, r1 = (int64_t)(lo0 + h0) * n1;
   const bool emit_times = (U.u->flags & SSG_UF_EMISSIONS) != 0;
   const bool logging = (U.u->flags & SSG_UF_BATCH_LOG) != 0;
   const double fa4 = od.fa;
+  // emission slot of this runner's next token
+  const int64_t ebase = (mine && emit_times) ? U.emit_base[j] + (U.hot[j].decode - rem) : 0;
+  const int64_t free0 = c.total_units;
   int done = 0;
   while (done < max_iters) {
-    // schedule: every runner reserves kv+1 tokens (must all fit: no preemption)
-    const int64_t need = mine ? shortfall_held(c, held, (int64_t)kv + 1) : 0;
-    const int64_t total_need = warp_sum64(need);
-    if (total_need > c.total_units - S.allocated) break;
-    // decode attention of microbatch m on lane m, then the operator-order sum
-    double acc = 0.0, fl = 0.0;
+    const int k = done + lane;  // this lane's iteration
+    const bool active = k < max_iters;
+    // ---- schedule: every runner reserves kv+k+1 tokens (no preemption allowed)
+    int64_t need = 0;
+    for (int r = 0; r < nd; ++r) {
+      const int32_t kv_r = __shfl_sync(SSG_FULL, kv, r);
+      const int32_t held_r = __shfl_sync(SSG_FULL, held, r);
+      int64_t hk = held_r;
+      if (k > 0) {
+        const int64_t u = units_for(c, (int64_t)kv_r + k);
+        hk = hk < u ? u : hk;
+      }
+      const int64_t s = units_for(c, (int64_t)kv_r + k + 1) - hk;
+      need += s > 0 ? s : 0;
+    }
+    // ---- cost: decode attention per microbatch, operator order, makespan
+    double tim[SSG_FF_MAX_PP];
+    double fl_tot = 0.0;
     int good = 1;
-    if (lane < nm) {
-      const double v1 = __dmul_rn((double)ctx_m, od.kvb);
-      if (!(v1 >= md.lower[1] && v1 <= md.upper[1])) {
-        good = 0;
-      } else {
-        int32_t lo1;
-        double f1;
-        ssg_axis_cell_hint(ax1, n1, ssg_log1p(v1, FMA), &U.ax1_hint, &lo1, &f1);
-        const int32_t h1 = n1 == 1 ? 0 : 1;
-        const double g1 = __dsub_rn(1.0, f1);
-        const double w1lo = g1, w1hi = h1 ? f1 : g1;
-        double r = __dmul_rn(__dmul_rn(w1lo, w0lo), __ldg(vals + r0 + lo1));
-        r = __dadd_rn(r, __dmul_rn(__dmul_rn(w1lo, w0hi), __ldg(vals + r1 + lo1)));
-        r = __dadd_rn(r, __dmul_rn(__dmul_rn(w1hi, w0lo), __ldg(vals + r0 + lo1 + h1)));
-        r = __dadd_rn(r, __dmul_rn(__dmul_rn(w1hi, w0hi), __ldg(vals + r1 + lo1 + h1)));
-        if (!ssg_exp_in_range(r)) {
+#pragma unroll
+    for (int m = 0; m < SSG_FF_MAX_PP; ++m) {
+      tim[m] = 0.0;
+      if (m < nm) {
+        const int64_t cm0 = __shfl_sync(SSG_FULL, ctx_m, m);
+        const int ndm = __shfl_sync(SSG_FULL, nd_m, m);
+        const int32_t lo0m = __shfl_sync(SSG_FULL, lo0, m);
+        const double f0m = __shfl_sync(SSG_FULL, f0, m);
+        const double ts = __shfl_sync(SSG_FULL, tok_s, m);
+        const double tf = __shfl_sync(SSG_FULL, tok_f, m);
+        double cs[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) cs[q] = __shfl_sync(SSG_FULL, comm_sum[q], m);
+        const double g0 = __dsub_rn(1.0, f0m);
+        const double w0lo = g0, w0hi = h0 ? f0m : g0;
+        const int64_t r0 = (int64_t)lo0m * n1, r1 = (int64_t)(lo0m + h0) * n1;
+        const double v1 = __dmul_rn((double)(cm0 + (int64_t)k * ndm), od.kvb);
+        if (!(v1 >= md.lower[1] && v1 <= md.upper[1])) {
           good = 0;
         } else {
-          const double pred = __dmul_rn(od.count, ssg_exp(r, FMA));
-          acc = __dadd_rn(tok_s, pred);
+          int32_t lo1;
+          double f1;
+          ssg_axis_cell_hint(ax1, n1, ssg_log1p(v1, FMA), &U.ax1_hint, &lo1, &f1);
+          const int32_t h1 = n1 == 1 ? 0 : 1;
+          const double g1 = __dsub_rn(1.0, f1);
+          const double w1lo = g1, w1hi = h1 ? f1 : g1;
+          double r = __dmul_rn(__dmul_rn(w1lo, w0lo), __ldg(vals + r0 + lo1));
+          r = __dadd_rn(r, __dmul_rn(__dmul_rn(w1lo, w0hi), __ldg(vals + r1 + lo1)));
+          r = __dadd_rn(r, __dmul_rn(__dmul_rn(w1hi, w0lo), __ldg(vals + r0 + lo1 + h1)));
+          r = __dadd_rn(r, __dmul_rn(__dmul_rn(w1hi, w0hi), __ldg(vals + r1 + lo1 + h1)));
+          if (!ssg_exp_in_range(r)) {
+            good = 0;
+          } else {
+            const double pred = __dmul_rn(od.count, ssg_exp(r, FMA));
+            double acc = __dadd_rn(ts, pred);
 #pragma unroll
-          for (int k = 0; k < 3; ++k)
-            if (k < c.ncomm) acc = __dadd_rn(acc, comm_s[k]);
-          const double ctx_tokens = v1 / od.kvb;
-          fl = __dadd_rn(tok_f, __dmul_rn(od.count, __dmul_rn(__dmul_rn(4.0, ctx_tokens), fa4)));
-          if (!(acc > 0.0)) good = 0;
+            for (int q = 0; q < 3; ++q)
+              if (q < c.ncomm) acc = __dadd_rn(acc, cs[q]);
+            const double ctx_tokens = v1 / od.kvb;
+            const double fl = __dadd_rn(tf, __dmul_rn(od.count, __dmul_rn(__dmul_rn(4.0, ctx_tokens), fa4)));
+            if (!(acc > 0.0)) good = 0;
+            tim[m] = acc;
+            if (pp == 1)
+              fl_tot = __dmul_rn(fl, (double)c.tp);
+            else
+              fl_tot = __dadd_rn(fl_tot, __dmul_rn(fl, (double)(c.tp * c.pp)));
+          }
         }
       }
     }
-    if (!__all_sync(SSG_FULL, good)) break;  // the normal path raises it
-    // latency: pipeline makespan over the microbatches (all lanes, same values)
-    double lat, fl_tot;
+    double lat;
     if (pp == 1) {
-      lat = __shfl_sync(SSG_FULL, acc, 0);
-      fl_tot = __dmul_rn(__shfl_sync(SSG_FULL, fl, 0), (double)c.tp);
+      lat = tim[0];
     } else {
+      // synchronous pipeline finish times (scheduler.hpp:566-579)
       double fin[SSG_FF_MAX_PP];
-      double tim[SSG_FF_MAX_PP];
-      fl_tot = 0.0;
 #pragma unroll
-      for (int m = 0; m < SSG_FF_MAX_PP; ++m) {
-        tim[m] = __shfl_sync(SSG_FULL, acc, m);
-        const double fm = __shfl_sync(SSG_FULL, fl, m);
-        fin[m] = 0.0;
-        if (m < nm) fl_tot = __dadd_rn(fl_tot, __dmul_rn(fm, (double)(c.tp * c.pp)));
-      }
+      for (int m = 0; m < SSG_FF_MAX_PP; ++m) fin[m] = 0.0;
       for (int st = 0; st < pp; ++st) {
         double prev = 0.0;
 #pragma unroll
@@ -503,56 +553,105 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, double next_
         if (m == nm - 1) lat = fin[m];
     }
     lat = __dadd_rn(lat, c.cpu_overhead);
-    if (!(lat > 0.0)) break;
-    const double t_done = __dadd_rn(U.clock, lat);
-    // an arrival at or before this completion is processed between the batch's
-    // start and completion events: that iteration belongs to the event loop
-    if (next_arrival_time <= t_done) break;
-    // ---- the iteration happens
-    U.serial += 1;
-    held += (int32_t)need;
-    S.allocated += total_need;
+    // ---- the order-dependent parts, in iteration order
+    // allocation before this lane's iteration: exclusive prefix of the needs
+    int64_t incl = need;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t t = __shfl_up_sync(SSG_FULL, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int64_t alloc_after = S.allocated + incl;
+    const bool fits = need <= free0 - (alloc_after - need);
+    // iterations that can happen as far as memory and the cost go
+    const bool pre = active && fits && good && lat > 0.0;
+    const unsigned bad = __ballot_sync(SSG_FULL, !pre);
+    const int C = bad ? __ffs(bad) - 1 : 32;
+    if (C == 0) break;
+    // clock / busy time / flops: one fp64 add per iteration, in order; the
+    // chain (warp-uniform) stops at the first completion at or after the next
+    // arrival: an arrival at or before a completion is processed between the
+    // batch's start and completion events, so that iteration is the loop's
+    double clk = U.clock, busy = S.busy_time, fla = *flops_acc;
+    double t_done = 0.0;
+    int K = 0;
+#pragma unroll 4
+    for (; K < C; ++K) {
+      const double li = __shfl_sync(SSG_FULL, lat, K);
+      const double fi = __shfl_sync(SSG_FULL, fl_tot, K);
+      const double c2 = __dadd_rn(clk, li);
+      if (next_arrival_time <= c2) break;
+      clk = c2;
+      busy = __dadd_rn(busy, li);
+      fla = __dadd_rn(fla, fi);
+      if (lane == K) t_done = clk;
+    }
+    if (K == 0) break;
+    const int last = K - 1;
+    // ---- commit iterations done .. done+K-1
     if (logging) {
       const int64_t need_w = 6 + 2LL * nd;
       const int64_t used = U.out->log_used;
-      if (used >= 0 && used + need_w <= U.u->log_cap) {
-        int64_t* L = U.log + used;
-        if (lane == 0) {
-          L[0] = 0;
-          L[1] = __double_as_longlong(U.clock);
-          L[2] = S.allocated;
-          L[3] = 0;
-          L[4] = nd;
-          L[5] = __double_as_longlong(lat);
+      int64_t fit = 0;
+      if (used >= 0) {
+        fit = (U.u->log_cap - used) / need_w;
+        fit = fit < 0 ? 0 : (fit > K ? K : fit);
+      }
+      if (lane < fit) {
+        int64_t* L = U.log + used + lane * need_w;
+        L[0] = 0;
+        L[2] = alloc_after;
+        L[3] = 0;
+        L[4] = nd;
+        L[5] = __double_as_longlong(lat);
+      }
+      // batch start clock of iteration i = completion of iteration i-1
+      const double t_prev = __shfl_up_sync(SSG_FULL, t_done, 1);
+      if (lane < fit) U.log[used + lane * need_w + 1] = __double_as_longlong(lane == 0 ? U.clock : t_prev);
+      for (int r = 0; r < nd; ++r) {
+        const int64_t id_r = U.ids[__shfl_sync(SSG_FULL, j, r)];
+        const int32_t kv_r = __shfl_sync(SSG_FULL, kv, r);
+        if (lane < fit) {
+          int64_t* L = U.log + used + lane * need_w;
+          L[6 + 2 * r] = id_r;
+          L[7 + 2 * r] = (int64_t)kv_r + k + 1;
         }
-        if (mine) {
-          L[6 + 2 * lane] = U.ids[j];
-          L[7 + 2 * lane] = kv + 1;
-        }
-        wput(U, &U.out->log_used, used + need_w);
-      } else {
-        wput(U, &U.out->log_used, (int64_t)-1);
+      }
+      __syncwarp();
+      wput(U, &U.out->log_used, used >= 0 && fit == K ? used + K * need_w : (int64_t)-1);
+    }
+    if (emit_times) {
+      for (int r = 0; r < nd; ++r) {
+        const int64_t e = __shfl_sync(SSG_FULL, ebase, r);
+        if (lane < K) U.emissions[e + k] = t_done;
       }
     }
-    S.busy_time = __dadd_rn(S.busy_time, lat);
-    S.iterations += 1;
-    S.tokens += nd;
-    const double util = (double)S.allocated / (double)c.total_units;
-    S.peak_kv = S.peak_kv < util ? util : S.peak_kv;
-    *flops_acc = __dadd_rn(*flops_acc, fl_tot);
-    U.iters += 1;
-    U.entries += nd;
-    U.qbytes += (int64_t)nm * (c.qb_fixed + c.qb_dec);
-    kv += 1;
-    if (mine && emit_times) U.emissions[U.emit_base[j] + (U.hot[j].decode - rem) + done] = t_done;
-    ctx_m += nd_m;
-    U.clock = t_done;
-    ++done;
+    const double util = (double)alloc_after / (double)c.total_units;
+    double pk = lane < K ? util : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double t = __shfl_xor_sync(SSG_FULL, pk, o);
+      pk = pk < t ? t : pk;
+    }
+    S.peak_kv = S.peak_kv < pk ? pk : S.peak_kv;
+    S.allocated = __shfl_sync(SSG_FULL, alloc_after, last);
+    S.busy_time = busy;
+    *flops_acc = fla;
+    U.clock = clk;
+    U.serial += K;
+    S.iterations += K;
+    S.tokens += (int64_t)nd * K;
+    U.iters += K;
+    U.entries += (int64_t)nd * K;
+    U.qbytes += (int64_t)K * nm * (c.qb_fixed + c.qb_dec);
+    done += K;
+    if (K < 32) break;
   }
   if (done > 0 && mine) {
     ReqHot& h = U.hot[j];
-    h.kv = kv;
-    h.held = held;
+    const int64_t u = units_for(c, (int64_t)kv + done);
+    h.kv = kv + done;
+    h.held = held < u ? (int32_t)u : held;
     h.emitted = h.emitted + done;
   }
   __syncwarp();
@@ -747,6 +846,13 @@ __device__ void run_unit(Unit& U) {
       // loop would reach; afterwards the replica is again "BatchStart at clock"
       double fl = U.out->flops;
       const int k = fast_forward<FMA>(U, S, next_arrival_time, &fl);
+#ifdef SSG_FF_STATS
+      if (U.lane == 0) {
+        atomicAdd(&g_ff_stats[0], 1ull);
+        atomicAdd(&g_ff_stats[1], (unsigned long long)k);
+        atomicAdd(&g_ff_stats[2 + (k == 0 ? 0 : min(6, 32 - __clz(k)))], 1ull);
+      }
+#endif
       if (k > 0) {
         wput(U, &U.out->flops, fl);
         events += 2 * k;
@@ -918,6 +1024,15 @@ __global__ void __launch_bounds__(SSG_SIM_WARPS * 32)
 }
 
 }  // namespace ssgk
+#ifdef SSG_FF_STATS
+extern "C" void ssg_debug_ff_stats(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, ssgk::g_ff_stats, sizeof(ssgk::g_ff_stats));
+  if (reset) {
+    unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(ssgk::g_ff_stats, z, sizeof z);
+  }
+}
+#endif
 
 namespace ssg {
 
