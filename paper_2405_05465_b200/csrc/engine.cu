@@ -26,6 +26,9 @@ namespace ssgk {
 // diagnostics build only: fast-forward calls, committed iterations, histogram
 // of stretch lengths (0, 1, 2-3, 4-7, 8-15, 16-31, 32+), event-loop iterations
 __device__ unsigned long long g_ff_stats[16];
+#define FFSTAT(i) do { if (U.lane == 0) atomicAdd(&g_ff_stats[i], 1ull); } while (0)
+#else
+#define FFSTAT(i) do { } while (0)
 #endif
 
 // ---------------------------------------------------------------- helpers
@@ -397,7 +400,7 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, double next_
     // non-negative terms never decrease), so an arrival at or before that
     // point stops the stretch before it starts
     const double lb = __dadd_rn(U.tables[c.tab_off + (nd + pp - 1) / pp], c.cpu_overhead);
-    if (next_arrival_time <= __dadd_rn(U.clock, lb)) return 0;
+    if (next_arrival_time <= __dadd_rn(U.clock, lb)) { FFSTAT(9); return 0; }
   }
   const int lane = U.lane;
   const bool mine = lane < nd;
@@ -418,7 +421,7 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, double next_
     min_rem = t < min_rem ? t : min_rem;
   }
   const int max_iters = min_rem - 1;
-  if (max_iters < 1) return 0;
+  if (max_iters < 1) { FFSTAT(10); return 0; }
   // per-microbatch invariants on lane m < nm: size, context sum, decode model cell
   const SimOp& od = c.ops[c.idx_dec];
   const SsgModelDesc& md = U.E.models[od.slot];
@@ -446,7 +449,7 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, double next_
     ok = v0 >= md.lower[0] && v0 <= md.upper[0];
     ssg_axis_cell(U.E.dpool + md.axis_off[0], md.axis_len[0], ssg_log1p(v0, FMA), &lo0, &f0);
   }
-  if (!__all_sync(SSG_FULL, ok)) return 0;
+  if (!__all_sync(SSG_FULL, ok)) { FFSTAT(11); return 0; }
   const int32_t n1 = md.axis_len[1];
   const int32_t h0 = md.axis_len[0] == 1 ? 0 : 1;
   const double* vals = U.E.dpool + md.values_off;
@@ -567,7 +570,7 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, double next_
     const bool pre = active && fits && good && lat > 0.0;
     const unsigned bad = __ballot_sync(SSG_FULL, !pre);
     const int C = bad ? __ffs(bad) - 1 : 32;
-    if (C == 0) break;
+    if (C == 0) { if (done == 0) FFSTAT(12); break; }
     // clock / busy time / flops: one fp64 add per iteration, in order; the
     // chain (warp-uniform) stops at the first completion at or after the next
     // arrival: an arrival at or before a completion is processed between the
@@ -586,7 +589,7 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, double next_
       fla = __dadd_rn(fla, fi);
       if (lane == K) t_done = clk;
     }
-    if (K == 0) break;
+    if (K == 0) { if (done == 0) FFSTAT(13); break; }
     const int last = K - 1;
     // ---- commit iterations done .. done+K-1
     if (logging) {
@@ -840,6 +843,12 @@ __device__ void run_unit(Unit& U) {
     }
     const int r = bw;
     RepState S = reg1 ? S1 : load_rep(U, r);
+#ifdef SSG_FF_STATS
+    if (FAST && S.ev_kind == 1 && reg1) {
+      if (S.run_n > 32) FFSTAT(14);
+      else if (!(S.wait_n == 0 || S.run_n >= c.max_batch)) FFSTAT(15);
+    }
+#endif
     if (FAST && S.ev_kind == 1 && reg1 && (S.wait_n == 0 || S.run_n >= c.max_batch) &&
         S.run_n >= 1 && S.run_n <= 32) {
       // pure-decode stretch: iterations that end at the same state the event

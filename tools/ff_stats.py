@@ -2,7 +2,7 @@
 VARIANT_FLAGS=-DSSG_FF_STATS, passed as SSG_LIB).  Runs cfg #1, cfg #2 and a
 sweep shard (AB_SHARD=r/N, default 0/8) and prints, for each, the number of
 fast-forward calls, the iterations they committed, the total iterations and
-the histogram of stretch lengths (0, 1, 2-3, 4-7, 8-15, 16-31, 32+)."""
+the histogram of stretch lengths (0, 1, 2-3, 4-7, 8-15, 16-31, 32+); then zero-length reasons: arrival pre-filter, a runner finishing, bbox, memory/cost, arrival in the chain; and BatchStarts not tried: > 32 runners, requests waiting."""
 import ctypes as C, os, sys, tempfile
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -18,8 +18,8 @@ def report(label):
     L.ssg_debug_ff_stats(buf, 1)
     st = ssg.stats()
     v = list(buf)
-    print("%-10s ff_calls %d ff_iters %d of %d iterations (%.0f%%) hist %s" % (
-        label, v[0], v[1], st["iterations"], 100.0 * v[1] / max(1, st["iterations"]), v[2:9]), flush=True)
+    print("%-10s ff_calls %d ff_iters %d of %d iterations (%.0f%%) hist %s zero-reasons %s not-tried %s" % (
+        label, v[0], v[1], st["iterations"], 100.0 * v[1] / max(1, st["iterations"]), v[2:9], v[9:14], v[14:16]), flush=True)
 
 
 L.ssg_debug_ff_stats(buf, 1)
