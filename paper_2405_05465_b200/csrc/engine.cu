@@ -374,6 +374,18 @@ __global__ void k_build_tables(const SimConfig* __restrict__ cfgs, int32_t n, in
 // condition (or raise) and hands it to the normal path, so every decision,
 // clock value and counter stays identical.  Returns iterations executed.
 #define SSG_FF_MAX_PP 8  // the fast-forward keeps per-microbatch state in registers
+#ifndef SSG_FF_ARRIVE_ONE
+#define SSG_FF_ARRIVE_ONE 1  // a batch that is not full still runs the iteration an arrival lands in
+#endif
+//
+// Arrivals.  A request arriving during an iteration (at or before its
+// completion: arrivals carry the lower sequence numbers) is routed to the lone
+// replica and enqueued while the replica is busy, so the batch in flight is
+// unaffected.  A full batch stays the same batch afterwards (every policy admits
+// only while running < max_batch_size), so the stretch goes on with the queue
+// longer; a batch that is not full ends the stretch after that iteration, and
+// the next BatchStart (admission) is the event loop's.  An arrival whose
+// enqueue would raise (KV capacity) ends the stretch before its iteration.
 //
 // Lane-parallel over iterations.  Inside a stretch, iteration k's schedule and
 // cost are functions of k alone: runner r reserves kv_r+k+1 tokens holding
@@ -387,8 +399,8 @@ __global__ void k_build_tables(const SimConfig* __restrict__ cfgs, int32_t n, in
 // iteration that breaks a condition, exactly where the one-iteration loop
 // stopped.
 template <int FMA>
-__device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, double next_arrival_time,
-                                              double* flops_acc) {
+__device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* next_arrival,
+                                              double* next_arrival_time, double* flops_acc) {
   const SimConfig& c = *U.cfg;
   const int nd = S.run_n, pp = c.pp;
   if (pp > SSG_FF_MAX_PP) return 0;  // deeper pipelines take the normal path
@@ -400,7 +412,11 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, double next_
     // non-negative terms never decrease), so an arrival at or before that
     // point stops the stretch before it starts
     const double lb = __dadd_rn(U.tables[c.tab_off + (nd + pp - 1) / pp], c.cpu_overhead);
-    if (next_arrival_time <= __dadd_rn(U.clock, lb)) { FFSTAT(9); return 0; }
+    if (!SSG_FF_ARRIVE_ONE && nd < c.max_batch && *next_arrival < U.u->n &&
+        *next_arrival_time <= __dadd_rn(U.clock, lb)) {
+      FFSTAT(9);
+      return 0;
+    }
   }
   const int lane = U.lane;
   const bool mine = lane < nd;
@@ -578,16 +594,41 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, double next_
     double clk = U.clock, busy = S.busy_time, fla = *flops_acc;
     double t_done = 0.0;
     int K = 0;
-#pragma unroll 4
+    const int32_t na0 = *next_arrival;
+    int32_t na = na0;                  // arrivals up to the last committed completion
+    // (the event loop keeps the last arrival's time once every arrival is in)
+    double ta = na0 < U.u->n ? *next_arrival_time : INFINITY;
+    bool ends = false;                 // an arrival ends the stretch after iteration K
     for (; K < C; ++K) {
       const double li = __shfl_sync(SSG_FULL, lat, K);
       const double fi = __shfl_sync(SSG_FULL, fl_tot, K);
       const double c2 = __dadd_rn(clk, li);
-      if (next_arrival_time <= c2) break;
+      int32_t na2 = na;
+      double ta2 = ta;
+      bool reject = false;
+      while (ta2 <= c2) {  // arrivals during iteration K
+        const int32_t ja = U.arr_order ? U.arr_order[na2] : na2;
+        const ReqHot h = U.hot[ja];
+        if (units_for(c, (int64_t)h.prefill + h.decode) > c.total_units) {
+          reject = true;  // enqueue raises: the event loop's
+          break;
+        }
+        ++na2;
+        ta2 = na2 < U.u->n ? U.tm[U.arr_order ? U.arr_order[na2] : na2].arrival : INFINITY;
+      }
+      if (reject) break;
       clk = c2;
       busy = __dadd_rn(busy, li);
       fla = __dadd_rn(fla, fi);
       if (lane == K) t_done = clk;
+      const bool arrived = na2 != na;
+      na = na2;
+      ta = ta2;
+      if (arrived && nd < c.max_batch) {
+        ends = true;
+        ++K;
+        break;
+      }
     }
     if (K == 0) { if (done == 0) FFSTAT(13); break; }
     const int last = K - 1;
@@ -648,7 +689,12 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, double next_
     U.entries += (int64_t)nd * K;
     U.qbytes += (int64_t)K * nm * (c.qb_fixed + c.qb_dec);
     done += K;
-    if (K < 32) break;
+    // the arrivals of the committed iterations: routed to the lone replica and
+    // enqueued (sim.hpp:211-220); the replica is busy, so nothing starts
+    for (int32_t q = na0; q < na; ++q) enqueue(U, S, 0, U.arr_order ? U.arr_order[q] : q);
+    *next_arrival = na;
+    *next_arrival_time = ta;
+    if (ends || K < 32) break;
   }
   if (done > 0 && mine) {
     ReqHot& h = U.hot[j];
@@ -662,8 +708,8 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, double next_
 }
 
 template <int FMA>
-__device__ SSG_FFWD int fast_forward(Unit& U, RepState& S, double next_arrival_time,
-                                     double* flops_acc) {
+__device__ SSG_FFWD int fast_forward(Unit& U, RepState& S, int32_t* next_arrival,
+                                     double* next_arrival_time, double* flops_acc) {
   const SimConfig& c = *U.cfg;
   if (c.policy != SSG_POL_VLLM && c.policy != SSG_POL_ORCA && c.policy != SSG_POL_LIGHTLLM &&
       c.policy != SSG_POL_SARATHI)
@@ -677,7 +723,7 @@ __device__ SSG_FFWD int fast_forward(Unit& U, RepState& S, double next_arrival_t
   const int nd = S.run_n, pp = c.pp;
   if (c.policy == SSG_POL_SARATHI ? nd > c.chunk : nd > c.max_tokens) return 0;
   if (nd > c.max_batch || (nd + pp - 1) / pp > c.tab_tmax) return 0;
-  return fast_forward_t<FMA>(U, S, next_arrival_time, flops_acc);
+  return fast_forward_t<FMA>(U, S, next_arrival, next_arrival_time, flops_acc);
 }
 
 template <int FMA, int FOREST, int FAST>
@@ -854,7 +900,8 @@ __device__ void run_unit(Unit& U) {
       // pure-decode stretch: iterations that end at the same state the event
       // loop would reach; afterwards the replica is again "BatchStart at clock"
       double fl = U.out->flops;
-      const int k = fast_forward<FMA>(U, S, next_arrival_time, &fl);
+      const int32_t na_before = next_arrival;
+      const int k = fast_forward<FMA>(U, S, &next_arrival, &next_arrival_time, &fl);
 #ifdef SSG_FF_STATS
       if (U.lane == 0) {
         atomicAdd(&g_ff_stats[0], 1ull);
@@ -864,7 +911,7 @@ __device__ void run_unit(Unit& U) {
 #endif
       if (k > 0) {
         wput(U, &U.out->flops, fl);
-        events += 2 * k;
+        events += 2 * k + (next_arrival - na_before);
         S.ev_time = U.clock;
         S.ev_seq = U.seq++;
         S1 = S;
