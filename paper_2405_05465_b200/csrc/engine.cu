@@ -984,9 +984,15 @@ __device__ void run_unit(Unit& U) {
 #ifndef SSG_SIM_MINB
 #define SSG_SIM_MINB 6  // 6 blocks x 2 warps per SM: <= 168 registers (measured best, DESIGN 6.4)
 #endif
+#ifdef SSG_FAST_MAXNREG
+// diagnostic builds: a register cap for the fast-forward variant between the
+// launch-bounds steps (A/B of occupancy against spills)
+#define SSG_SIM_BOUNDS(FAST) __launch_bounds__(SSG_SIM_WARPS * 32) __maxnreg__(FAST ? SSG_FAST_MAXNREG : 168)
+#else
+#define SSG_SIM_BOUNDS(FAST) __launch_bounds__(SSG_SIM_WARPS * 32, FAST ? SSG_SIM_FAST_MINB : SSG_SIM_MINB)
+#endif
 template <int FMA, int FOREST, int FAST>
-__global__ void __launch_bounds__(SSG_SIM_WARPS * 32, FAST ? SSG_SIM_FAST_MINB : SSG_SIM_MINB)
-    k_simulate(SimLaunch L) {
+__global__ void SSG_SIM_BOUNDS(FAST) k_simulate(SimLaunch L) {
   __shared__ int64_t stats[SSG_SIM_WARPS][SSG_MAX_PP * 6];
   __shared__ double part[SSG_SIM_WARPS][4 * SSG_MAX_PP];
   __shared__ SimConfig cfg_s[SSG_SIM_WARPS];  // the unit's config, read every event

@@ -414,14 +414,15 @@ void run_launch(SweepLane& lane, ProbeLaunch& L, const ResidentWorkload& w,
   K.log = nullptr;
   K.out = B.out.ptr;
   K.tables = lane.tables;
-  // decode fast-forward only for launches too small to fill the device (its
-  // larger body costs I-cache misses when many warps share an SM, and saves
-  // half the work of a lone warp's decode stretches)
-  // (measured on cfg #4 shards: threshold 16 units per SM is the best of
-  // 6/8/12/16 for 1, 2, 4 and 8 shards; a 1/8 shard goes 0.91 -> 0.68 s)
+  // decode fast-forward variant for every launch with at most SSG_FF_UNITS
+  // units (default: all).  Measured on cfg #4 shards since the fast-forward
+  // runs lane-parallel over iterations and through arrivals: all launches
+  // beat the earlier threshold of 16 units per SM at every shard count
+  // (1/2 shard 0.944 -> 0.742 s, full sweep 1.207 -> 1.193 s); before, its
+  // larger body lost to instruction-cache misses on loaded launches.
   const int64_t ff_units = [] {
     const char* e = std::getenv("SSG_FF_UNITS");
-    return e ? std::atoll(e) : 16LL * context().num_sms;
+    return e ? std::atoll(e) : INT64_MAX;
   }();
   K.fast_forward = sweep_fast_forward_enabled() ||
                    static_cast<int64_t>(L.units.size()) <= ff_units ? 1 : 0;
