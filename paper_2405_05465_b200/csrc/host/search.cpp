@@ -415,14 +415,15 @@ void run_launch(SweepLane& lane, ProbeLaunch& L, const ResidentWorkload& w,
   K.out = B.out.ptr;
   K.tables = lane.tables;
   // decode fast-forward variant for every launch with at most SSG_FF_UNITS
-  // units (default: all).  Measured on cfg #4 shards since the fast-forward
-  // runs lane-parallel over iterations and through arrivals: all launches
-  // beat the earlier threshold of 16 units per SM at every shard count
-  // (1/2 shard 0.944 -> 0.742 s, full sweep 1.207 -> 1.193 s); before, its
-  // larger body lost to instruction-cache misses on loaded launches.
+  // units (default 54 per SM).  Measured on cfg #4 shards since the
+  // fast-forward runs lane-parallel over iterations and through arrivals: it
+  // beats the earlier threshold of 16 units per SM at every shard count (1/2
+  // shard 0.944 -> 0.742 s), and only the two most loaded rounds of the full
+  // sweep (~10K units: its 240-register body fits 8 warps per SM, the other
+  // 12) still run faster without it (full sweep 1.188 -> 1.158 s with the cap).
   const int64_t ff_units = [] {
     const char* e = std::getenv("SSG_FF_UNITS");
-    return e ? std::atoll(e) : INT64_MAX;
+    return e ? std::atoll(e) : 54LL * context().num_sms;
   }();
   K.fast_forward = sweep_fast_forward_enabled() ||
                    static_cast<int64_t>(L.units.size()) <= ff_units ? 1 : 0;
