@@ -329,3 +329,29 @@ def test_full_batches_with_a_queue(ssg, ref, policy, extra):
     cluster = catalog.cluster_doc("llama2_7b", "a100_80g", policy=policy, max_batch_size=16, **extra)
     mine, theirs = run_both(ssg, m, t, cluster, trace_fixture(500, 30.0, 8))
     assert_same(mine, theirs)
+
+
+@pytest.mark.parametrize("policy,extra", [("vllm", {}), ("orca_plus", {}), ("lightllm", {}),
+                                          ("sarathi_serve", {"chunk_size": 256})])
+@pytest.mark.parametrize("max_batch,qps", [(8, 40.0), (64, 3.0)])
+def test_fast_forward_through_arrivals(ssg, ref, policy, extra, max_batch, qps):
+    """Binary-output runs (no batch log) whose decode stretches take arrivals:
+    a full batch (max_batch 8, overloaded) keeps its stretch going with a longer
+    queue, a batch that is not full (light load) ends it after the iteration the
+    request arrives in; the trace tail runs past the last arrival.  Per-request
+    times, every token's emission time and the report equal the reference's."""
+    m, t = estimators(ssg, ref, "llama2_7b", "a100_80g", [1])
+    cluster = catalog.cluster_doc("llama2_7b", "a100_80g", policy=policy, max_batch_size=max_batch, **extra)
+    ids, arr, pre, dec = trace_fixture(400, qps, 11)
+    run = ssg.simulate_run(cluster, m, ids, arr, pre, dec)
+    theirs = t.simulate(cluster, ids, arr, pre, dec)
+    for i, q in enumerate(theirs["requests"]):
+        assert run.first_scheduled[i] == q["first_scheduled"] and run.first_token[i] == q["first_token"], i
+        assert run.completion[i] == q["completion"] and run.restarts[i] == q["restarts"], i
+    emis = np.concatenate([np.asarray(q["emissions"]) for q in theirs["requests"]])
+    assert np.array_equal(run.emissions[:len(emis)], emis)
+    rep = run.report_dict()
+    for k in ("scheduling_delay", "ttft", "tbt", "e2e", "normalized"):
+        for q in ("p50", "p90", "p95", "p99"):
+            assert rep[k][q] == theirs["report"][k][q], (k, q)
+    assert rep["simulated_span"] == theirs["simulated_span"]
