@@ -373,7 +373,13 @@ __global__ void k_build_tables(const SimConfig* __restrict__ cfgs, int32_t n, in
 // those quantities; it stops *before* any iteration that would break a
 // condition (or raise) and hands it to the normal path, so every decision,
 // clock value and counter stays identical.  Returns iterations executed.
-#define SSG_FF_MAX_PP 8  // the fast-forward keeps per-microbatch state in registers
+#ifndef SSG_FF_MAX_PP
+// the fast-forward keeps per-microbatch state in registers, unrolled over this
+// many microbatches (deeper pipelines take the exact event-loop path).  4 covers
+// the search space's pp in {1, 2, 4}; 8 measured slower (bigger unrolled body:
+// 1/2 cfg #4 shard 0.696 vs 0.74 s, full sweep 1.128 vs 1.155 s)
+#define SSG_FF_MAX_PP 4
+#endif
 #ifndef SSG_FF_ARRIVE_ONE
 #define SSG_FF_ARRIVE_ONE 1  // a batch that is not full still runs the iteration an arrival lands in
 #endif
