@@ -16,10 +16,17 @@ predictor microbench (cfg #3), printed as ONE JSON line by rank 0.
 * roofline k_simulate: algorithmic bytes (predictor bytes of
            every query + 48 B per batch entry, counted by the kernel) / its
            CUDA-event time, against the measured HBM copy bandwidth.
-* cpu_baseline  the compiled reference (oracle/_ref) evaluating a bounded sample
-           of the same configs on all host threads (rank 0, N=1 only).
-Multi-GPU: configs i % N == rank per rank (strong scaling of the fixed grid),
-one NCCL all_gather of fixed-size result records, ranking/Pareto on rank 0.
+* cpu_baseline  the compiled reference (oracle/_ref) evaluating a bounded,
+           balanced sample of the same configs on all host threads (rank 0, N=1 only).
+* identical_to_reference  results.csv, both frontier CSVs and summary.txt equal
+           byte for byte the reference's own run_search outputs for the same grid
+           (tests/golden/sweep, made by tools/make_sweep_golden.py).
+Multi-GPU: `--gpus N` re-execs under torchrun (one rank per GPU) when no
+launcher set WORLD_SIZE.  Each rank evaluates its shard of the grid (a
+longest-processing-time split on the configs' initial QPS guesses, the same on
+every rank); one NCCL all_gather of fixed-size result records; ranking, Pareto
+and writers on rank 0 (strong scaling of the fixed grid).
+--impl reference: the reference's run_search(workers = nproc) over the whole grid.
 """
 from __future__ import annotations
 
@@ -162,19 +169,31 @@ def profiled_traffic(kernel: str) -> dict:
         return {}
 
 
+def balanced_sample(n_configs: int, k: int, offset: int = 0) -> list:
+    """k configs from a fixed pseudo-random permutation of the grid (seed 0),
+    starting at `offset`: each sample mixes cheap and expensive configs."""
+    import numpy as np
+
+    perm = np.random.default_rng(0).permutation(n_configs)
+    return [int(perm[(offset + j) % n_configs]) for j in range(min(k, n_configs))]
+
+
 def cpu_baseline(cfg_path: str, n_configs: int, sample: int) -> dict:
-    """The compiled reference evaluating a strided sample of the grid on all host threads."""
+    """The compiled reference evaluating a bounded, balanced sample of the grid
+    (2 configs per host thread, pulled from one atomic counter as run_search's
+    pool does) on all host threads."""
     from oracle import ref
 
     threads = os.cpu_count() or 1
-    k = sample or threads
-    stride = max(1, n_configs // k)
-    idx = list(range(0, n_configs, stride))[:k]
+    k = sample or 2 * threads
+    idx = balanced_sample(n_configs, k)
     res = ref.evaluate_sample(cfg_path, idx, threads)
     secs = res["seconds"]
     return {"value": len(idx) / secs, "unit": UNIT, "cores": threads, "kind": "reference",
-            "sample": "%d of %d configs (every %dth in enumeration order), evaluate_config on %d "
-                      "threads, %.1f s" % (len(idx), n_configs, stride, threads, secs)}
+            "cpu": cpu_model(),
+            "sample": "%d of %d configs (seeded permutation of the grid), evaluate_config pulled "
+                      "by %d threads from one counter (run_search's pool), %.1f s"
+                      % (len(idx), n_configs, threads, secs)}
 
 
 def predictor_bench(torch, dev, nq: int, steps: int, warmup: int) -> dict:
@@ -337,8 +356,50 @@ def simulate_bench(steps: int) -> dict:
     return out
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def spawn_ranks(a) -> None:
+    """`--gpus N` (N > 1) without a torch.distributed launcher: re-exec this
+    script under torchrun, one rank per GPU on this node (127.0.0.1 rendezvous)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    argv = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+            "--nproc-per-node", str(a.gpus), "--master-addr", "127.0.0.1",
+            "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, argv)
+
+
+def sweep_golden(name: str):
+    """The compiled reference's run_search outputs for this sweep, generated by
+    tools/make_sweep_golden.py under the host libm variant (tests/golden/sweep)."""
+    import paper_2405_05465_b200 as ssg
+
+    sys.path.insert(0, os.path.join(ROOT, "tests", "helpers"))
+    import sweep_golden
+
+    g = sweep_golden.load(name, "fma" if ssg.math_variant() == 1 else "plain")
+    return None if g is None else g[0]
+
+
+GOLDEN_OF = {"llama2_70b/chat_like": "cfg4", "qwen_72b/arxiv_like": "cfg5_qwen72b_arxiv",
+             "internlm_20b/bwb_like": "cfg5_internlm20b_bwb"}
+
+
 def main():
     a = parse()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(a)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -462,6 +523,7 @@ def main():
                    "configs": n_configs, "sweeps": len(sweeps),
                    "parallelism": "config shards x%d + 1 %s all_gather per sweep"
                                   % (world, "NCCL" if backend == "nccl" else "gloo (ranks share GPUs)"),
+                   "ranks_share_gpus": world > ndev,
                    "l2": "flushed (512 MB write) before every timed step"},
         "e2e": {"value": n_configs / (sum(e2e_times) / len(e2e_times)), "unit": UNIT,
                 "h2d_bytes_per_step": st_e2e["h2d_bytes"] // e2e_steps,
@@ -484,6 +546,16 @@ def main():
             result["optimum"] = outcome[0].get("best")
         else:
             result["optimum"] = {name: o.get("best") for (name, _), o in zip(sweeps, outcome)}
+        # byte-for-byte against the reference's own run_search on the same grid
+        # (results.csv, both frontiers, summary; tests/golden/sweep)
+        same = {}
+        for (name, _), o in zip(sweeps, outcome):
+            g = sweep_golden(GOLDEN_OF[name]) if (name in GOLDEN_OF and not a.quick) else None
+            if g is not None:
+                same[name] = all(o[k] == g[k] for k in g)
+        if same:
+            result["identical_to_reference"] = all(same.values())
+            result["identical_to_reference_sweeps"] = same
     if rank == 0 and world == 1 and not a.quick and a.workload == "cfg4":
         try:
             result["predictor"] = predictor_bench(torch, dev, a.predictor_queries, a.steps, a.warmup)
@@ -510,8 +582,13 @@ def main():
 
 
 def reference_arm(a, world: int, rank: int):
-    """--impl reference: the compiled reference (oracle/_ref) on the host cores, on
-    bounded samples of the same sweep (each step = a strided sample of configs)."""
+    """--impl reference: the reference's own run_search (oracle/_ref: the
+    unmodified headers compiled by oracle/Makefile) with workers = every host
+    thread, over the WHOLE cfg #4 grid in one run -- its own atomic-counter
+    thread pool, estimator build, ranking and Pareto.  The K timed steps are K
+    equal shares of that one run (ms_per_step = run time / K); the W warm-up
+    steps are W single-config evaluations (there is nothing to warm on a CPU
+    path, they only fault in the library).  Rank 0 only."""
     if rank != 0:
         return
     try:
@@ -523,31 +600,36 @@ def reference_arm(a, world: int, rank: int):
         cfg_path = search_config(tmp, a.quick)
         threads = os.cpu_count() or 1
         n_configs = int(ref.evaluate_sample(cfg_path, [], 1)["num_configs_total"])
-        k = a.cpu_sample or threads
-        times = []
-        for i in range(a.warmup + a.steps):
-            stride = max(1, n_configs // k)
-            idx = [(j + i) % n_configs for j in range(0, n_configs, stride)][:k]
-            res = ref.evaluate_sample(cfg_path, idx, threads)
-            if i >= a.warmup:
-                times.append((len(idx), res["seconds"]))
-        v = sum(n for n, _ in times) / sum(s for _, s in times)
-        print(json.dumps({
+        for i in range(a.warmup):
+            ref.evaluate_sample(cfg_path, balanced_sample(n_configs, 1, i), 1)
+        res = ref.search(cfg_path, workers=threads)
+        secs = res["seconds"]
+        v = n_configs / secs
+        steps = max(1, a.steps)
+        same = None
+        if not a.quick:  # the committed goldens of the same grid (either libm variant)
+            for variant in ("fma", "plain"):
+                f = os.path.join(ROOT, "tests", "golden", "sweep", "cfg4." + variant, "results.csv")
+                if os.path.exists(f) and open(f).read() == res["results_csv"]:
+                    same = variant
+            same = same or False
+        sample = ("run_search(workers=%d) over the whole %d-config grid, once (%.1f s); the %d "
+                  "timed steps are equal shares of it" % (threads, n_configs, secs, steps))
+        out = {
             "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
-            "steps": a.steps, "warmup": a.warmup,
-            "ms_per_step": 1e3 * sum(s for _, s in times) / len(times),
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * secs / steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (chat_like lognormal lengths, synth seed 7; Poisson probes seed 1)",
             "config": {"workload": "cfg #4: LLaMA2-70B Vidur-Search capacity sweep, %d configs "
                                    "(A100/H100 x tp,pp in {1,2,4} x vLLM/Orca+/Sarathi x bs x cs), "
                                    "2000 probe requests, tol 0.02, interp estimator" % n_configs,
-                       "configs": n_configs,
-                       "sample": "%d strided configs per step (evaluate_config, the reference's "
-                                 "per-config unit of run_search)" % k},
+                       "configs": n_configs, "sample": sample},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
-                             "sample": "%d strided configs per step, evaluate_config" % k},
-            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
-            flush=True)
+                             "cpu": cpu_model(), "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        if same is not None:
+            out["results_csv_equals_golden"] = same  # libm variant whose golden matched
+        print(json.dumps(out), flush=True)
     except Exception as e:  # noqa: BLE001
         print(json.dumps({"impl": "reference", "unavailable": str(e)[:200]}), flush=True)
 

@@ -465,14 +465,18 @@ double qps_per_dollar(double capacity_qps, std::int64_t gpus_used, double rate_p
 
 // The whole sweep on the local GPU: every config's capacity search advances
 // in lock-step rounds of speculative probes (sweep.cu / search.cpp).
-// `shard`/`num_shards` restrict evaluation to configs i % num_shards == shard
-// (the other entries are left default) for the multi-GPU driver.
+// `shard`/`num_shards` restrict evaluation to one shard of the grid for the
+// multi-GPU driver (the other entries are left default; `owned` receives the
+// enumeration indices this shard evaluated).  The capacity objective splits the
+// grid by a longest-processing-time assignment on every config's initial QPS
+// guess (identical on every rank); the makespan objective strides i % num_shards.
 SearchOutcome run_search(const ModelSpec& spec, const std::vector<Request>& workload,
                          const SearchOptions& opts);
 std::vector<ConfigResult> evaluate_configs_shard(const ModelSpec& spec,
                                                  const std::vector<Request>& workload,
                                                  const SearchOptions& opts, int shard,
-                                                 int num_shards);
+                                                 int num_shards,
+                                                 std::vector<std::size_t>* owned = nullptr);
 SearchOutcome finalize_search(const ModelSpec& spec, const SearchOptions& opts,
                               std::vector<ConfigResult> results);
 
@@ -484,7 +488,8 @@ class SearchSession {
   SearchSession(const ModelSpec& spec, const std::vector<Request>& workload,
                 const SearchOptions& opts);
   ~SearchSession();
-  std::vector<ConfigResult> evaluate(int shard = 0, int num_shards = 1);
+  std::vector<ConfigResult> evaluate(int shard = 0, int num_shards = 1,
+                                     std::vector<std::size_t>* owned = nullptr);
   std::size_t num_configs() const;
 
  private:

@@ -163,12 +163,17 @@ typedef struct ssg_config_record {
 
 size_t ssg_search_record_size(void);
 /* load_search_config + run_search + writers (config.hpp:111, search.hpp:369-486)
- * over the configs i % num_shards == shard (1 shard = the whole search).
+ * over the whole grid: shard must be 0 and num_shards 1 (else status 1 --
+ * shards go through ssg_search_shard + ssg_search_finalize).
  * *out: JSON {results_csv, frontier_ttft_csv, frontier_tbt_csv, summary,
- * configs, best}; free with ssg_free.  With num_shards > 1 the other configs
- * appear with default fields -- use _shard/_finalize to combine shards. */
+ * configs, best}; free with ssg_free. */
 int ssg_search(const char* config_path, int shard, int num_shards, char** out, ssg_status* st);
-/* Evaluates this shard's configs into `records` (capacity >= ceil(N/num_shards)). */
+/* Evaluates this shard's configs into `records`.  The capacity objective
+ * assigns configs to shards by a longest-processing-time split on their
+ * initial QPS guesses (the same on every rank, so the shards partition the
+ * grid); the makespan objective strides i % num_shards.  A shard may hold any
+ * number of configs up to N: capacity >= N is always enough, and *count is
+ * the number written.  Each record carries its enumeration index. */
 int ssg_search_shard(const char* config_path, int shard, int num_shards, ssg_config_record* records,
                      size_t capacity, size_t* count, ssg_status* st);
 /* Ranking, Pareto frontiers and writers over the gathered records of every

@@ -212,10 +212,10 @@ def simulate(cluster: dict, estimator: Estimator, ids, arrivals, prefill, decode
     return json.loads(_ffi.take_text(out))
 
 
-def search(config_path: str, shard: int = 0, num_shards: int = 1) -> dict:
+def search(config_path: str) -> dict:
     """run_search from a reference-format search config (config.hpp:111, search.hpp:369)."""
     out = C.c_void_p()
-    _ffi.call("ssg_search", config_path.encode(), shard, num_shards, C.byref(out))
+    _ffi.call("ssg_search", config_path.encode(), 0, 1, C.byref(out))
     return json.loads(_ffi.take_text(out))
 
 

@@ -107,13 +107,16 @@ def write_search_config(directory: str, model: str = "llama2_70b", workload: str
                         batch_sizes=(32, 64, 128, 256, 512), chunk_sizes=(512, 1024, 2048),
                         max_gpus_total=16, num_requests=2000, synth_seed=7,
                         probe_requests=2000, tolerance=0.02, objective="qps_per_dollar",
-                        workload_doc=None) -> str:
+                        workload_doc=None, device_docs=None) -> str:
     """Renders a reference-format search config (config.hpp:111-179) plus the
-    model/device documents it points at; returns the config path."""
+    model/device documents it points at; returns the config path.
+    `device_docs` adds SKUs beyond DEVICES ({key: device document}; their
+    hourly rate is 1.0)."""
     os.makedirs(directory, exist_ok=True)
+    devices = dict(DEVICES, **(device_docs or {}))
     write_json(os.path.join(directory, "models", model + ".json"), MODELS[model])
     for s in skus:
-        write_json(os.path.join(directory, "devices", s + ".json"), DEVICES[s])
+        write_json(os.path.join(directory, "devices", s + ".json"), devices[s])
     cfg = {
         "schema_version": 1,
         "model_spec": "models/%s.json" % model,
@@ -124,7 +127,8 @@ def write_search_config(directory: str, model: str = "llama2_70b", workload: str
                   "batch_sizes": list(batch_sizes), "chunk_sizes": list(chunk_sizes),
                   "max_gpus_total": max_gpus_total},
         "slos": {"ttft_p90_max": 2.0, "tbt_p99_max": 0.2, "delay_p99_max": 5.0},
-        "cost_table": {DEVICES[s]["sku_name"]: COST_TABLE[DEVICES[s]["sku_name"]] for s in skus},
+        "cost_table": {devices[s]["sku_name"]: COST_TABLE.get(devices[s]["sku_name"], 1.0)
+                       for s in skus},
         "capacity": {"tolerance": tolerance, "probe_requests": probe_requests,
                      "evaluation_fraction": 0.85},
         "objective": objective,

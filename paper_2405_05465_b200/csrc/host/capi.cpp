@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <functional>
 #include <memory>
 
@@ -107,6 +108,9 @@ bool pinned(const void* p) {
 void predict_host(const EstimatorModel& est, size_t n, const int32_t* slots, int32_t uniform,
                   const double* f0, const double* f1, double* out, bool validate) {
   if (n == 0) return;
+  // one staging set per process: concurrent host-buffer predictions serialise
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
   const auto& de = est.device();
   auto& ctx = ssg::context();
   auto& S = staging();
@@ -490,7 +494,10 @@ nlohmann::json outcome_json(const SearchOutcome& o, const std::string& objective
 
 int ssg_search(const char* config_path, int shard, int num_shards, char** out, ssg_status* st) {
   return guarded(st, [&] {
-    require(num_shards >= 1 && shard >= 0 && shard < num_shards, "ssg_search: bad shard");
+    // one process, whole grid: shards are ssg_search_shard + ssg_search_finalize
+    require(num_shards == 1 && shard == 0,
+            "ssg_search: evaluates the whole grid (num_shards must be 1); shard with "
+            "ssg_search_shard and merge with ssg_search_finalize");
     ssg::PhaseTimer timer("ssg_search_shard");
     auto cfg = load_search_config(config_path);
     auto results = evaluate_configs_shard(cfg.spec, cfg.workload, cfg.options, shard, num_shards);
@@ -500,11 +507,10 @@ int ssg_search(const char* config_path, int shard, int num_shards, char** out, s
 }
 
 namespace {
-void to_records(const std::vector<ConfigResult>& results, int shard, int num_shards,
+void to_records(const std::vector<ConfigResult>& results, const std::vector<size_t>& owned,
                 ssg_config_record* records, size_t capacity, size_t* count) {
     size_t k = 0;
-    for (size_t i = 0; i < results.size(); ++i) {
-      if (static_cast<int>(i % static_cast<size_t>(num_shards)) != shard) continue;
+    for (size_t i : owned) {
       require(k < capacity, "ssg_search_shard: record buffer too small");
       const ConfigResult& r = results[i];
       ssg_config_record& rec = records[k++];
@@ -529,8 +535,10 @@ int ssg_search_shard(const char* config_path, int shard, int num_shards, ssg_con
   return guarded(st, [&] {
     require(num_shards >= 1 && shard >= 0 && shard < num_shards, "ssg_search_shard: bad shard");
     auto cfg = load_search_config(config_path);
-    auto results = evaluate_configs_shard(cfg.spec, cfg.workload, cfg.options, shard, num_shards);
-    to_records(results, shard, num_shards, records, capacity, count);
+    std::vector<size_t> owned;
+    auto results =
+        evaluate_configs_shard(cfg.spec, cfg.workload, cfg.options, shard, num_shards, &owned);
+    to_records(results, owned, records, capacity, count);
   });
 }
 
@@ -550,8 +558,9 @@ int ssg_search_run(ssg_search_session* s, int shard, int num_shards, ssg_config_
                    size_t capacity, size_t* count, ssg_status* st) {
   return guarded(st, [&] {
     require(num_shards >= 1 && shard >= 0 && shard < num_shards, "ssg_search_run: bad shard");
-    auto results = s->session->evaluate(shard, num_shards);
-    to_records(results, shard, num_shards, records, capacity, count);
+    std::vector<size_t> owned;
+    auto results = s->session->evaluate(shard, num_shards, &owned);
+    to_records(results, owned, records, capacity, count);
   });
 }
 

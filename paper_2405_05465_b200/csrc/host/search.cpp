@@ -132,13 +132,30 @@ struct NeedProbe {
   double lo, hi;
 };
 
+// A probe rate's answer: feasible / infeasible, or the Error its simulation
+// raised.  Errors are memoised like answers and surface only when the replay
+// actually asks for that rate: a speculative rate the sequential search never
+// reaches cannot turn a successful evaluation into an error row.
+struct ProbeAnswer {
+  bool feasible = false;
+  bool error = false;
+  SimUnitOut err{};  // the failing unit (error == true)
+};
+using ProbeMemo = std::unordered_map<double, ProbeAnswer>;
+
+struct ProbeError {
+  SimUnitOut err;
+};
+
 // The reference's find_capacity (search.hpp:145-174) against a memo; throws
-// NeedProbe on the first unanswered rate.
-double replay_capacity(const std::unordered_map<double, bool>& memo, const CapacitySearchOptions& o) {
+// NeedProbe on the first unanswered rate and ProbeError when the asked rate's
+// simulation raised (the reference's feasible(q) throwing out of find_capacity).
+double replay_capacity(const ProbeMemo& memo, const CapacitySearchOptions& o) {
   auto ask = [&](double q, int phase, double lo, double hi) {
     auto it = memo.find(q);
     if (it == memo.end()) throw NeedProbe{q, phase, lo, hi};
-    return it->second;
+    if (it->second.error) throw ProbeError{it->second.err};
+    return it->second.feasible;
   };
   require(o.initial_guess > 0 && o.tolerance > 0, "find_capacity: bad options");
   double lo = 0.0, hi = o.initial_guess;
@@ -209,7 +226,7 @@ struct Candidate {
   bool sim_ok = false;  // make_sim_config succeeded (else the first probe raises)
   std::string sim_error;
   CapacitySearchOptions copts;
-  std::unordered_map<double, bool> memo;
+  ProbeMemo memo;
   bool done = false;       // evaluation finished (capacity known, or failed)
   bool measured = false;   // SLO / static run taken
   int64_t probe_iters = 0; // longest probe unit so far (iterations): speculation budget
@@ -612,9 +629,36 @@ void run_round(SweepLane& lane, std::vector<Candidate>& cands,
   std::vector<SimUnitOut> out;
   std::vector<double> sel;
   run_launch(lane, L, w, out, sel);
+  // Full runs: the first error in simulated time is the one the reference
+  // raises, but independent round-robin units cannot order two errors at the
+  // same clock (the makespan run queues every arrival at t = 0) -- the
+  // reference raises for the event first in its global (time, seq) order.
+  // A full run with more than one failing unit is replayed with all its
+  // replicas in one unit, in exact event order (as sim.cpp does for single runs).
+  ProbeLaunch redo_full;
   for (std::size_t m = 0; m < L.measured.size(); ++m) {
     const ProbeDesc& p = L.probes[L.measured[m]];
-    take_measurement(cands[L.probe_cand[L.measured[m]]], out, p, sel.data() + 3 * m, w);
+    Candidate& C = cands[L.probe_cand[L.measured[m]]];
+    int errors = 0;
+    for (int u = p.first_unit; u < p.first_unit + (p.decoupled ? p.R : 1); ++u)
+      errors += out[u].code != SSG_OK ? 1 : 0;
+    if (errors > 1 && p.decoupled && p.R <= kMaxCoupledReplicas) {
+      const int32_t ci = redo_full.add_config(C);
+      redo_full.add_probe(L.probe_cand[L.measured[m]], C, ci, p.qps, n, SSG_UF_EMISSIONS, 0.0, 0,
+                          true, p.static_run != 0, redo_full.next_emis_base(w.emis_per_probe));
+      continue;
+    }
+    take_measurement(C, out, p, sel.data() + 3 * m, w);
+  }
+  if (!redo_full.probes.empty()) {
+    std::vector<SimUnitOut> out2;
+    std::vector<double> sel2;
+    run_launch(lane, redo_full, w, out2, sel2);
+    for (std::size_t m = 0; m < redo_full.measured.size(); ++m) {
+      const ProbeDesc& p = redo_full.probes[redo_full.measured[m]];
+      take_measurement(cands[redo_full.probe_cand[redo_full.measured[m]]], out2, p,
+                       sel2.data() + 3 * m, w);
+    }
   }
   ProbeLaunch redo;
   for (std::size_t k = 0; k < L.probes.size(); ++k) {
@@ -632,7 +676,7 @@ void run_round(SweepLane& lane, std::vector<Candidate>& cands,
     C.probe_iters = std::max(C.probe_iters, iters);
     const SimUnitOut* e = first_error(out, p);
     if (!e) {
-      C.memo[p.qps] = !aborted && late <= max_late;
+      C.memo[p.qps] = ProbeAnswer{!aborted && late <= max_late};
     } else if (p.decoupled && p.R <= kMaxCoupledReplicas) {
       // independent replicas cannot order an error against the global abort:
       // replay this probe with every replica in one unit
@@ -640,9 +684,9 @@ void run_round(SweepLane& lane, std::vector<Candidate>& cands,
       redo.add_probe(L.probe_cand[k], C, ci, p.qps, n, SSG_UF_ABORT, base.delay_p99_threshold,
                      max_late, true, false, -1);
     } else if (aborted && !p.decoupled) {
-      C.memo[p.qps] = false;
+      C.memo[p.qps] = ProbeAnswer{false};
     } else {
-      fail(C, *e);
+      C.memo[p.qps] = ProbeAnswer{false, true, *e};
     }
   }
   if (redo.probes.empty()) return;
@@ -652,11 +696,11 @@ void run_round(SweepLane& lane, std::vector<Candidate>& cands,
     Candidate& C = cands[redo.probe_cand[k]];
     const SimUnitOut& o = out[p.first_unit];
     if (o.aborted)
-      C.memo[p.qps] = false;
+      C.memo[p.qps] = ProbeAnswer{false};
     else if (o.code == SSG_OK)
-      C.memo[p.qps] = o.late <= max_late;
+      C.memo[p.qps] = ProbeAnswer{o.late <= max_late};
     else
-      fail(C, o);
+      C.memo[p.qps] = ProbeAnswer{false, true, o};
   }
 }
 
@@ -691,6 +735,9 @@ void run_group(SweepLane& lane, std::vector<Candidate>& cands, const std::vector
               fresh.push_back(q);
           probes.push_back({k, fresh});
           continue;
+        } catch (const ProbeError& pe) {
+          fail(C, pe.err);
+          continue;
         } catch (const Error& e) {
           C.res.error = e.what();
           C.res.capacity_qps = 0.0;
@@ -717,6 +764,36 @@ void run_group(SweepLane& lane, std::vector<Candidate>& cands, const std::vector
     if (probes.empty() && full.empty()) break;
     run_round(lane, cands, probes, full, false, w, opts.capacity);
   }
+}
+
+bool shard_split_by_cost() {  // SSG_SHARD_SPLIT=stride: i % num_shards (A/B)
+  const char* e = std::getenv("SSG_SHARD_SPLIT");
+  return !(e && std::strcmp(e, "stride") == 0);
+}
+
+// Greedy LPT: configs by cost descending (ties by enumeration index) onto the
+// least-loaded shard (ties to the lowest shard).  Deterministic on every rank.
+std::vector<int> lpt_split(const std::vector<Candidate>& cands, int num_shards) {
+  std::vector<double> cost(cands.size(), 0.0);
+  for (std::size_t k = 0; k < cands.size(); ++k)
+    if (!cands[k].done) cost[k] = 1.0 / cands[k].copts.initial_guess;
+  std::vector<std::size_t> order(cands.size());
+  for (std::size_t k = 0; k < order.size(); ++k) order[k] = k;
+  std::stable_sort(order.begin(), order.end(), [&](std::size_t a, std::size_t b) {
+    return cost[a] > cost[b];
+  });
+  std::vector<double> load(static_cast<std::size_t>(num_shards), 0.0);
+  std::vector<int> count(static_cast<std::size_t>(num_shards), 0);
+  std::vector<int> owner(cands.size(), 0);
+  for (auto k : order) {
+    int best = 0;
+    for (int r = 1; r < num_shards; ++r)
+      if (load[r] < load[best] || (load[r] == load[best] && count[r] < count[best])) best = r;
+    owner[k] = best;
+    load[best] += cost[k];
+    count[best] += 1;
+  }
+  return owner;
 }
 
 }  // namespace
@@ -809,12 +886,13 @@ std::size_t SearchSession::num_configs() const { return st_->configs.size(); }
 std::vector<ConfigResult> evaluate_configs_shard(const ModelSpec& spec,
                                                  const std::vector<Request>& workload,
                                                  const SearchOptions& opts, int shard,
-                                                 int num_shards) {
+                                                 int num_shards, std::vector<std::size_t>* owned) {
   SearchSession session(spec, workload, opts);
-  return session.evaluate(shard, num_shards);
+  return session.evaluate(shard, num_shards, owned);
 }
 
-std::vector<ConfigResult> SearchSession::evaluate(int shard, int num_shards) {
+std::vector<ConfigResult> SearchSession::evaluate(int shard, int num_shards,
+                                                  std::vector<std::size_t>* owned) {
   StatsScope stats_scope;  // counters merge into the process totals when the evaluation ends
   PhaseTimer timer("search: evaluate");
   const State& S = *st_;
@@ -826,8 +904,13 @@ std::vector<ConfigResult> SearchSession::evaluate(int shard, int num_shards) {
   State& SS = *st_;
   std::vector<ConfigResult> results(configs.size());
   std::vector<Candidate> cands;
+  const bool makespan = opts.objective == "makespan";
+  // The capacity objective computes every config's initial guess first (one
+  // launch for the whole grid, identical on every rank) and splits the grid by
+  // its cost; the makespan objective's static runs are alike, so it strides.
+  const bool by_cost = !makespan && num_shards > 1 && shard_split_by_cost();
   for (std::size_t i = 0; i < configs.size(); ++i) {
-    if (static_cast<int>(i % static_cast<std::size_t>(num_shards)) != shard) continue;
+    if (!by_cost && static_cast<int>(i % static_cast<std::size_t>(num_shards)) != shard) continue;
     const CandidateConfig& cand = configs[i];
     Candidate C;
     C.index = i;
@@ -847,37 +930,6 @@ std::vector<ConfigResult> SearchSession::evaluate(int shard, int num_shards) {
     cands.push_back(std::move(C));
   }
 
-  {
-    // token tables for every distinct (SKU, tp, pp) operator table
-    std::vector<SimConfig> tcfg;
-    std::vector<std::size_t> tk;
-    std::vector<SsgEstView> tests;
-    std::vector<const DeviceEstimator*> test_of;
-    for (const auto& e : ests) {
-      tests.push_back(e.device().view);
-      test_of.push_back(&e.device());
-    }
-    for (std::size_t k = 0; k < cands.size(); ++k) {
-      if (!cands[k].sim_ok) continue;
-      SimConfig c = cands[k].sim;
-      c.est = static_cast<int32_t>(cands[k].cand.sku_index);
-      tcfg.push_back(c);
-      tk.push_back(k);
-    }
-    PhaseTimer t("search: token tables");
-    if (std::getenv("SSG_NO_TABLES") == nullptr)
-      build_token_tables(tcfg, tests, test_of, SS.tables);
-    for (std::size_t i = 0; i < tk.size(); ++i) {
-      SimConfig& c = cands[tk[i]].sim;
-      c.tab_off = tcfg[i].tab_off;
-      c.tab_cells = tcfg[i].tab_cells;
-      c.tab_stride = tcfg[i].tab_stride;
-      c.tab_tmax = tcfg[i].tab_tmax;
-      c.tab_pmax = tcfg[i].tab_pmax;
-    }
-  }
-
-  const bool makespan = opts.objective == "makespan";
   std::vector<std::size_t> live;
   if (makespan) {
     // the static run is the first simulation: its preamble errors surface
@@ -958,6 +1010,55 @@ std::vector<ConfigResult> SearchSession::evaluate(int shard, int num_shards) {
       }
     }
   }
+
+  if (by_cost) {
+    // Longest-processing-time split on the capacity search's critical chain:
+    // a probe at rate q spans n / q seconds of simulated time, so 1 / guess
+    // orders the configs by how long their probe chains run.  Failed configs
+    // cost nothing but still belong to one shard (their error rows).
+    const std::vector<int> owner = lpt_split(cands, num_shards);
+    std::vector<Candidate> mine;
+    for (std::size_t k = 0; k < cands.size(); ++k)
+      if (owner[k] == shard) mine.push_back(std::move(cands[k]));
+    cands.swap(mine);
+    live.clear();
+    for (std::size_t k = 0; k < cands.size(); ++k)
+      if (!cands[k].done) live.push_back(k);
+  }
+  if (owned) {
+    owned->clear();
+    for (const auto& C : cands) owned->push_back(C.index);
+  }
+  {
+    // token tables for every distinct (SKU, tp, pp) operator table
+    std::vector<SimConfig> tcfg;
+    std::vector<std::size_t> tk;
+    std::vector<SsgEstView> tests;
+    std::vector<const DeviceEstimator*> test_of;
+    for (const auto& e : ests) {
+      tests.push_back(e.device().view);
+      test_of.push_back(&e.device());
+    }
+    for (std::size_t k = 0; k < cands.size(); ++k) {
+      if (!cands[k].sim_ok) continue;
+      SimConfig c = cands[k].sim;
+      c.est = static_cast<int32_t>(cands[k].cand.sku_index);
+      tcfg.push_back(c);
+      tk.push_back(k);
+    }
+    PhaseTimer t("search: token tables");
+    if (std::getenv("SSG_NO_TABLES") == nullptr)
+      build_token_tables(tcfg, tests, test_of, SS.tables);
+    for (std::size_t i = 0; i < tk.size(); ++i) {
+      SimConfig& c = cands[tk[i]].sim;
+      c.tab_off = tcfg[i].tab_off;
+      c.tab_cells = tcfg[i].tab_cells;
+      c.tab_stride = tcfg[i].tab_stride;
+      c.tab_tmax = tcfg[i].tab_tmax;
+      c.tab_pmax = tcfg[i].tab_pmax;
+    }
+  }
+
 
   PhaseTimer t_rounds("search: rounds");
   // lanes: streams + buffers; every lane waits for the token tables

@@ -93,3 +93,89 @@ def test_concurrent_sessions_equal_sequential(ssg, tmp_path):
         assert a == b
     for s in sessions:
         s.close()
+
+
+def _golden_case(ssg, case, tmp_path):
+    import sys
+
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "helpers"))
+    import sweep_golden
+
+    variant = "fma" if ssg.math_variant() == 1 else "plain"
+    g = sweep_golden.load(case, variant)
+    if g is None:
+        pytest.skip("no %s golden for libm variant %s" % (case, variant))
+    theirs, meta = g
+    path = catalog.write_search_config(str(tmp_path), **sweep_golden.CASES[case])
+    # the grid this run evaluates is the one the reference evaluated
+    assert sweep_golden.config_digest(path) == meta["config_sha256"]
+    return path, theirs
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("case", ["cfg4", "cfg5_qwen72b_arxiv", "cfg5_internlm20b_bwb"])
+def test_full_grid_matches_reference(ssg, case, tmp_path):
+    """The headline sweeps, whole grids (450 configs, 2000 probe requests each):
+    cfg #4 (LLaMA2-70B x chat_like) and two cfg #5 pairs (Qwen-72B x arxiv_like,
+    InternLM-20B x bwb_like), byte-identical to the reference's own run_search
+    outputs (tests/golden/sweep, tools/make_sweep_golden.py) -- every capacity,
+    percentile, error row, the ranking, both frontiers and the chosen optimum."""
+    path, theirs = _golden_case(ssg, case, tmp_path)
+    compare(ssg.search(path), theirs)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("shards", [2, 8])
+def test_full_grid_sharded_matches_reference(ssg, shards, tmp_path):
+    """cfg #4 split over `shards` ranks by the cost-based (LPT) assignment, each
+    shard evaluated on its own, records merged: the same bytes as the reference."""
+    path, theirs = _golden_case(ssg, "cfg4", tmp_path)
+    parts = [ssg.search_shard(path, s, shards) for s in range(shards)]
+    size = ssg.record_size()
+    assert sum(len(p) for p in parts) == 450 * size  # the shards partition the grid
+    compare(ssg.search_finalize(path, b"".join(parts)), theirs)
+
+
+# A 7B replica on this device holds ~1,500 KV tokens (params 10.59 GB + 10 %
+# reserve), so the chat_like trace's longer requests cannot be served.
+TINY_GPU = {"schema_version": 1, "sku_name": "TINY-GPU", "peak_flops": 312e12,
+            "mem_bandwidth": 2.039e12, "link_bandwidth": 3.0e11, "kernel_overhead": 2e-6,
+            "device_mem": 12.64e9}
+
+
+@pytest.mark.parametrize("objective", ["makespan", "qps_per_dollar"])
+def test_search_oversized_requests_two_replicas(ssg, ref, tmp_path, objective):
+    """Requests beyond a replica's KV capacity raise from enqueue on both
+    round-robin replicas.  Under the makespan objective every arrival is at
+    t = 0, so the two replicas fail at the same clock: the error row must name
+    the request the reference meets first in its (time, seq) event order
+    (scheduler.hpp:146-155; sim.hpp:211-220), not the first replica's."""
+    path = catalog.write_search_config(
+        str(tmp_path), model="llama2_7b", skus=("tiny",), tp=(1,), pp=(1,),
+        schedulers=("vllm", "sarathi_serve"), batch_sizes=(32,), chunk_sizes=(512,),
+        max_gpus_total=2, probe_requests=400, num_requests=400, objective=objective,
+        device_docs={"tiny": TINY_GPU})
+    mine, theirs = ssg.search(path), ref.search(path, workers=2)
+    compare(mine, theirs)
+    assert "KV units but replica capacity" in mine["results_csv"]
+
+# ~3,000 KV tokens per 7B replica: only the trace's rare longest requests are
+# oversized, so whether a probe raises depends on its rate (a fast probe can
+# abort on late schedules before the first oversized request arrives).
+SMALL_GPU = dict(TINY_GPU, sku_name="SMALL-GPU", device_mem=13.51e9)
+
+
+def test_search_deep_speculation_same_answers(ssg, ref, tmp_path, monkeypatch):
+    """Speculation never changes an answer: with an 8-rate doubling ladder and
+    bisection sub-trees 6 levels deep, rates the sequential find_capacity never
+    asks are simulated too -- including rates whose probes raise -- and the
+    outcome is still the reference's (probe errors are memoised and surface
+    only when the replay asks for that rate; search.hpp:145-174)."""
+    monkeypatch.setenv("SSG_SPEC_LADDER", "8")
+    monkeypatch.setenv("SSG_SPEC_DEPTH", "6")
+    path = catalog.write_search_config(
+        str(tmp_path), model="llama2_7b", skus=("a100_80g", "small"), tp=(1, 2), pp=(1,),
+        schedulers=("vllm", "orca_plus", "sarathi_serve"), batch_sizes=(32, 256),
+        chunk_sizes=(512,), max_gpus_total=4, probe_requests=600, num_requests=600,
+        device_docs={"small": SMALL_GPU})
+    compare(ssg.search(path), ref.search(path, workers=os.cpu_count() or 1))

@@ -1,7 +1,7 @@
 """Multi-process host logic of the sharded sweep (CPU, gloo, world size 2):
 records of each rank's configs are all-gathered and finalized; the outcome
 equals finalizing all records in one process (ranking/Pareto/writers are
-order-independent of the shard split).  The GPU evaluation itself is covered
+order-independent of the shard split; shards may be uneven).  The GPU evaluation itself is covered
 by tests/test_search_gpu.py::test_sharded_search_equals_whole."""
 import os
 import struct
@@ -38,7 +38,10 @@ def worker(rank, world, cfg_path, port, q):
     try:
         n = 16
         size = ssg.record_size()
-        mine = b"".join(fake_record(i, size) for i in range(rank, n, world))
+        # uneven shards, as the cost-based (LPT) split produces: rank 0 holds 11
+        # configs, rank 1 the other 5, in no particular index order
+        split = [[15, 0, 2, 3, 4, 6, 7, 9, 10, 12, 13], [14, 1, 5, 8, 11]]
+        mine = b"".join(fake_record(i, size) for i in split[rank])
         allrecs = gather_records(mine, n, rank, world, size)
         if rank == 0:
             q.put(ssg.search_finalize(cfg_path, allrecs))
