@@ -270,12 +270,24 @@ def predictor_bench(torch, dev, nq: int, steps: int, warmup: int) -> dict:
         threads = os.cpu_count() or 1
         ns = min(nq, 2_000_000)
         opi = np.array([ssg.OP_INDEX[o] for o in ops], dtype=np.int32)[which[:ns]]
-        _, secs = r.predict_timed(opi, np.full(ns, 4), f0[:ns], f1[:ns], threads)
+        theirs, secs = r.predict_timed(opi, np.full(ns, 4), f0[:ns], f1[:ns], threads)
         base = {"value": ns / secs, "unit": "queries/s", "cores": threads, "kind": "reference",
+                "cpu": cpu_model(),
                 "sample": "%d queries, EstimatorModel::predict on %d threads" % (ns, threads)}
+        # the device-resident run's answers for the same queries, bit for bit
+        mine = d_out[:ns].cpu().numpy()
+        identical = bool(np.array_equal(mine.view(np.uint64), theirs.view(np.uint64)))
+        # and the e2e (host-buffer) call's answers for all nq queries equal the device run's
+        identical_e2e = bool(np.array_equal(out.numpy().view(np.uint64),
+                                            d_out.cpu().numpy().view(np.uint64)))
     except Exception as e:  # noqa: BLE001
         base = {"unavailable": str(e)}
-    return {"workload": "cfg #3: %d forest queries, LLaMA2-70B H100 tp4, attn_prefill/attn_decode/"
+        identical = identical_e2e = None
+    return {"identical_to_reference": identical,
+            "identical_to_reference_sample": "first %d of the %d queries vs EstimatorModel::predict"
+                                             % (min(nq, 2_000_000), nq),
+            "e2e_identical_to_device": identical_e2e,
+            "workload": "cfg #3: %d forest queries, LLaMA2-70B H100 tp4, attn_prefill/attn_decode/"
                         "mlp_up_proj mix" % nq,
             "value": nq / t, "unit": "queries/s", "ms_per_step": t * 1e3,
             "e2e": {"value": nq / min(e2e), "unit": "queries/s",

@@ -43,6 +43,15 @@ int ssg_init(int device, ssg_status* st);
 int ssg_shutdown(void);
 /* 1 if the host libm is the FMA-contracted glibc variant, 0 if plain, -1 before init. */
 int ssg_math_variant(void);
+/* Self-check of the device libm restatement (glibc_math.h) against this
+ * host's glibc: evaluates fn (0 = log1p, 1 = exp) on the GPU, with the libm
+ * variant ssg_init selected, at every x_k = base + k * step, k in [0, n), and
+ * counts the results whose bits differ from the host's std::log1p / std::exp.
+ * The predictor's log1p inputs are integer multiples of one quantum per
+ * feature (estimator.hpp:300-341), so a progression with base 0 covers a
+ * feature's whole domain.  reference: estimator.hpp:120-122 (log1p, exp). */
+int ssg_math_check(int fn, double base, double step, int64_t n, int64_t* mismatches,
+                   double* first_bad_x, ssg_status* st);
 /* Library build identifier (sm arch, git-independent). */
 const char* ssg_version(void);
 /* Frees any buffer this library returned (JSON/CSV text). */

@@ -37,6 +37,16 @@ def math_variant() -> int:
     return _ffi.lib().ssg_math_variant()
 
 
+def math_check(fn: str, base: float, step: float, n: int):
+    """Device log1p / exp (the glibc restatement, host variant) at base + k*step,
+    k in [0, n), against this host's libm: (mismatches, first mismatching x)."""
+    bad = C.c_int64(0)
+    first = C.c_double(0.0)
+    _ffi.call("ssg_math_check", {"log1p": 0, "exp": 1}[fn], float(base), float(step), int(n),
+              C.byref(bad), C.byref(first))
+    return bad.value, first.value
+
+
 class Estimator:
     """Trained per-operator predictors (reference EstimatorModel, estimator.hpp:90-181)."""
 

@@ -53,6 +53,8 @@ _SIGNATURES = {
     "ssg_init": (C.c_int, [C.c_int, C.POINTER(Status)]),
     "ssg_shutdown": (C.c_int, []),
     "ssg_math_variant": (C.c_int, []),
+    "ssg_math_check": (C.c_int, [C.c_int, C.c_double, C.c_double, C.c_int64, pi64, pd,
+                                 C.POINTER(Status)]),
     "ssg_version": (C.c_char_p, []),
     "ssg_free": (None, [P]),
     "ssg_estimator_from_json": (C.c_int, [C.c_char_p, C.c_size_t, C.POINTER(P), C.POINTER(Status)]),

@@ -10,6 +10,7 @@
 #include <mutex>
 #include <functional>
 #include <memory>
+#include <vector>
 
 #include "json.hpp"
 #include "runtime.h"
@@ -184,6 +185,40 @@ int ssg_shutdown(void) {
   ssg::release_sweep_lanes();
   ssg::shutdown_context();
   return SSG_STATUS_OK;
+}
+
+int ssg_math_check(int fn, double base, double step, int64_t n, int64_t* mismatches,
+                   double* first_bad_x, ssg_status* st) {
+  return guarded(st, [&] {
+    require(fn == 0 || fn == 1, "ssg_math_check: fn must be 0 (log1p) or 1 (exp)");
+    require(n >= 0, "ssg_math_check: n must be >= 0");
+    auto& ctx = ssg::context();
+    const int variant = ctx.math_fma;
+    const int64_t chunk = int64_t(1) << 24;
+    ssg::DeviceBuffer<double> d(static_cast<std::size_t>(std::min(n, chunk) + 1));
+    std::vector<double> dev(static_cast<std::size_t>(std::min(n, chunk) + 1));
+    int64_t bad = 0;
+    double first = std::nan("");
+    for (int64_t k0 = 0; k0 < n; k0 += chunk) {
+      const int64_t m = std::min(chunk, n - k0);
+      ssg::launch_math_eval(fn, variant, base, step, k0, m, d.ptr, ctx.stream);
+      d.download(dev.data(), m, ctx.stream);
+      ssg::cuda_check(cudaStreamSynchronize(ctx.stream), "math check");
+      for (int64_t i = 0; i < m; ++i) {
+        // the same x as the device: base + k * step, two roundings, no contraction
+        const double x = base + static_cast<double>(k0 + i) * step;
+        const double h = fn == 0 ? std::log1p(x) : std::exp(x);
+        const bool dev_nan = std::isnan(dev[i]);
+        if ((fn == 1 && dev_nan) || std::memcmp(&h, &dev[i], sizeof h) != 0) {
+          if (fn == 1 && dev_nan && !(std::fabs(x) < 512.0)) continue;  // outside the guarded range
+          if (bad == 0) first = x;
+          ++bad;
+        }
+      }
+    }
+    *mismatches = bad;
+    if (first_bad_x) *first_bad_x = first;
+  });
 }
 
 int ssg_math_variant(void) {

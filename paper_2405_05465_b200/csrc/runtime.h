@@ -59,6 +59,9 @@ struct StreamScope {
 
 // Which glibc contraction this host's libm runs (host_math.cpp).
 int probe_host_math_variant();
+// mathcheck.cu: fn 0 = log1p, 1 = exp of x_k = base + k * step, k in [k0, k0 + n)
+void launch_math_eval(int fn, int fma_variant, double base, double step, int64_t k0, int64_t n,
+                      double* d_out, cudaStream_t s);
 
 // Counters over the library's own kernels (reset/read through the C ABI; the
 // bench reports them next to its timings).

@@ -355,3 +355,34 @@ def test_fast_forward_through_arrivals(ssg, ref, policy, extra, max_batch, qps):
         for q in ("p50", "p90", "p95", "p99"):
             assert rep[k][q] == theirs["report"][k][q], (k, q)
     assert rep["simulated_span"] == theirs["simulated_span"]
+
+
+# acceptance criterion 4 (acceptance.cpp:245-310): LLaMA2-7B on a 30 GB A100,
+# 2 round-robin replicas, bs 64 / 4096 tokens / chunk 512, lognormal lengths
+# (prefill 300 / 1.0, decode 40 / 0.9, max_total 2048) synth seed 404 at 60 QPS
+# seed 405 -- a tight KV pool, so every policy preempts heavily.
+ACCEPT4_DEV = dict(catalog.DEVICES["a100_80g"], device_mem=30e9)
+ACCEPT4_DIST = {"schema_version": 1, "kind": "lognormal", "prefill": {"median": 300, "sigma": 1.0},
+                "decode": {"median": 40, "sigma": 0.9}, "max_total": 2048}
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("policy", ["faster_transformer", "orca_plus", "vllm", "sarathi_serve",
+                                    "lightllm"])
+def test_acceptance4_workload(ssg, ref, policy):
+    """The reference's scheduler-invariant workload at full size (5 policies x
+    10,000 requests): every batch of both replicas, every emission time, the
+    aggregates and the report equal the reference's, preemptions included."""
+    key = ("accept4",)
+    if key not in _EST:
+        text = ref.train(catalog.MODELS["llama2_7b"], ACCEPT4_DEV, [1], "interp", 42)
+        _EST[key] = (ssg.Estimator.from_json(text), ref.Estimator(text))
+    m, t = _EST[key]
+    cluster = catalog.cluster_doc("llama2_7b", ACCEPT4_DEV, tp=1, pp=1, replicas=2, policy=policy,
+                                  max_batch_size=64, max_tokens_per_iter=4096, chunk_size=512)
+    lengths = ssg.synth_trace(ACCEPT4_DIST, 10000, 404)
+    mine, theirs = run_both(ssg, m, t, cluster, baseline_trace(ssg, lengths, 60.0, 405))
+    assert_same(mine, theirs)
+    assert len(theirs["requests"]) == 10000
+    if policy == "vllm":  # the policy that preempts to admit (the criterion's 552K preemptions)
+        assert sum(r["preemptions"] for r in theirs["replicas"]) > 1000
