@@ -12,13 +12,18 @@
 #pragma once
 
 #include <cstdint>
+#include <deque>
 #include <functional>
 #include <map>
 #include <memory>
 #include <optional>
+#include <span>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
+
+#include "json.hpp"  // nlohmann/json 3.11, as the reference (vendor/json.hpp)
 
 namespace servesim {
 
@@ -179,6 +184,48 @@ struct RegressorData {
   std::vector<double> values;
 };
 
+// Prediction backend for one operator (reference regressor.hpp:19-24): trained
+// on log1p-transformed features.  predict() runs on the GPU -- the regressor is
+// flattened to HBM on first use and evaluated by the same device code as the
+// batched predictor (predictor.cuh); data() is the trained parameter set the
+// upload flattens.
+struct DeviceRegressor;  // HBM copy (predictor.cu)
+class Regressor {
+ public:
+  virtual ~Regressor();
+  virtual double predict(std::span<const double> x) const;
+  virtual nlohmann::json to_json() const;
+  const RegressorData& data() const { return data_; }
+
+ protected:
+  explicit Regressor(RegressorData d);
+  RegressorData data_;
+
+ private:
+  mutable std::shared_ptr<DeviceRegressor> dev_;
+};
+
+// reference regressor.hpp:78-270 (random forest of piecewise-linear trees)
+class ForestRegressor final : public Regressor {
+ public:
+  static ForestRegressor train(const std::vector<std::vector<double>>& x,
+                               const std::vector<double>& y, const ForestConfig& cfg);
+  static ForestRegressor from_json(const nlohmann::json& j);
+  explicit ForestRegressor(RegressorData d);
+};
+
+// reference regressor.hpp:273-376 (multilinear interpolation over the profiled grid)
+class GridInterpolator final : public Regressor {
+ public:
+  static GridInterpolator fit(const std::vector<std::vector<double>>& x,
+                              const std::vector<double>& y);
+  static GridInterpolator from_json(const nlohmann::json& j);
+  explicit GridInterpolator(RegressorData d);
+};
+
+// reference regressor.hpp:379-386
+std::unique_ptr<Regressor> regressor_from_json(const nlohmann::json& j);
+
 struct OpModelKey {
   OpName op;
   std::int64_t tp_degree;
@@ -196,7 +243,7 @@ class EstimatorModel {
     std::vector<std::string> schema;
     std::vector<double> bbox_lo, bbox_hi;
     std::vector<std::vector<double>> levels;
-    RegressorData regressor;
+    std::unique_ptr<Regressor> regressor;  // over log1p(features) -> log(runtime)
     double holdout_mape = 0.0;
     std::size_t n_points = 0;
   };
@@ -215,8 +262,9 @@ class EstimatorModel {
   // Single query (reference estimator.hpp:105-123), evaluated on the GPU.
   double predict(OpName op, std::int64_t tp, const FeatureMap& features) const;
 
-  std::string to_json() const;
-  static EstimatorModel from_json(const std::string& text);
+  // reference estimator.hpp:137-177 (the serialized handoff format)
+  nlohmann::json to_json() const;
+  static EstimatorModel from_json(const nlohmann::json& j);
 
   // HBM-resident copy, built on first use and reused by every kernel.
   const DeviceEstimator& device() const;
@@ -274,6 +322,189 @@ struct PolicyConfig {
 };
 void validate(const PolicyConfig& c);
 
+// ---------------------------------------------------------------- scheduler plugin
+struct SchedulerView;  // builds the SimObserver's read-only scheduler views (sim.cpp)
+// reference: scheduler.hpp:78-233, memory.hpp:51-104
+
+// Per-request progress inside one replica (scheduler.hpp:81-96).
+struct RequestState {
+  Request req;
+  std::int64_t prefill_target = 0, prefill_done = 0, emitted = 0, kv_context = 0, restarts = 0;
+  double first_scheduled_time = -1.0, first_token_time = -1.0, completion_time = -1.0;
+  std::vector<double> emission_times;
+  bool prefill_complete() const { return prefill_done >= prefill_target; }
+  bool finished() const { return emitted >= req.decode_tokens; }
+};
+
+struct PrefillEntry {
+  RequestState* request;
+  std::int64_t chunk_tokens;
+  std::int64_t prior_context;
+};
+struct DecodeEntry {
+  RequestState* request;
+  std::int64_t context_tokens;
+};
+
+struct BatchPlan {
+  std::vector<PrefillEntry> prefills;
+  std::vector<DecodeEntry> decodes;
+  bool empty() const { return prefills.empty() && decodes.empty(); }
+  std::int64_t batch_size() const { return static_cast<std::int64_t>(prefills.size() + decodes.size()); }
+  std::int64_t total_current_tokens() const {
+    std::int64_t t = static_cast<std::int64_t>(decodes.size());
+    for (const auto& p : prefills) t += p.chunk_tokens;
+    return t;
+  }
+  BatchComposition composition() const {
+    BatchComposition c;
+    for (const auto& p : prefills) {
+      c.prefill_lengths.push_back(p.chunk_tokens);
+      c.prefill_prior_context.push_back(p.prior_context);
+    }
+    for (const auto& d : decodes) c.decode_context_lengths.push_back(d.context_tokens);
+    return c;
+  }
+};
+
+// Block accounting of one replica (memory.hpp:51-104).  Standalone it is the
+// reference's integer bookkeeping; a ReplicaScheduler's memory() is a snapshot
+// of the accounting its device state holds after the last call.
+class BlockManager {
+ public:
+  BlockManager() = default;
+  BlockManager(const MemoryPlan& plan, bool token_granular)
+      : plan_(plan), token_granular_(token_granular) {}
+  std::int64_t total_units() const {
+    return token_granular_ ? plan_.kv_capacity_tokens : plan_.num_blocks;
+  }
+  std::int64_t free_units() const { return total_units() - allocated_; }
+  std::int64_t allocated_units() const { return allocated_; }
+  std::int64_t watermark_units() const {
+    return token_granular_ ? plan_.watermark_blocks * plan_.block_size : plan_.watermark_blocks;
+  }
+  std::int64_t units_for_tokens(std::int64_t tokens) const {
+    return token_granular_ ? tokens : (tokens + plan_.block_size - 1) / plan_.block_size;
+  }
+  std::int64_t held_units(std::int64_t request_id) const {
+    auto it = held_.find(request_id);
+    return it == held_.end() ? 0 : it->second;
+  }
+  std::int64_t shortfall(std::int64_t request_id, std::int64_t tokens) const {
+    const std::int64_t s = units_for_tokens(tokens) - held_units(request_id);
+    return s > 0 ? s : 0;
+  }
+  bool try_reserve(std::int64_t request_id, std::int64_t tokens);
+  void release(std::int64_t request_id);
+
+ private:
+  friend class ReplicaScheduler;
+  friend struct SchedulerView;
+  MemoryPlan plan_;
+  bool token_granular_ = false;
+  std::int64_t allocated_ = 0;
+  std::map<std::int64_t, std::int64_t> held_;
+};
+
+// Replica-tier scheduler: batching policy + paged KV management
+// (scheduler.hpp:136-233).  The state lives in HBM and every call is one warp
+// of the device scheduler (sched_api.cu) -- the code the simulation kernel runs
+// per BatchStart -- so plans, preemptions and block counts are the engine's.
+// Request states are shared with the caller: after each call the scheduler
+// writes back the fields it owns (progress, restarts, times, emission_times).
+class ReplicaScheduler {
+ public:
+  ReplicaScheduler();
+  ReplicaScheduler(PolicyConfig cfg, MemoryPlan plan);
+  ~ReplicaScheduler();
+  ReplicaScheduler(ReplicaScheduler&&) noexcept;
+  ReplicaScheduler& operator=(ReplicaScheduler&&) noexcept;
+
+  const BlockManager& memory() const { return mem_; }
+  const MemoryPlan& memory_plan() const { return plan_; }
+  const PolicyConfig& config() const { return cfg_; }
+
+  void enqueue(std::shared_ptr<RequestState> r);
+  std::size_t outstanding() const { return outstanding_; }
+  bool has_work() const { return outstanding_ > 0; }
+  std::size_t preemption_count() const { return preemptions_; }
+  // Members of the in-flight request-level batch (FasterTransformer only).
+  std::vector<std::int64_t> ft_member_ids() const { return ft_members_; }
+  void set_now(double now) { now_ = now; }
+  BatchPlan schedule_iteration();
+  std::vector<std::shared_ptr<RequestState>> complete_iteration(const BatchPlan& plan, double now);
+
+ private:
+  friend struct SchedulerView;  // the SimObserver's read-only views (sim.cpp)
+  PolicyConfig cfg_;
+  MemoryPlan plan_;
+  BlockManager mem_;
+  double now_ = 0.0;
+  std::size_t outstanding_ = 0, preemptions_ = 0;
+  std::vector<std::int64_t> ft_members_;
+  struct Device;
+  std::unique_ptr<Device> dev_;  // null for observer views
+  void refresh_();
+};
+
+// Global-tier routing (scheduler.hpp:492-561).  The simulation kernel routes on
+// the device (engine.cu); this is the same policy for callers that drive
+// ReplicaSchedulers themselves.
+class Router {
+ public:
+  Router(RoutingPolicy policy, std::size_t num_replicas, std::int64_t deferred_threshold)
+      : policy_(policy), n_(num_replicas), threshold_(deferred_threshold) {
+    require(n_ >= 1, "router: need at least one replica");
+    require(threshold_ >= 1, "router: deferred threshold must be >= 1");
+  }
+  // Replica for `r`, or nullopt while the deferred policy pools it.
+  template <typename OutstandingFn>
+  std::optional<std::size_t> route(std::shared_ptr<RequestState> r, OutstandingFn&& outstanding) {
+    if (policy_ == RoutingPolicy::RoundRobin) {
+      const std::size_t k = next_;
+      next_ = next_ + 1 == n_ ? 0 : next_ + 1;
+      return k;
+    }
+    if (policy_ == RoutingPolicy::LeastOutstanding) {
+      std::size_t best = 0, load = outstanding(std::size_t(0));
+      for (std::size_t k = 1; k < n_; ++k) {
+        const std::size_t c = outstanding(k);
+        if (c < load) best = k, load = c;  // ties stay on the lowest index
+      }
+      return best;
+    }
+    pool_.push_back(std::move(r));
+    return std::nullopt;
+  }
+  // Deferred policy: pooled requests to replicas below the threshold, least
+  // loaded first (counts advance as requests are assigned).
+  template <typename OutstandingFn>
+  std::vector<std::pair<std::size_t, std::shared_ptr<RequestState>>> drain(OutstandingFn&& outstanding) {
+    std::vector<std::pair<std::size_t, std::shared_ptr<RequestState>>> out;
+    if (policy_ != RoutingPolicy::Deferred || pool_.empty()) return out;
+    std::vector<std::int64_t> load(n_);
+    for (std::size_t k = 0; k < n_; ++k) load[k] = static_cast<std::int64_t>(outstanding(k));
+    while (!pool_.empty()) {
+      std::size_t best = n_;
+      for (std::size_t k = 0; k < n_; ++k)
+        if (load[k] < threshold_ && (best == n_ || load[k] < load[best])) best = k;
+      if (best == n_) break;
+      out.emplace_back(best, std::move(pool_.front()));
+      pool_.pop_front();
+      ++load[best];
+    }
+    return out;
+  }
+  std::size_t pooled() const { return pool_.size(); }
+
+ private:
+  RoutingPolicy policy_;
+  std::size_t n_;
+  std::int64_t threshold_;
+  std::size_t next_ = 0;
+  std::deque<std::shared_ptr<RequestState>> pool_;
+};
+
 // ---------------------------------------------------------------- engine
 // reference: sim.hpp:20-320
 struct ClusterConfig {
@@ -325,13 +556,34 @@ struct BatchLog {
   double now;
   std::int64_t kv_allocated_units;
   std::vector<BatchEntryLog> entries;
+  // observer runs only: the replica's scheduler state at this batch
+  std::int64_t outstanding = 0, preemptions = 0;
+  std::vector<std::int64_t> ft_members;
+};
+
+// Observation hook (sim.hpp:92-97): called with each scheduled batch, in the
+// global event order, before it executes.  run_simulation with an observer runs
+// the replicas in one coupled warp with the batch log enabled and replays the
+// log through the callback after the kernel: `plan` points at RequestStates
+// carrying each request's `req` (progress fields are the device's and are not
+// mirrored), `sched` is a read-only view of the replica at that batch --
+// memory() (allocated / total units), outstanding(), preemption_count(),
+// ft_member_ids(), config(), memory_plan().
+class SimObserver {
+ public:
+  virtual ~SimObserver() = default;
+  virtual void on_batch(std::size_t replica, double now, const BatchPlan& plan,
+                        const ReplicaScheduler& sched) = 0;
 };
 
 struct SimOptions {
   bool record_iterations = false;
-  bool record_batches = false;
+  SimObserver* observer = nullptr;
+  // capacity probes: stop once more than abort_max_late requests were first
+  // scheduled later than abort_delay_threshold after arrival (sim.hpp:99-107)
   double abort_delay_threshold = 0.0;
   std::size_t abort_max_late = 0;
+  bool record_batches = false;  // B200: return the device batch log (SimulationOutput::batches)
 };
 class ProbeInfeasible : public std::exception {
  public:
@@ -374,7 +626,11 @@ struct MetricsReport {
 double percentile(const std::vector<double>& samples, double q);
 MetricsReport build_report(const SimulationResult& result, bool static_mode = false);
 std::string request_metrics_to_csv(const MetricsReport& rep);
-std::string summary_to_json(const MetricsReport& rep);
+nlohmann::ordered_json summary_to_json(const MetricsReport& rep);
+// requests.csv (or requests.json) plus summary.json under out_dir
+// (metrics.hpp:200-231); returns the files written.
+std::vector<std::string> export_metrics(const MetricsReport& rep, const std::string& out_dir,
+                                        const std::string& format);
 
 // ---------------------------------------------------------------- search
 // reference: search.hpp:25-486
@@ -445,23 +701,57 @@ struct SearchOutcome {
   std::optional<std::size_t> best;
 };
 
-// Loaded search config (reference config.hpp:101-179).
+// ---------------------------------------------------------------- files and configs
+// reference: csv.hpp:56-70, config.hpp:17-179 (paths resolve relative to the config file)
+std::string read_text_file(const std::string& path);
+void write_text_file(const std::string& path, const std::string& content);
+nlohmann::json load_json_file(const std::string& path);
+ModelSpec load_model_spec_file(const std::string& path);
+DeviceProfile load_device_file(const std::string& path);
+PolicyConfig parse_policy_config(const nlohmann::json& j);
+
 struct LoadedSearchConfig {
   ModelSpec spec;
-  std::vector<Request> workload;
+  std::vector<Request> workload;  // lengths; arrivals assigned per probe
   SearchOptions options;
+  std::string model_spec_path;
+  std::vector<std::string> device_paths;
+  std::string trace_path;  // empty for synthetic workloads
 };
 LoadedSearchConfig load_search_config(const std::string& path);
 struct LoadedClusterConfig {
   ClusterConfig cluster;
+  std::string model_spec_path;
+  std::string device_path;
 };
 LoadedClusterConfig load_cluster_config(const std::string& path);
 
+// Maximum sustainable rate by doubling then bisection over a monotone
+// feasibility callback (search.hpp:145-174); the feasible end is returned.
+double find_capacity(const std::function<bool(double)>& feasible_at, const CapacitySearchOptions& opts);
 double find_capacity_replay(const std::function<bool(double)>& feasible,
-                            const CapacitySearchOptions& opts);
+                            const CapacitySearchOptions& opts);  // same search (kept name)
 double initial_qps_guess(const ModelSpec& spec, const CandidateConfig& cand,
                          const EstimatorModel& est, const ClusterConfig& cluster);
 double qps_per_dollar(double capacity_qps, std::int64_t gpus_used, double rate_per_gpu_hr);
+
+// One candidate end to end (search.hpp:294-363): capacity search, SLO run at
+// evaluation_fraction of capacity (or the static run of the makespan
+// objective).  Runs on the GPU as a one-config sweep.
+ConfigResult evaluate_config(const ModelSpec& spec, const CandidateConfig& cand,
+                             const DeviceProfile& dev, const EstimatorModel& estimator,
+                             const std::vector<Request>& workload, const SearchOptions& opts);
+// B200: any list of candidates in one sweep (every capacity search advances in
+// the same rounds of speculative probes).  skus[cand.sku_index] and
+// estimators[cand.sku_index] serve each candidate; results are in `cands` order
+// and equal evaluate_config on each.  This is how axes the search config
+// cannot express (watermark, replica count, block size) are swept.
+std::vector<ConfigResult> evaluate_configs(const ModelSpec& spec,
+                                           const std::vector<CandidateConfig>& cands,
+                                           const std::vector<DeviceProfile>& skus,
+                                           const std::vector<const EstimatorModel*>& estimators,
+                                           const std::vector<Request>& workload,
+                                           const SearchOptions& opts);
 
 // The whole sweep on the local GPU: every config's capacity search advances
 // in lock-step rounds of speculative probes (sweep.cu / search.cpp).
@@ -487,6 +777,12 @@ class SearchSession {
  public:
   SearchSession(const ModelSpec& spec, const std::vector<Request>& workload,
                 const SearchOptions& opts);
+  // A session over the caller's candidates, SKUs and trained estimators
+  // (estimators[k] serves skus[k]); evaluate_configs is built on it.
+  SearchSession(const ModelSpec& spec, std::vector<CandidateConfig> cands,
+                const std::vector<DeviceProfile>& skus,
+                const std::vector<const EstimatorModel*>& estimators,
+                const std::vector<Request>& workload, const SearchOptions& opts);
   ~SearchSession();
   std::vector<ConfigResult> evaluate(int shard = 0, int num_shards = 1,
                                      std::vector<std::size_t>* owned = nullptr);
@@ -495,6 +791,7 @@ class SearchSession {
  private:
   struct State;
   std::unique_ptr<State> st_;
+  void open_workload(const std::vector<Request>& workload);
 };
 
 std::string search_results_to_csv(const SearchOutcome& outcome);

@@ -134,3 +134,39 @@ def write_search_config(directory: str, model: str = "llama2_70b", workload: str
         "objective": objective,
     }
     return write_json(os.path.join(directory, "search.json"), cfg)
+
+
+def write_cluster_config(directory: str, model: str, device: str, tp=1, pp=1, replicas=1,
+                         policy="vllm", routing="round_robin", cpu_overhead=0.0,
+                         device_mem=None, **sched) -> str:
+    """File-form cluster config (config.hpp:71-98): model and device documents
+    beside it, referenced by relative path; returns the config path."""
+    os.makedirs(directory, exist_ok=True)
+    dev = dict(DEVICES[device])
+    if device_mem is not None:
+        dev["device_mem"] = device_mem
+    write_json(os.path.join(directory, "models", model + ".json"), MODELS[model])
+    write_json(os.path.join(directory, "devices", device + ".json"), dev)
+    scheduler = {"policy": policy}
+    scheduler.update(sched)
+    cfg = {"schema_version": 1, "model_spec": "models/%s.json" % model,
+           "device": "devices/%s.json" % device,
+           "parallelism": {"tp_degree": tp, "pp_degree": pp, "num_replicas": replicas},
+           "scheduler": scheduler, "routing": {"policy": routing},
+           "cpu_overhead_per_iter": cpu_overhead}
+    return write_json(os.path.join(directory, "cluster.json"), cfg)
+
+
+def write_trace_csv(path: str, lengths, arrivals=None) -> str:
+    """Reference trace CSV (workload.hpp:28-79): ids 0..n-1, with or without arrivals."""
+    os.makedirs(os.path.dirname(os.path.abspath(path)), exist_ok=True)
+    with open(path, "w") as f:
+        if arrivals is None:
+            f.write("request_id,prefill_tokens,decode_tokens\n")
+            for i, (p, d) in enumerate(lengths):
+                f.write("%d,%d,%d\n" % (i, p, d))
+        else:
+            f.write("request_id,arrival_time_s,prefill_tokens,decode_tokens\n")
+            for i, ((p, d), a) in enumerate(zip(lengths, arrivals)):
+                f.write("%d,%r,%d,%d\n" % (i, float(a), p, d))
+    return path

@@ -31,43 +31,6 @@ __device__ unsigned long long g_ff_stats[16];
 #define FFSTAT(i) do { } while (0)
 #endif
 
-// ---------------------------------------------------------------- helpers
-__device__ __forceinline__ RepState load_rep(Unit& U, int r) {
-  __syncwarp();
-  RepState s = U.reps[r];
-  __syncwarp();
-  return s;
-}
-__device__ __forceinline__ void store_rep(Unit& U, int r, const RepState& s) {
-  __syncwarp();
-  if (U.lane == 0) U.reps[r] = s;
-  __syncwarp();
-}
-
-// ReplicaScheduler::enqueue (scheduler.hpp:146-155)
-__device__ __forceinline__ bool enqueue(Unit& U, RepState& S, int r, int32_t j) {
-  const SimConfig& c = *U.cfg;
-  const ReqHot h = U.hot[j];
-  const int64_t need = units_for(c, (int64_t)h.prefill + h.decode);
-  if (need > c.total_units) {
-    set_error(U, SSG_ERR_ENQUEUE, r, U.ids[j], need, (double)c.total_units);
-    return false;
-  }
-  wput(U, &U.hot[j].target, h.prefill + h.emitted);
-  wait_insert(U, S, r, j);
-  S.outstanding += 1;
-  return true;
-}
-
-// start_if_idle (sim.hpp:191-195): has_work() == outstanding() > 0
-__device__ __forceinline__ void start_if_idle(Unit& U, RepState& S) {
-  if (S.busy || S.outstanding == 0) return;
-  S.ev_kind = 1;
-  S.ev_time = U.clock;
-  S.ev_seq = U.seq++;
-  S.busy = 1;
-}
-
 // Router::drain for the deferred policy (scheduler.hpp:532-551) followed by the
 // engine's enqueue + start_if_idle per assignment (sim.hpp:197-202).
 __device__ SSG_COLD void drain_pool(Unit& U) {
@@ -115,94 +78,6 @@ __device__ SSG_COLD void drain_pool(Unit& U) {
   wput(U, &ph[1], size);
 }
 
-// complete_iteration (scheduler.hpp:197-233), warp-parallel over the batch.
-__device__ void complete_batch(Unit& U, RepState& S, int r) {
-  const int32_t np = S.np, nd = S.nd;
-  const bool emit_times = (U.u->flags & SSG_UF_EMISSIONS) != 0;
-  int newly_finished = 0;
-  bool bad = false;
-  for (int32_t k = U.lane; k < np + nd; k += 32) {
-    int32_t j;
-    bool emit;
-    if (k < np) {
-      j = P_IDX(U, r)[k];
-      ReqHot& h = U.hot[j];
-      const int32_t done = h.done + P_CHUNK(U, r)[k];
-      h.done = done;
-      h.kv = done;
-      if (done > h.target) bad = true;  // "prefill progressed past its target"
-      emit = done >= h.target;
-    } else {
-      j = D_IDX(U, r)[k - np];
-      U.hot[j].kv = D_CTX(U, r)[k - np];
-      emit = true;
-    }
-    if (emit) {
-      ReqHot& h = U.hot[j];
-      if (h.emitted >= h.decode) bad = true;  // "emit_token on finished request"
-      const int32_t e = h.emitted + 1;
-      h.emitted = e;
-      if (emit_times) U.emissions[U.emit_base[j] + e - 1] = U.clock;
-      ReqTimes& t = U.tm[j];
-      if (t.first_tok < 0) t.first_tok = U.clock;
-      if (e >= h.decode) {
-        t.completion = U.clock;
-        ++newly_finished;
-      }
-    }
-  }
-  __syncwarp();
-  if (__any_sync(SSG_FULL, bad)) {
-    set_error(U, SSG_ERR_INTERNAL, 4, 0, 0, 0.0);
-    return;
-  }
-  newly_finished = (int)__reduce_add_sync(SSG_FULL, (unsigned)newly_finished);
-  S.outstanding -= newly_finished;
-  // only a request that just emitted its last token holds KV and sits in the
-  // running queue while finished (earlier finishers were released and dropped,
-  // or -- FT -- released with held = 0 and still unfinished members remain):
-  // with none, the release/compaction pass below changes nothing
-  if (newly_finished == 0) return;
-  // release finished runners; drop them from running unless FT froze membership
-  int32_t* a = RUN(U, r);
-  int32_t write = 0;
-  int64_t freed = 0;
-  bool any_unfinished = false;
-  for (int32_t base = 0; base < S.run_n; base += 32) {
-    const int32_t p = base + U.lane;
-    int32_t j = -1;
-    bool fin = false;
-    if (p < S.run_n) {
-      j = a[p];
-      ReqHot& h = U.hot[j];
-      fin = h.emitted >= h.decode;
-      if (fin) {
-        freed += h.held;
-        h.held = 0;
-      } else {
-        any_unfinished = true;
-      }
-    }
-    if (!S.ft_inflight) {
-      const unsigned keep = __ballot_sync(SSG_FULL, p < S.run_n && !fin);
-      const int dst = write + __popc(keep & ((1u << U.lane) - 1u));
-      __syncwarp();
-      if (p < S.run_n && !fin) a[dst] = j;
-      write += __popc(keep);
-    }
-    __syncwarp();
-  }
-  freed = warp_sum64(freed);
-  S.allocated -= freed;
-  if (!S.ft_inflight) {
-    S.run_n = write;
-  } else if (!__any_sync(SSG_FULL, any_unfinished)) {
-    S.run_n = 0;
-    S.ft_inflight = 0;
-  }
-  __syncwarp();
-}
-
 // One BatchStart event (sim.hpp:221-283).  Returns false when the unit must
 // stop (error or probe abort).
 template <int FMA, int FOREST>
@@ -213,13 +88,7 @@ __device__ bool batch_start(Unit& U, RepState& S, int r) {
   S.nd = 0;
   U.plan_tokens = 0;
   U.plan_late = 0;
-  switch (c.policy) {
-    case SSG_POL_FT: schedule_ft(U, S, r); break;
-    case SSG_POL_VLLM: schedule_vllm(U, S, r); break;
-    case SSG_POL_ORCA:
-    case SSG_POL_LIGHTLLM: schedule_orca(U, S, r); break;
-    case SSG_POL_SARATHI: schedule_sarathi(U, S, r); break;
-  }
+  schedule_batch(U, S, r);
   if (failed(U)) return false;
   if (S.np + S.nd == 0) {
     S.busy = 0;
@@ -234,7 +103,11 @@ __device__ bool batch_start(Unit& U, RepState& S, int r) {
   // batch log (SimObserver::on_batch payload, before the abort check)
   int64_t log_hdr = -1;
   if (U.u->flags & SSG_UF_BATCH_LOG) {
-    const int64_t need = 6 + 3LL * S.np + 2LL * S.nd;
+    // observer runs append the scheduler state the SimObserver may query:
+    // outstanding, preemptions, ft_inflight, FT member count + ids (running order)
+    const bool obs = (U.u->flags & SSG_UF_OBSERVER) != 0;
+    const int32_t members = obs && S.ft_inflight ? S.run_n : 0;
+    const int64_t need = 6 + 3LL * S.np + 2LL * S.nd + (obs ? 4 + members : 0);
     const int64_t used = U.out->log_used;
     if (used >= 0 && used + need <= U.u->log_cap) {
       int64_t* L = U.log + used;
@@ -254,6 +127,16 @@ __device__ bool batch_start(Unit& U, RepState& S, int r) {
       for (int32_t k = U.lane; k < S.nd; k += 32) {
         L[6 + 3 * S.np + 2 * k] = U.ids[D_IDX(U, r)[k]];
         L[7 + 3 * S.np + 2 * k] = D_CTX(U, r)[k];
+      }
+      if (obs) {
+        int64_t* X = L + 6 + 3 * S.np + 2 * S.nd;
+        if (U.lane == 0) {
+          X[0] = S.outstanding;
+          X[1] = S.preemptions;
+          X[2] = S.ft_inflight;
+          X[3] = members;
+        }
+        for (int32_t k = U.lane; k < members; k += 32) X[4 + k] = U.ids[RUN(U, r)[k]];
       }
       log_hdr = used;
       wput(U, &U.out->log_used, used + need);

@@ -352,7 +352,7 @@ __device__ __forceinline__ void push_prefill(Unit& U, RepState& S, int r, int32_
 // first one that would not fit are admitted together (no preemption can occur
 // for them); that entry, if any, replays the sequential ensure_decode_memory
 // path, after which the window scan resumes.
-__device__ void schedule_decodes(Unit& U, RepState& S, int r, int32_t max_entries,
+static __device__ void schedule_decodes(Unit& U, RepState& S, int r, int32_t max_entries,
                                  int32_t* budget) {
   const SimConfig& c = *U.cfg;
   int32_t i = 0;
@@ -605,6 +605,143 @@ __device__ SSG_COLD void schedule_ft(Unit& U, RepState& S, int r) {
     __syncwarp();
     S.nd += __popc(m);
   }
+}
+
+// ReplicaScheduler::schedule_iteration's policy dispatch (scheduler.hpp:184-194)
+__device__ __forceinline__ void schedule_batch(Unit& U, RepState& S, int r) {
+  switch (U.cfg->policy) {
+    case SSG_POL_FT: schedule_ft(U, S, r); break;
+    case SSG_POL_VLLM: schedule_vllm(U, S, r); break;
+    case SSG_POL_ORCA:
+    case SSG_POL_LIGHTLLM: schedule_orca(U, S, r); break;
+    case SSG_POL_SARATHI: schedule_sarathi(U, S, r); break;
+  }
+}
+
+// ---------------------------------------------------------------- replica state
+// ---------------------------------------------------------------- helpers
+__device__ __forceinline__ RepState load_rep(Unit& U, int r) {
+  __syncwarp();
+  RepState s = U.reps[r];
+  __syncwarp();
+  return s;
+}
+__device__ __forceinline__ void store_rep(Unit& U, int r, const RepState& s) {
+  __syncwarp();
+  if (U.lane == 0) U.reps[r] = s;
+  __syncwarp();
+}
+
+// ReplicaScheduler::enqueue (scheduler.hpp:146-155)
+__device__ __forceinline__ bool enqueue(Unit& U, RepState& S, int r, int32_t j) {
+  const SimConfig& c = *U.cfg;
+  const ReqHot h = U.hot[j];
+  const int64_t need = units_for(c, (int64_t)h.prefill + h.decode);
+  if (need > c.total_units) {
+    set_error(U, SSG_ERR_ENQUEUE, r, U.ids[j], need, (double)c.total_units);
+    return false;
+  }
+  wput(U, &U.hot[j].target, h.prefill + h.emitted);
+  wait_insert(U, S, r, j);
+  S.outstanding += 1;
+  return true;
+}
+
+// start_if_idle (sim.hpp:191-195): has_work() == outstanding() > 0
+__device__ __forceinline__ void start_if_idle(Unit& U, RepState& S) {
+  if (S.busy || S.outstanding == 0) return;
+  S.ev_kind = 1;
+  S.ev_time = U.clock;
+  S.ev_seq = U.seq++;
+  S.busy = 1;
+}
+
+// complete_iteration (scheduler.hpp:197-233), warp-parallel over the batch.
+static __device__ void complete_batch(Unit& U, RepState& S, int r) {
+  const int32_t np = S.np, nd = S.nd;
+  const bool emit_times = (U.u->flags & SSG_UF_EMISSIONS) != 0;
+  int newly_finished = 0;
+  bool bad = false;
+  for (int32_t k = U.lane; k < np + nd; k += 32) {
+    int32_t j;
+    bool emit;
+    if (k < np) {
+      j = P_IDX(U, r)[k];
+      ReqHot& h = U.hot[j];
+      const int32_t done = h.done + P_CHUNK(U, r)[k];
+      h.done = done;
+      h.kv = done;
+      if (done > h.target) bad = true;  // "prefill progressed past its target"
+      emit = done >= h.target;
+    } else {
+      j = D_IDX(U, r)[k - np];
+      U.hot[j].kv = D_CTX(U, r)[k - np];
+      emit = true;
+    }
+    if (emit) {
+      ReqHot& h = U.hot[j];
+      if (h.emitted >= h.decode) bad = true;  // "emit_token on finished request"
+      const int32_t e = h.emitted + 1;
+      h.emitted = e;
+      if (emit_times) U.emissions[U.emit_base[j] + e - 1] = U.clock;
+      ReqTimes& t = U.tm[j];
+      if (t.first_tok < 0) t.first_tok = U.clock;
+      if (e >= h.decode) {
+        t.completion = U.clock;
+        ++newly_finished;
+      }
+    }
+  }
+  __syncwarp();
+  if (__any_sync(SSG_FULL, bad)) {
+    set_error(U, SSG_ERR_INTERNAL, 4, 0, 0, 0.0);
+    return;
+  }
+  newly_finished = (int)__reduce_add_sync(SSG_FULL, (unsigned)newly_finished);
+  S.outstanding -= newly_finished;
+  // only a request that just emitted its last token holds KV and sits in the
+  // running queue while finished (earlier finishers were released and dropped,
+  // or -- FT -- released with held = 0 and still unfinished members remain):
+  // with none, the release/compaction pass below changes nothing
+  if (newly_finished == 0) return;
+  // release finished runners; drop them from running unless FT froze membership
+  int32_t* a = RUN(U, r);
+  int32_t write = 0;
+  int64_t freed = 0;
+  bool any_unfinished = false;
+  for (int32_t base = 0; base < S.run_n; base += 32) {
+    const int32_t p = base + U.lane;
+    int32_t j = -1;
+    bool fin = false;
+    if (p < S.run_n) {
+      j = a[p];
+      ReqHot& h = U.hot[j];
+      fin = h.emitted >= h.decode;
+      if (fin) {
+        freed += h.held;
+        h.held = 0;
+      } else {
+        any_unfinished = true;
+      }
+    }
+    if (!S.ft_inflight) {
+      const unsigned keep = __ballot_sync(SSG_FULL, p < S.run_n && !fin);
+      const int dst = write + __popc(keep & ((1u << U.lane) - 1u));
+      __syncwarp();
+      if (p < S.run_n && !fin) a[dst] = j;
+      write += __popc(keep);
+    }
+    __syncwarp();
+  }
+  freed = warp_sum64(freed);
+  S.allocated -= freed;
+  if (!S.ft_inflight) {
+    S.run_n = write;
+  } else if (!__any_sync(SSG_FULL, any_unfinished)) {
+    S.run_n = 0;
+    S.ft_inflight = 0;
+  }
+  __syncwarp();
 }
 
 // ---------------------------------------------------------------- latency

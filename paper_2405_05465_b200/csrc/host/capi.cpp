@@ -235,7 +235,13 @@ void ssg_free(void* p) { std::free(p); }
 
 int ssg_estimator_from_json(const char* json, size_t len, ssg_estimator** out, ssg_status* st) {
   return guarded(st, [&] {
-    auto* e = new ssg_estimator{EstimatorModel::from_json(std::string(json, len))};
+    nlohmann::json doc;
+    try {
+      doc = nlohmann::json::parse(std::string(json, len));
+    } catch (const nlohmann::json::exception& ex) {
+      throw Error(std::string("estimator file: invalid JSON: ") + ex.what());
+    }
+    auto* e = new ssg_estimator{EstimatorModel::from_json(doc)};
     *out = e;
   });
 }
@@ -262,7 +268,7 @@ int ssg_estimator_train(const char* model_spec_json, const char* device_json, co
 }
 
 int ssg_estimator_to_json(const ssg_estimator* e, char** out, size_t* len, ssg_status* st) {
-  return guarded(st, [&] { *out = dup_text(e->model.to_json(), len); });
+  return guarded(st, [&] { *out = dup_text(e->model.to_json().dump(), len); });
 }
 
 void ssg_estimator_free(ssg_estimator* e) { delete e; }

@@ -105,7 +105,7 @@ std::string request_metrics_to_csv(const MetricsReport& rep) {
   return out.str();
 }
 
-std::string summary_to_json(const MetricsReport& rep) {
+nlohmann::ordered_json summary_to_json(const MetricsReport& rep) {  // metrics.hpp:173-197
   auto metric = [](const MetricSummary& s) {
     nlohmann::ordered_json j;
     j["mean"] = s.mean;
@@ -127,7 +127,36 @@ std::string summary_to_json(const MetricsReport& rep) {
                   {"kv_utilization_peak", rep.cluster.kv_utilization_peak},
                   {"busy_fraction", rep.cluster.busy_fraction},
                   {"preemptions", rep.cluster.preemptions}};
-  return j.dump(2) + "\n";
+  return j;
+}
+
+std::vector<std::string> export_metrics(const MetricsReport& rep, const std::string& out_dir,
+                                        const std::string& format) {  // metrics.hpp:200-231
+  require(format == "csv" || format == "json", "export: format must be csv or json");
+  std::vector<std::string> written;
+  if (format == "csv") {
+    written.push_back(out_dir + "/requests.csv");
+    write_text_file(written.back(), request_metrics_to_csv(rep));
+  } else {
+    nlohmann::ordered_json rows = nlohmann::ordered_json::array();
+    for (const auto& m : rep.requests) {
+      nlohmann::ordered_json r;
+      r["request_id"] = m.id;
+      r["prefill_tokens"] = m.prefill_tokens;
+      r["decode_tokens"] = m.decode_tokens;
+      r["scheduling_delay_s"] = m.scheduling_delay;
+      r["ttft_s"] = m.ttft;
+      r["e2e_s"] = m.e2e_latency;
+      r["normalized_s_per_token"] = m.normalized_latency;
+      r["restarts"] = m.restarts;
+      rows.push_back(std::move(r));
+    }
+    written.push_back(out_dir + "/requests.json");
+    write_text_file(written.back(), rows.dump(2) + "\n");
+  }
+  written.push_back(out_dir + "/summary.json");
+  write_text_file(written.back(), summary_to_json(rep).dump(2) + "\n");
+  return written;
 }
 
 }  // namespace servesim

@@ -802,7 +802,8 @@ struct SearchSession::State {
   ModelSpec spec;
   SearchOptions opts;
   std::vector<CandidateConfig> configs;
-  std::vector<EstimatorModel> ests;
+  std::vector<EstimatorModel> owned;        // trained by the session (run_search)
+  std::vector<const EstimatorModel*> ests;  // per SKU index: owned or the caller's
   Workload w;
   ResidentWorkload rw;
   DeviceBuffer<double> tables;                    // token tables (context stream)
@@ -831,8 +832,35 @@ SearchSession::SearchSession(const ModelSpec& spec, const std::vector<Request>& 
     if (spec.num_kv_heads % tp == 0) tps.push_back(tp);
   require(!tps.empty(), "search: no valid tp degree for this model");
   for (const auto& sku : opts.space.skus)
-    S.ests.push_back(train(generate_synthetic_profile(spec, sku, tps), opts.train));
-  for (const auto& e : S.ests) e.device();  // resident in HBM before any timed work
+    S.owned.push_back(train(generate_synthetic_profile(spec, sku, tps), opts.train));
+  for (const auto& e : S.owned) S.ests.push_back(&e);
+  open_workload(workload);
+}
+
+SearchSession::SearchSession(const ModelSpec& spec, std::vector<CandidateConfig> cands,
+                             const std::vector<DeviceProfile>& skus,
+                             const std::vector<const EstimatorModel*>& estimators,
+                             const std::vector<Request>& workload, const SearchOptions& opts)
+    : st_(std::make_unique<State>()) {
+  StatsScope stats_scope;
+  PhaseTimer timer("search: session open");
+  State& S = *st_;
+  S.spec = spec;
+  S.opts = opts;
+  S.opts.space.skus = skus;
+  require(estimators.size() == skus.size(), "evaluate_configs: one estimator per SKU");
+  for (const auto& c : cands)
+    require(c.sku_index < skus.size(), "evaluate_configs: candidate " + c.id + " has no SKU");
+  for (auto* e : estimators) internal_check(e != nullptr, "evaluate_configs: null estimator");
+  S.configs = std::move(cands);
+  S.ests = estimators;
+  open_workload(workload);
+}
+
+void SearchSession::open_workload(const std::vector<Request>& workload) {
+  State& S = *st_;
+  const SearchOptions& opts = S.opts;
+  for (const auto* e : S.ests) e->device();  // resident in HBM before any timed work
   require(!workload.empty(), "search: empty workload");
   for (std::size_t i = 0; i < opts.capacity.probe_requests; ++i) {
     Request r = workload[i % workload.size()];
@@ -919,7 +947,7 @@ std::vector<ConfigResult> SearchSession::evaluate(int shard, int num_shards,
     C.res.sku_name = opts.space.skus[cand.sku_index].sku_name;
     C.cluster = ClusterConfig{spec, cand.par, opts.space.skus[cand.sku_index], cand.policy,
                               opts.routing, 0, opts.cpu_overhead_per_iter};
-    C.est = &ests[cand.sku_index];
+    C.est = ests[cand.sku_index];
     C.copts = opts.capacity;
     try {
       C.sim = make_sim_config(C.cluster, *C.est, 0);
@@ -1035,9 +1063,9 @@ std::vector<ConfigResult> SearchSession::evaluate(int shard, int num_shards,
     std::vector<std::size_t> tk;
     std::vector<SsgEstView> tests;
     std::vector<const DeviceEstimator*> test_of;
-    for (const auto& e : ests) {
-      tests.push_back(e.device().view);
-      test_of.push_back(&e.device());
+    for (const auto* e : ests) {
+      tests.push_back(e->device().view);
+      test_of.push_back(&e->device());
     }
     for (std::size_t k = 0; k < cands.size(); ++k) {
       if (!cands[k].sim_ok) continue;
@@ -1166,6 +1194,62 @@ std::vector<ConfigResult> SearchSession::evaluate(int shard, int num_shards,
   for (std::size_t i = 0; i < configs.size(); ++i)
     if (results[i].config.id.empty()) results[i].config = configs[i];
   return results;
+}
+
+double find_capacity(const std::function<bool(double)>& feasible_at,
+                     const CapacitySearchOptions& opts) {  // search.hpp:145-174
+  // the sweep's replay against a memo, answering each rate it asks for from the
+  // caller's probe as it is first needed: the probes run in the reference's order
+  ProbeMemo memo;
+  while (true) {
+    try {
+      return replay_capacity(memo, opts);
+    } catch (const NeedProbe& need) {
+      ProbeAnswer a;
+      a.feasible = feasible_at(need.q);
+      memo.emplace(need.q, a);
+    }
+  }
+}
+
+double find_capacity_replay(const std::function<bool(double)>& feasible,
+                            const CapacitySearchOptions& opts) {
+  return find_capacity(feasible, opts);
+}
+
+double initial_qps_guess(const ModelSpec& spec, const CandidateConfig& cand,
+                         const EstimatorModel& estimator, const ClusterConfig& cluster) {  // search.hpp:278-290
+  auto ops = derive_operators(spec, cand.par);
+  const std::int64_t len = std::min<std::int64_t>(512, spec.max_context);
+  BatchComposition prefill, decode;
+  prefill.prefill_lengths = {len};
+  prefill.prefill_prior_context = {0};
+  decode.decode_context_lengths = {len};
+  const double service =
+      predict_batch(estimator, ops, prefill) + 64.0 * predict_batch(estimator, ops, decode);
+  const double per_replica = 1.0 / std::max(service, 1e-9);
+  return std::max(1e-3, per_replica * static_cast<double>(cluster.par.num_replicas));
+}
+
+std::vector<ConfigResult> evaluate_configs(const ModelSpec& spec,
+                                           const std::vector<CandidateConfig>& cands,
+                                           const std::vector<DeviceProfile>& skus,
+                                           const std::vector<const EstimatorModel*>& estimators,
+                                           const std::vector<Request>& workload,
+                                           const SearchOptions& opts) {
+  if (cands.empty()) return {};
+  SearchSession session(spec, cands, skus, estimators, workload, opts);
+  return session.evaluate();
+}
+
+ConfigResult evaluate_config(const ModelSpec& spec, const CandidateConfig& cand,
+                             const DeviceProfile& dev, const EstimatorModel& estimator,
+                             const std::vector<Request>& workload, const SearchOptions& opts) {
+  CandidateConfig c = cand;
+  c.sku_index = 0;
+  ConfigResult r = evaluate_configs(spec, {c}, {dev}, {&estimator}, workload, opts).at(0);
+  r.config = cand;
+  return r;
 }
 
 SearchOutcome finalize_search(const ModelSpec& spec, const SearchOptions& opts,

@@ -8,6 +8,7 @@
 #include <map>
 #include <numeric>
 #include <string>
+#include <unordered_map>
 
 #include "sim_host.h"
 #include "engine_limits.h"
@@ -331,7 +332,9 @@ void run_jobs(const SimJobs& J, SimResults& R, bool want_requests) {
   L.log = J.log_words > 0 ? d_log.ptr : nullptr;
   L.out = d_out.ptr;
   L.tables = J.tables;
-  L.fast_forward = fast_forward_enabled();
+  bool observed = false;
+  for (const auto& u : J.units) observed = observed || (u.flags & SSG_UF_OBSERVER);
+  L.fast_forward = fast_forward_enabled() && !observed;
   L.has_forest = J.has_forest ? 1 : 0;
   cudaEvent_t ev0, ev1;
   cuda_check(cudaEventCreate(&ev0), "event");
@@ -429,6 +432,24 @@ namespace servesim {
 
 using namespace ssg;
 
+// Read-only ReplicaScheduler views handed to SimObserver::on_batch: the
+// replica's configuration plus the scheduler state the batch log recorded.
+struct SchedulerView {
+  static ReplicaScheduler make(const PolicyConfig& cfg, const MemoryPlan& plan) {
+    ReplicaScheduler s;
+    s.cfg_ = cfg;
+    s.plan_ = plan;
+    s.mem_ = BlockManager(plan, cfg.policy == SchedulerPolicy::LightLLM);
+    return s;
+  }
+  static void set(ReplicaScheduler& s, const BatchLog& b) {
+    s.mem_.allocated_ = b.kv_allocated_units;
+    s.outstanding_ = static_cast<std::size_t>(b.outstanding);
+    s.preemptions_ = static_cast<std::size_t>(b.preemptions);
+    s.ft_members_ = b.ft_members;
+  }
+};
+
 namespace {
 
 struct Placement {
@@ -462,10 +483,11 @@ Placement place(const ClusterConfig& cluster, const std::vector<Request>& trace,
   std::stable_sort(ev.begin(), ev.end(), [&](int32_t a, int32_t b) {
     return trace[a].arrival_time < trace[b].arrival_time;
   });
-  const bool want_log = opts.record_batches || opts.record_iterations;
+  const bool want_log = opts.record_batches || opts.record_iterations || opts.observer;
   UnitSpec us;
   us.config = 0;
   us.flags = SSG_UF_EMISSIONS | (want_log ? SSG_UF_BATCH_LOG : 0) |
+             (opts.observer ? SSG_UF_OBSERVER : 0) |
              (opts.abort_delay_threshold > 0.0 ? SSG_UF_ABORT : 0);
   us.abort_thr = opts.abort_delay_threshold;
   us.abort_max_late = static_cast<int32_t>(std::min<std::size_t>(opts.abort_max_late, INT32_MAX));
@@ -505,7 +527,7 @@ Placement place(const ClusterConfig& cluster, const std::vector<Request>& trace,
     }
     if (identity) order.clear();
     UnitSpec s2 = us;
-    if (want_log) s2.log_cap = 1024 + 16 * tokens;
+    if (want_log) s2.log_cap = 1024 + (opts.observer ? 24 : 16) * tokens;
     J.add_unit(s2, reqs, order);
   }
   return P;
@@ -521,8 +543,13 @@ SimulationOutput run_simulation_logged(const ClusterConfig& cluster,
                                  " has no arrival time; assign arrivals before simulating");
   const int R = static_cast<int>(cluster.par.num_replicas);
   // probes with an abort bound need the global event order of late schedules
+  // an observer sees every replica's batches in the global event order: one
+  // coupled unit logs them in exactly that order
   bool coupled = cluster.routing != RoutingPolicy::RoundRobin ||
-                 (opts.abort_delay_threshold > 0.0 && R > 1);
+                 (opts.abort_delay_threshold > 0.0 && R > 1) || (opts.observer && R > 1);
+  if (opts.observer)
+    require(R <= kMaxCoupledReplicas, "ssg: an observed simulation supports up to " +
+                                          std::to_string(kMaxCoupledReplicas) + " replicas");
   PhaseTimer total("sim: run_simulation");
   Placement P = place(cluster, trace, estimator, opts, coupled);
   SimResults res;
@@ -540,6 +567,86 @@ SimulationOutput run_simulation_logged(const ClusterConfig& cluster,
   }
   const SimJobs& J = P.jobs;
   const SimConfig& cfg = J.configs[0];
+  const bool want_log = opts.record_batches || opts.record_iterations || opts.observer;
+  SimulationOutput out;
+  SimulationResult& r = out.result;
+  std::vector<BatchLog> batches;
+  if (want_log) {
+    for (std::size_t u = 0; u < J.units.size(); ++u) {
+      const SimUnit& su = J.units[u];
+      const int64_t used = res.out[u].log_used;
+      internal_check(used >= 0, "batch log overflow");
+      for (int64_t p = 0; p < used;) {
+        const int64_t* L = res.log.data() + su.log_off + p;
+        BatchLog b;
+        b.replica = !P.coupled ? u : static_cast<std::size_t>(L[0]);
+        b.now = __builtin_bit_cast(double, L[1]);
+        b.kv_allocated_units = L[2];
+        const int64_t np = L[3], nd = L[4];
+        const double lat = __builtin_bit_cast(double, L[5]);
+        for (int64_t k = 0; k < np; ++k)
+          b.entries.push_back(BatchEntryLog{true, L[6 + 3 * k], L[7 + 3 * k], L[8 + 3 * k]});
+        for (int64_t k = 0; k < nd; ++k)
+          b.entries.push_back(BatchEntryLog{false, L[6 + 3 * np + 2 * k], 1, L[7 + 3 * np + 2 * k]});
+        int64_t extra = 0;
+        if (su.flags & SSG_UF_OBSERVER) {
+          const int64_t* X = L + 6 + 3 * np + 2 * nd;
+          b.outstanding = X[0];
+          b.preemptions = X[1];
+          b.ft_members.assign(X + 4, X + 4 + X[3]);
+          extra = 4 + X[3];
+        }
+        if (opts.record_iterations && lat > 0.0) {
+          IterationRecord it;
+          it.start = b.now;
+          it.latency = lat;
+          it.replica = b.replica;
+          it.batch_requests = np + nd;
+          int64_t tok = nd;
+          for (int64_t k = 0; k < np; ++k) tok += L[7 + 3 * k];
+          it.current_tokens = tok;
+          it.prefill_entries = np;
+          it.decode_entries = nd;
+          it.kv_utilization =
+              static_cast<double>(b.kv_allocated_units) / static_cast<double>(cfg.total_units);
+          r.iterations.push_back(it);
+        }
+        batches.push_back(std::move(b));
+        p += 6 + 3 * np + 2 * nd + extra;
+      }
+    }
+    std::stable_sort(r.iterations.begin(), r.iterations.end(), [](const auto& a, const auto& b) {
+      return a.start != b.start ? a.start < b.start : a.replica < b.replica;
+    });
+  }
+  if (opts.observer) {
+    // SimObserver::on_batch in event order (the coupled unit logged it so),
+    // including the batches before an error or abort, as the reference calls it
+    std::vector<RequestState> states(trace.size());
+    std::unordered_map<std::int64_t, RequestState*> by_id;
+    for (std::size_t i = 0; i < trace.size(); ++i) {
+      states[i].req = trace[i];
+      by_id.emplace(trace[i].id, &states[i]);
+    }
+    MemoryPlan plan = plan_memory(cluster.spec, cluster.par, cluster.dev, cluster.policy.block_size,
+                                  cluster.policy.watermark_fraction,
+                                  cluster.policy.activation_reserve_fraction);
+    std::vector<ReplicaScheduler> views;
+    for (int k = 0; k < R; ++k) views.push_back(SchedulerView::make(cluster.policy, plan));
+    for (const auto& b : batches) {
+      BatchPlan bp;
+      for (const auto& e : b.entries) {
+        RequestState* rs = by_id.at(e.request_id);
+        if (e.prefill)
+          bp.prefills.push_back({rs, e.tokens, e.context});
+        else
+          bp.decodes.push_back({rs, e.context});
+      }
+      ReplicaScheduler& v = views.at(b.replica);
+      SchedulerView::set(v, b);
+      opts.observer->on_batch(b.replica, b.now, bp, v);
+    }
+  }
   const SimUnitOut* first_err = nullptr;
   bool aborted = false;
   for (const auto& o : res.out) {
@@ -550,9 +657,6 @@ SimulationOutput run_simulation_logged(const ClusterConfig& cluster,
   if (aborted) throw ProbeInfeasible();
 
   const std::size_t n = trace.size();
-  const bool want_log = opts.record_batches || opts.record_iterations;
-  SimulationOutput out;
-  SimulationResult& r = out.result;
   r.num_devices = cluster.gpus_used();
   r.peak_device_flops = cluster.dev.peak_flops;
   r.replicas.resize(R);
@@ -589,47 +693,33 @@ SimulationOutput run_simulation_logged(const ClusterConfig& cluster,
     rec.emission_times.assign(res.emissions.begin() + b,
                               res.emissions.begin() + b + trace[i].decode_tokens);
   }
-  if (want_log) {
-    for (std::size_t u = 0; u < J.units.size(); ++u) {
-      const SimUnit& su = J.units[u];
-      const int64_t used = res.out[u].log_used;
-      internal_check(used >= 0, "batch log overflow");
-      for (int64_t p = 0; p < used;) {
-        const int64_t* L = res.log.data() + su.log_off + p;
-        BatchLog b;
-        b.replica = !P.coupled ? u : static_cast<std::size_t>(L[0]);
-        b.now = __builtin_bit_cast(double, L[1]);
-        b.kv_allocated_units = L[2];
-        const int64_t np = L[3], nd = L[4];
-        const double lat = __builtin_bit_cast(double, L[5]);
-        for (int64_t k = 0; k < np; ++k)
-          b.entries.push_back(BatchEntryLog{true, L[6 + 3 * k], L[7 + 3 * k], L[8 + 3 * k]});
-        for (int64_t k = 0; k < nd; ++k)
-          b.entries.push_back(BatchEntryLog{false, L[6 + 3 * np + 2 * k], 1, L[7 + 3 * np + 2 * k]});
-        if (opts.record_iterations) {
-          IterationRecord it;
-          it.start = b.now;
-          it.latency = lat;
-          it.replica = b.replica;
-          it.batch_requests = np + nd;
-          int64_t tok = nd;
-          for (int64_t k = 0; k < np; ++k) tok += L[7 + 3 * k];
-          it.current_tokens = tok;
-          it.prefill_entries = np;
-          it.decode_entries = nd;
-          it.kv_utilization =
-              static_cast<double>(b.kv_allocated_units) / static_cast<double>(cfg.total_units);
-          r.iterations.push_back(it);
-        }
-        if (opts.record_batches) out.batches.push_back(std::move(b));
-        p += 6 + 3 * np + 2 * nd;
-      }
-    }
-    std::stable_sort(r.iterations.begin(), r.iterations.end(), [](const auto& a, const auto& b) {
-      return a.start != b.start ? a.start < b.start : a.replica < b.replica;
-    });
-  }
+  if (opts.record_batches) out.batches = std::move(batches);
   return out;
+}
+
+double predict_batch(const EstimatorModel& model, const std::vector<OperatorDescriptor>& ops,
+                     const BatchComposition& batch) {  // estimator.hpp:294-348, on the GPU
+  require(batch.prefill_prior_context.empty() ||
+              batch.prefill_prior_context.size() == batch.prefill_lengths.size(),
+          "predict_batch: prefill_prior_context size mismatch");
+  require(batch.total_current_tokens() > 0, "predict_batch: empty batch");
+  // the models the reference would look up, in its order (a missing one raises first)
+  for (const auto& d : ops) {
+    if (d.op == OpName::AttnPrefill && batch.prefill_lengths.empty()) continue;
+    if (d.op == OpName::AttnDecode && batch.decode_context_lengths.empty()) continue;
+    model.find(d.op, d.tp_degree);
+  }
+  SimConfig cfg{};
+  fill_sim_ops(cfg, ops, model.device());
+  const int64_t np = static_cast<int64_t>(batch.prefill_lengths.size());
+  const int64_t nd = static_cast<int64_t>(batch.decode_context_lengths.size());
+  std::vector<int64_t> prior = batch.prefill_prior_context;
+  prior.resize(static_cast<std::size_t>(np), 0);
+  const int64_t p_off[2] = {0, np}, d_off[2] = {0, nd};
+  double seconds = 0.0, flops = 0.0;
+  predict_batches(model, cfg, 1, p_off, batch.prefill_lengths.data(), prior.data(), d_off,
+                  batch.decode_context_lengths.data(), &seconds, &flops);
+  return seconds;
 }
 
 SimulationResult run_simulation(const ClusterConfig& cluster, const std::vector<Request>& trace,

@@ -292,6 +292,46 @@ std::vector<ProfileRecord> generate_synthetic_profile(const ModelSpec& spec,
   return out;
 }
 
+// Root-sum-square prefill length (estimator.hpp:38-46); the engine forms the
+// same value on the device from integer sums of squares (exact below 2^53).
+std::int64_t equivalent_prefill_length(const std::vector<std::int64_t>& prefill_lengths) {
+  require(!prefill_lengths.empty(), "equivalent_prefill_length: empty prefill set");
+  double sq = 0.0;
+  for (auto p : prefill_lengths) {
+    require(p > 0, "equivalent_prefill_length: lengths must be positive");
+    sq += static_cast<double>(p) * static_cast<double>(p);
+  }
+  return static_cast<std::int64_t>(std::llround(std::sqrt(sq)));
+}
+
+// Model flops of one batch on one device (estimator.hpp:353-380): the MFU
+// numerator for callers of the API; the engine accumulates the same terms on
+// the device per iteration (engine.cuh batch_latency).
+double batch_device_flops(const std::vector<OperatorDescriptor>& ops, const BatchComposition& batch) {
+  const double total_tokens = static_cast<double>(batch.total_current_tokens());
+  double flops = 0.0;
+  for (const auto& d : ops) {
+    const double count = static_cast<double>(d.count);
+    if (d.op_class == OpClass::TokenLevel) {
+      flops += count * token_work(d, total_tokens).flops;
+    } else if (d.op_class == OpClass::SequenceLevel) {
+      const double kvb = 2.0 * static_cast<double>(d.elem_bytes) *
+                         static_cast<double>(d.kv_heads_per_device * d.head_dim);
+      if (d.op == OpName::AttnPrefill && !batch.prefill_lengths.empty()) {
+        const double n_eq = static_cast<double>(equivalent_prefill_length(batch.prefill_lengths));
+        double prior = 0.0;
+        for (auto c : batch.prefill_prior_context) prior += static_cast<double>(c);
+        flops += count * attention_work(d, n_eq, prior * kvb).flops;
+      } else if (d.op == OpName::AttnDecode && !batch.decode_context_lengths.empty()) {
+        double ctx = 0.0;
+        for (auto c : batch.decode_context_lengths) ctx += static_cast<double>(c);
+        flops += count * attention_work(d, static_cast<double>(batch.num_decode_tokens()), ctx * kvb).flops;
+      }
+    }
+  }
+  return flops;
+}
+
 // ------------------------------------------------------------------ regressors
 namespace {
 
@@ -593,7 +633,11 @@ EstimatorModel train(const std::vector<ProfileRecord>& records, const TrainConfi
       }
       m.holdout_mape = ape / static_cast<double>(held.size());
     }
-    m.regressor = fit(cfg.regressor, x, y, fc);
+    RegressorData fitted = fit(cfg.regressor, x, y, fc);
+    if (fitted.type == "forest")
+      m.regressor = std::make_unique<ForestRegressor>(std::move(fitted));
+    else
+      m.regressor = std::make_unique<GridInterpolator>(std::move(fitted));
     model.insert(key, std::move(m));
   }
   return model;
@@ -659,7 +703,39 @@ RegressorData regressor_from(const json& j) {
 
 }  // namespace
 
-std::string EstimatorModel::to_json() const {
+// ------------------------------------------------------------------ Regressor
+Regressor::Regressor(RegressorData d) : data_(std::move(d)) {}
+Regressor::~Regressor() = default;
+json Regressor::to_json() const { return regressor_json(data_); }
+ForestRegressor::ForestRegressor(RegressorData d) : Regressor(std::move(d)) {
+  require(data_.type == "forest", "ForestRegressor: not a forest");
+}
+GridInterpolator::GridInterpolator(RegressorData d) : Regressor(std::move(d)) {
+  require(data_.type == "interp", "GridInterpolator: not an interpolator");
+}
+ForestRegressor ForestRegressor::train(const std::vector<std::vector<double>>& x,
+                                       const std::vector<double>& y, const ForestConfig& cfg) {
+  return ForestRegressor(fit_forest(x, y, cfg));
+}
+ForestRegressor ForestRegressor::from_json(const json& j) {
+  require(j.at("type").get<std::string>() == "forest", "forest model: wrong type");
+  return ForestRegressor(regressor_from(j));
+}
+GridInterpolator GridInterpolator::fit(const std::vector<std::vector<double>>& x,
+                                       const std::vector<double>& y) {
+  return GridInterpolator(fit_interp(x, y));
+}
+GridInterpolator GridInterpolator::from_json(const json& j) {
+  require(j.at("type").get<std::string>() == "interp", "interp model: wrong type");
+  return GridInterpolator(regressor_from(j));
+}
+std::unique_ptr<Regressor> regressor_from_json(const json& j) {
+  RegressorData r = regressor_from(j);  // throws "unknown regressor type '...'"
+  if (r.type == "forest") return std::make_unique<ForestRegressor>(std::move(r));
+  return std::make_unique<GridInterpolator>(std::move(r));
+}
+
+json EstimatorModel::to_json() const {
   json j;
   j["schema_version"] = 1;
   j["kind"] = "estimator";
@@ -674,20 +750,14 @@ std::string EstimatorModel::to_json() const {
     mj["levels"] = m.levels;
     mj["holdout_mape"] = m.holdout_mape;
     mj["n_points"] = m.n_points;
-    mj["regressor"] = regressor_json(m.regressor);
+    mj["regressor"] = m.regressor->to_json();
     ops[servesim::to_string(key)] = std::move(mj);
   }
   j["ops"] = std::move(ops);
-  return j.dump();
+  return j;
 }
 
-EstimatorModel EstimatorModel::from_json(const std::string& text) {
-  json j;
-  try {
-    j = json::parse(text);
-  } catch (const json::exception& e) {
-    throw Error(std::string("estimator file: invalid JSON: ") + e.what());
-  }
+EstimatorModel EstimatorModel::from_json(const json& j) {
   try {
     require(j.value("kind", "") == "estimator", "estimator file: wrong kind");
     require(j.at("schema_version").get<int>() == 1, "estimator file: unsupported schema_version");
@@ -702,7 +772,7 @@ EstimatorModel EstimatorModel::from_json(const std::string& text) {
       m.levels = mj.at("levels").get<std::vector<std::vector<double>>>();
       m.holdout_mape = mj.at("holdout_mape").get<double>();
       m.n_points = mj.at("n_points").get<std::size_t>();
-      m.regressor = regressor_from(mj.at("regressor"));
+      m.regressor = regressor_from_json(mj.at("regressor"));
       e.models_[key] = std::move(m);
     }
     return e;

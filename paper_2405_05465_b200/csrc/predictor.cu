@@ -238,9 +238,131 @@ void EstimatorModel::insert(const OpModelKey& k, PerOpModel m) {
   dev_.reset();
 }
 
+namespace {
+
+// Flattens one trained regressor into the device pools (interp axes + values
+// in dpool; forest trees as preorder 16 B nodes) and fills the descriptor's
+// regressor fields; returns the algorithmic bytes of one query:
+// features + output, plus interp: 2^nf corner values + binary-search probes
+// per axis; forest: per tree, visited nodes x 20 B + the leaf plane.
+int64_t flatten_regressor(const RegressorData& r, SsgModelDesc& desc, std::vector<double>& dpool,
+                          std::vector<SsgNode>& nodes, std::vector<int32_t>& roots) {
+  if (r.type == "interp") {
+    desc.kind = SSG_KIND_INTERP;
+    internal_check(r.axes.size() == static_cast<std::size_t>(desc.nf),
+                   "interp predict: feature count mismatch");
+    for (int f = 0; f < desc.nf; ++f) {
+      desc.axis_len[f] = static_cast<int32_t>(r.axes[f].size());
+      desc.axis_off[f] = static_cast<int64_t>(dpool.size());
+      dpool.insert(dpool.end(), r.axes[f].begin(), r.axes[f].end());
+    }
+    desc.values_off = static_cast<int64_t>(dpool.size());
+    dpool.insert(dpool.end(), r.values.begin(), r.values.end());
+  } else {
+    desc.kind = SSG_KIND_FOREST;
+    internal_check(r.num_features == static_cast<std::size_t>(desc.nf),
+                   "forest predict: feature count mismatch");
+    desc.ntrees = static_cast<int32_t>(r.trees.size());
+    desc.roots_off = static_cast<int64_t>(roots.size());
+    desc.y_lo = r.y_lo;
+    desc.y_hi = r.y_hi;
+    for (const auto& t : r.trees) roots.push_back(append_tree(t, r.num_features, nodes));
+  }
+  int64_t qb = 8 * desc.nf + 8;
+  if (desc.kind == SSG_KIND_INTERP) {
+    qb += 8 * (int64_t(1) << desc.nf);
+    for (int f = 0; f < desc.nf; ++f)
+      qb += 8 * static_cast<int64_t>(std::ceil(std::log2(std::max(1, desc.axis_len[f]))));
+  } else {
+    for (const auto& t : r.trees) {
+      // mean internal-node depth of the tree's leaves
+      std::vector<std::pair<int, int>> st{{0, 0}};
+      double sum = 0.0;
+      int leaves = 0;
+      while (!st.empty()) {
+        auto [node, depth] = st.back();
+        st.pop_back();
+        if (t.feature[node] >= 0) {
+          st.push_back({t.left[node], depth + 1});
+          st.push_back({t.right[node], depth + 1});
+        } else {
+          sum += depth;
+          ++leaves;
+        }
+      }
+      qb += static_cast<int64_t>(std::llround(20.0 * sum / std::max(1, leaves))) + 8 * (desc.nf + 1);
+    }
+  }
+  return qb;
+}
+
+// Uploads the pools (each kept non-empty so the view never carries null pointers).
+void upload_pools(DeviceEstimator& d, std::vector<double>& dpool, std::vector<SsgNode>& nodes,
+                  std::vector<int32_t>& roots) {
+  auto& ctx = ssg::context();
+  internal_check(nodes.size() < (1u << 31), "forest: node pool exceeds int32 addressing");
+  if (dpool.empty()) dpool.push_back(0.0);
+  if (nodes.empty()) nodes.push_back(SsgNode{});
+  if (roots.empty()) roots.push_back(0);
+  d.models.upload(d.host_models, ctx.stream);
+  d.dpool.upload(dpool, ctx.stream);
+  d.nodes.upload(nodes, ctx.stream);
+  d.roots.upload(roots, ctx.stream);
+  ssg::cuda_check(cudaStreamSynchronize(ctx.stream), "estimator upload");
+  d.bytes = d.host_models.size() * sizeof(SsgModelDesc) + dpool.size() * 8 +
+            nodes.size() * sizeof(SsgNode) + roots.size() * 4;
+  d.view.models = d.models.ptr;
+  d.view.dpool = d.dpool.ptr;
+  d.view.nodes = d.nodes.ptr;
+  d.view.roots = d.roots.ptr;
+  d.view.nmodels = static_cast<int32_t>(d.host_models.size());
+  d.view.math_fma = ctx.math_fma;
+}
+
+// Regressor::predict: the raw regressor output over already-transformed
+// features (no guard, no exp), by the same device code as the predictor.
+__global__ void k_regress(SsgEstView E, const double* x, double* out) {
+  const SsgModelDesc& m = E.models[0];
+  const double x1 = m.nf > 1 ? x[1] : 0.0;
+  out[0] = m.kind == SSG_KIND_FOREST ? ssg_forest(E, m, x[0], x1) : ssg_interp(E, m, x[0], x1);
+}
+
+}  // namespace
+
+struct DeviceRegressor {
+  DeviceEstimator est;
+};
+
+double Regressor::predict(std::span<const double> x) const {
+  auto& ctx = ssg::context();
+  if (!dev_) {
+    auto d = std::make_shared<DeviceRegressor>();
+    SsgModelDesc desc{};
+    desc.nf = static_cast<int32_t>(data_.type == "forest" ? data_.num_features : data_.axes.size());
+    internal_check(desc.nf >= 1 && desc.nf <= 2, "regressor upload: models take 1 or 2 features");
+    std::vector<double> dpool;
+    std::vector<SsgNode> nodes;
+    std::vector<int32_t> roots;
+    d->est.qbytes.push_back(flatten_regressor(data_, desc, dpool, nodes, roots));
+    d->est.host_models.push_back(desc);
+    upload_pools(d->est, dpool, nodes, roots);
+    dev_ = std::move(d);
+  }
+  const int nf = dev_->est.host_models[0].nf;
+  internal_check(x.size() >= static_cast<std::size_t>(nf), "regressor predict: feature count mismatch");
+  double v[3] = {x[0], nf > 1 ? x[1] : 0.0, 0.0};
+  ssg::DeviceBuffer<double> buf(3);
+  buf.upload(v, 2, ctx.stream);
+  k_regress<<<1, 1, 0, ctx.stream>>>(dev_->est.view, buf.ptr, buf.ptr + 2);
+  ssg::cuda_check(cudaGetLastError(), "k_regress launch");
+  double out = 0.0;
+  ssg::cuda_check(cudaMemcpyAsync(&out, buf.ptr + 2, 8, cudaMemcpyDeviceToHost, ctx.stream), "D2H");
+  ssg::cuda_check(cudaStreamSynchronize(ctx.stream), "regressor predict");
+  return out;
+}
+
 const DeviceEstimator& EstimatorModel::device() const {
   if (dev_) return *dev_;
-  auto& ctx = ssg::context();
   auto d = std::make_unique<DeviceEstimator>();
   std::vector<double> dpool;
   std::vector<SsgNode> nodes;
@@ -257,79 +379,14 @@ const DeviceEstimator& EstimatorModel::device() const {
       desc.lower[f] = m.bbox_lo[f] - margin;
       desc.upper[f] = m.bbox_hi[f] + margin;
     }
-    const RegressorData& r = m.regressor;
-    if (r.type == "interp") {
-      desc.kind = SSG_KIND_INTERP;
-      internal_check(r.axes.size() == static_cast<std::size_t>(desc.nf),
-                     "interp predict: feature count mismatch");
-      for (int f = 0; f < desc.nf; ++f) {
-        desc.axis_len[f] = static_cast<int32_t>(r.axes[f].size());
-        desc.axis_off[f] = static_cast<int64_t>(dpool.size());
-        dpool.insert(dpool.end(), r.axes[f].begin(), r.axes[f].end());
-      }
-      desc.values_off = static_cast<int64_t>(dpool.size());
-      dpool.insert(dpool.end(), r.values.begin(), r.values.end());
-    } else {
-      desc.kind = SSG_KIND_FOREST;
-      d->has_forest = true;
-      internal_check(r.num_features == static_cast<std::size_t>(desc.nf),
-                     "forest predict: feature count mismatch");
-      desc.ntrees = static_cast<int32_t>(r.trees.size());
-      desc.roots_off = static_cast<int64_t>(roots.size());
-      desc.y_lo = r.y_lo;
-      desc.y_hi = r.y_hi;
-      for (const auto& t : r.trees) roots.push_back(append_tree(t, r.num_features, nodes));
-    }
-    // algorithmic bytes per query: features + output, plus
-    // interp: 2^nf corner values + binary-search probes per axis;
-    // forest: per tree, visited nodes x 20 B + the leaf plane
-    int64_t qb = 8 * desc.nf + 8;
-    if (desc.kind == SSG_KIND_INTERP) {
-      qb += 8 * (int64_t(1) << desc.nf);
-      for (int f = 0; f < desc.nf; ++f)
-        qb += 8 * static_cast<int64_t>(std::ceil(std::log2(std::max(1, desc.axis_len[f]))));
-    } else {
-      for (const auto& t : r.trees) {
-        // mean internal-node depth of the tree's leaves
-        std::vector<std::pair<int, int>> st{{0, 0}};
-        double sum = 0.0;
-        int leaves = 0;
-        while (!st.empty()) {
-          auto [node, depth] = st.back();
-          st.pop_back();
-          if (t.feature[node] >= 0) {
-            st.push_back({t.left[node], depth + 1});
-            st.push_back({t.right[node], depth + 1});
-          } else {
-            sum += depth;
-            ++leaves;
-          }
-        }
-        qb += static_cast<int64_t>(std::llround(20.0 * sum / std::max(1, leaves))) + 8 * (desc.nf + 1);
-      }
-    }
+    internal_check(m.regressor != nullptr, "estimator upload: model without a regressor");
+    const int64_t qb = flatten_regressor(m.regressor->data(), desc, dpool, nodes, roots);
+    if (desc.kind == SSG_KIND_FOREST) d->has_forest = true;
     d->qbytes.push_back(qb);
     d->index[key] = static_cast<int32_t>(d->host_models.size());
     d->host_models.push_back(desc);
   }
-  internal_check(nodes.size() < (1u << 31), "forest: node pool exceeds int32 addressing");
-  // keep every pool non-empty so the view never carries null pointers
-  if (dpool.empty()) dpool.push_back(0.0);
-  if (nodes.empty()) nodes.push_back(SsgNode{});
-  if (roots.empty()) roots.push_back(0);
-  d->models.upload(d->host_models, ctx.stream);
-  d->dpool.upload(dpool, ctx.stream);
-  d->nodes.upload(nodes, ctx.stream);
-  d->roots.upload(roots, ctx.stream);
-  ssg::cuda_check(cudaStreamSynchronize(ctx.stream), "estimator upload");
-  d->bytes = d->host_models.size() * sizeof(SsgModelDesc) + dpool.size() * 8 +
-             nodes.size() * sizeof(SsgNode) + roots.size() * 4;
-  d->view.models = d->models.ptr;
-  d->view.dpool = d->dpool.ptr;
-  d->view.nodes = d->nodes.ptr;
-  d->view.roots = d->roots.ptr;
-  d->view.nmodels = static_cast<int32_t>(d->host_models.size());
-  d->view.math_fma = ctx.math_fma;
+  upload_pools(*d, dpool, nodes, roots);
   dev_ = std::move(d);
   return *dev_;
 }
