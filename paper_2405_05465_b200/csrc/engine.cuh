@@ -457,50 +457,6 @@ static __device__ void schedule_decodes(Unit& U, RepState& S, int r, int32_t max
   }
 }
 
-__device__ SSG_WARM void schedule_vllm(Unit& U, RepState& S, int r) {
-  const SimConfig& c = *U.cfg;
-  int32_t budget = c.max_tokens;
-  while (S.wait_n > 0 && S.run_n < c.max_batch) {
-    const int32_t head = wait_front(U, S, r);
-    const int32_t prompt = U.hot[head].target;
-    const bool alone = prompt > c.max_tokens;
-    if (alone && S.np > 0) break;
-    if (!alone && prompt > budget) break;
-    if (!admit_reserve(U, S, r, head, prompt, true, true)) break;
-    wait_erase(U, S, r, head);
-    run_insert(U, S, r, head);
-    mark_scheduled(U, head);
-    push_prefill(U, S, r, head, prompt, 0);
-    budget -= (prompt < budget ? prompt : budget);
-    if (alone || budget == 0) break;
-  }
-  __syncwarp();
-  if (S.np > 0) return;
-  schedule_decodes(U, S, r, c.max_batch, nullptr);
-}
-
-__device__ SSG_WARM void schedule_orca(Unit& U, RepState& S, int r) {
-  const SimConfig& c = *U.cfg;
-  int32_t budget = c.max_tokens;
-  while (S.wait_n > 0 && S.run_n < c.max_batch) {
-    const int32_t head = wait_front(U, S, r);
-    const int32_t prompt = U.hot[head].target;
-    const bool alone = prompt > c.max_tokens;
-    if (alone && S.np > 0) break;
-    if (!alone && prompt > budget) break;
-    if (!admit_reserve(U, S, r, head, prompt, false, true)) break;
-    wait_erase(U, S, r, head);
-    run_insert(U, S, r, head);
-    mark_scheduled(U, head);
-    push_prefill(U, S, r, head, prompt, 0);
-    budget -= (prompt < budget ? prompt : budget);
-    if (alone) return;
-    if (budget == 0) break;
-  }
-  __syncwarp();
-  schedule_decodes(U, S, r, c.max_batch, &budget);
-}
-
 // First position >= i of the running queue whose request matches `pred`
 // (warp-parallel 32-entry windows); run_n if none.
 #define PRED_PREFILL_LEFT 0
@@ -519,36 +475,76 @@ __device__ SSG_WARM int32_t next_running(Unit& U, const RepState& S, int r, int3
   return S.run_n;
 }
 
-__device__ SSG_WARM void schedule_sarathi(Unit& U, RepState& S, int r) {
+// vLLM, Orca+ / LightLLM and Sarathi-Serve batch formation in one body
+// (scheduler.hpp:354-444).  The three differ only in phase order -- vLLM and
+// Orca+ admit waiting prompts, then decode; Sarathi decodes, continues in-flight
+// chunks, then admits -- and in a few per-phase rules, so each phase has ONE
+// call site (the admission's admit_reserve, schedule_decodes and their
+// preemption paths are emitted once): the simulation kernel is instruction-
+// fetch bound, and co-resident warps of different policies now share this code.
+//   vLLM:    budget max_tokens, admission may preempt; decodes only when no
+//            prefill was admitted, with no token budget
+//   Orca+:   budget max_tokens, no preemption; decodes share the budget left;
+//            a prompt longer than the budget runs alone (no decodes)
+//   Sarathi: budget chunk_size; decodes first; then in-flight chunks in running
+//            order; then admission of chunk = min(budget, prompt)
+__device__ SSG_WARM void schedule_chunked(Unit& U, RepState& S, int r) {
   const SimConfig& c = *U.cfg;
-  int32_t budget = c.chunk;
-  schedule_decodes(U, S, r, c.max_batch, &budget);
-  // in-flight chunks in running order; a 32-entry window is scanned at once
-  // and only the requests with prefill left are visited one by one
-  for (int32_t i = 0; i < S.run_n;) {
-    if (budget < 1 || S.np + S.nd >= c.max_batch) break;
-    const int32_t k = next_running(U, S, r, i, PRED_PREFILL_LEFT);
-    if (k >= S.run_n) break;
-    const int32_t j = RUN(U, r)[k];
-    const ReqHot h = U.hot[j];
-    const int32_t rem = h.target - h.done;
-    const int32_t chunk = budget < rem ? budget : rem;
-    if (!admit_reserve(U, S, r, j, (int64_t)h.done + chunk, false, false)) break;
-    mark_scheduled(U, j);
-    push_prefill(U, S, r, j, chunk, h.done);
-    budget -= chunk;
-    i = k + 1;
-  }
-  while (budget > 0 && S.wait_n > 0 && S.run_n < c.max_batch && S.np + S.nd < c.max_batch) {
-    const int32_t head = wait_front(U, S, r);
-    const int32_t t = U.hot[head].target;
-    const int32_t chunk = budget < t ? budget : t;
-    if (!admit_reserve(U, S, r, head, chunk, false, true)) break;
-    wait_erase(U, S, r, head);
-    run_insert(U, S, r, head);
-    mark_scheduled(U, head);
-    push_prefill(U, S, r, head, chunk, 0);
-    budget -= chunk;
+  const bool sar = c.policy == SSG_POL_SARATHI, vl = c.policy == SSG_POL_VLLM;
+  int32_t budget = sar ? c.chunk : c.max_tokens;
+  bool decodes = true;
+#pragma unroll 1
+  for (int ph = 0; ph < 3; ++ph) {
+    // 0 = decodes, 1 = in-flight chunks, 2 = admission, 3 = nothing
+    const int what = sar ? ph : (ph == 0 ? 2 : (ph == 1 ? 0 : 3));
+    if (what == 0) {
+      if (decodes) schedule_decodes(U, S, r, c.max_batch, vl ? nullptr : &budget);
+    } else if (what == 1) {
+      // in-flight chunks in running order; a 32-entry window is scanned at once
+      // and only the requests with prefill left are visited one by one
+      for (int32_t i = 0; i < S.run_n;) {
+        if (budget < 1 || S.np + S.nd >= c.max_batch) break;
+        const int32_t k = next_running(U, S, r, i, PRED_PREFILL_LEFT);
+        if (k >= S.run_n) break;
+        const int32_t j = RUN(U, r)[k];
+        const ReqHot h = U.hot[j];
+        const int32_t rem = h.target - h.done;
+        const int32_t chunk = budget < rem ? budget : rem;
+        if (!admit_reserve(U, S, r, j, (int64_t)h.done + chunk, false, false)) break;
+        mark_scheduled(U, j);
+        push_prefill(U, S, r, j, chunk, h.done);
+        budget -= chunk;
+        i = k + 1;
+      }
+    } else if (what == 2) {
+      while (S.wait_n > 0 && S.run_n < c.max_batch) {
+        if (sar && !(budget > 0 && S.np + S.nd < c.max_batch)) break;
+        const int32_t head = wait_front(U, S, r);
+        const int32_t t = U.hot[head].target;
+        int32_t chunk = t;
+        bool alone = false;
+        if (sar) {
+          chunk = budget < t ? budget : t;
+        } else {
+          alone = t > c.max_tokens;
+          if (alone && S.np > 0) break;
+          if (!alone && t > budget) break;
+        }
+        if (!admit_reserve(U, S, r, head, chunk, vl, true)) break;
+        wait_erase(U, S, r, head);
+        run_insert(U, S, r, head);
+        mark_scheduled(U, head);
+        push_prefill(U, S, r, head, chunk, 0);
+        budget -= sar ? chunk : (t < budget ? t : budget);
+        if (alone) {
+          decodes = false;
+          break;
+        }
+        if (!sar && budget == 0) break;
+      }
+      __syncwarp();
+      if (vl && S.np > 0) decodes = false;
+    }
   }
   __syncwarp();
 }
@@ -609,13 +605,10 @@ __device__ SSG_COLD void schedule_ft(Unit& U, RepState& S, int r) {
 
 // ReplicaScheduler::schedule_iteration's policy dispatch (scheduler.hpp:184-194)
 __device__ __forceinline__ void schedule_batch(Unit& U, RepState& S, int r) {
-  switch (U.cfg->policy) {
-    case SSG_POL_FT: schedule_ft(U, S, r); break;
-    case SSG_POL_VLLM: schedule_vllm(U, S, r); break;
-    case SSG_POL_ORCA:
-    case SSG_POL_LIGHTLLM: schedule_orca(U, S, r); break;
-    case SSG_POL_SARATHI: schedule_sarathi(U, S, r); break;
-  }
+  if (U.cfg->policy == SSG_POL_FT)
+    schedule_ft(U, S, r);
+  else
+    schedule_chunked(U, S, r);
 }
 
 // ---------------------------------------------------------------- replica state
@@ -1109,9 +1102,8 @@ __device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, doubl
       }
       flops = __dadd_rn(flops, __dmul_rn(flop_part[m], (double)(c.tp * c.pp)));
     }
-#pragma unroll
-    for (int st_i = 0; st_i < 4; ++st_i) {
-      if (st_i >= pp) break;
+#pragma unroll 1
+    for (int st_i = 0; st_i < pp; ++st_i) {
       double prev = 0.0;
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
