@@ -49,6 +49,7 @@ __device__ SSG_COLD void drain_pool(Unit& U) {
   while (size > 0) {
     // best = lowest index among counts < threshold with the smallest count
     int64_t key = INT64_MAX;
+#pragma unroll 1
     for (int r0 = 0; r0 < R; r0 += 32) {
       const int r = r0 + U.lane;
       int64_t k2 = INT64_MAX;
@@ -119,11 +120,13 @@ __device__ bool batch_start(Unit& U, RepState& S, int r) {
         L[4] = S.nd;
         L[5] = 0;
       }
+#pragma unroll 1
       for (int32_t k = U.lane; k < S.np; k += 32) {
         L[6 + 3 * k] = U.ids[P_IDX(U, r)[k]];
         L[7 + 3 * k] = P_CHUNK(U, r)[k];
         L[8 + 3 * k] = P_PRIOR(U, r)[k];
       }
+#pragma unroll 1
       for (int32_t k = U.lane; k < S.nd; k += 32) {
         L[6 + 3 * S.np + 2 * k] = U.ids[D_IDX(U, r)[k]];
         L[7 + 3 * S.np + 2 * k] = D_CTX(U, r)[k];
@@ -136,6 +139,7 @@ __device__ bool batch_start(Unit& U, RepState& S, int r) {
           X[2] = S.ft_inflight;
           X[3] = members;
         }
+#pragma unroll 1
         for (int32_t k = U.lane; k < members; k += 32) X[4 + k] = U.ids[RUN(U, r)[k]];
       }
       log_hdr = used;
@@ -622,6 +626,7 @@ __device__ void run_unit(Unit& U) {
   const SimConfig& c = *U.cfg;
   const int R = u.R;
   // ---- reset per-request state and replicas
+#pragma unroll 1
   for (int32_t j = U.lane; j < u.n; j += 32) {
     ReqHot& h = U.hot[j];
     h.target = 0;
@@ -636,6 +641,7 @@ __device__ void run_unit(Unit& U) {
     t.completion = -1.0;
     U.restarts[j] = 0;
   }
+#pragma unroll 1
   for (int r = U.lane; r < R; r += 32) {
     RepState s;
     memset(&s, 0, sizeof s);
@@ -698,6 +704,7 @@ __device__ void run_unit(Unit& U) {
         }
       }
     } else
+#pragma unroll 1
     for (int r0 = 0; r0 < R; r0 += 32) {
       const int r = r0 + U.lane;
       double t = INFINITY;
@@ -745,6 +752,7 @@ __device__ void run_unit(Unit& U) {
       } else if (c.routing == SSG_ROUTE_LO) {
         // argmin outstanding, ties to the lowest index
         int64_t key = INT64_MAX;
+#pragma unroll 1
         for (int r0 = 0; r0 < R; r0 += 32) {
           const int r = r0 + U.lane;
           int64_t k2 = r < R ? (((int64_t)U.reps[r].outstanding) << 16 | r) : INT64_MAX;
@@ -854,6 +862,7 @@ __device__ void run_unit(Unit& U) {
   if (!failed(U) && !U.out->aborted) {
     // "simulation drained with unfinished request" (sim.hpp:305-306)
     int32_t first_bad = INT32_MAX;
+#pragma unroll 1
     for (int32_t j = U.lane; j < u.n; j += 32) {
       const ReqHot h = U.hot[j];
       if (h.emitted < h.decode && j < first_bad) first_bad = j;

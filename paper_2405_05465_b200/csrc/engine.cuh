@@ -170,6 +170,7 @@ __device__ __forceinline__ void ring_shift(Unit& U, int32_t* a, int32_t mask, in
   const int n = hi - lo;
   if (n <= 0) return;
   if (delta < 0) {
+#pragma unroll 1
     for (int c = 0; c < n; c += 32) {
       const int p = lo + c + U.lane;
       int32_t v = 0;
@@ -179,6 +180,7 @@ __device__ __forceinline__ void ring_shift(Unit& U, int32_t* a, int32_t mask, in
       __syncwarp();
     }
   } else {
+#pragma unroll 1
     for (int c = n; c > 0; c -= 32) {
       const int p = lo + c - 1 - U.lane;
       int32_t v = 0;
@@ -462,6 +464,7 @@ static __device__ void schedule_decodes(Unit& U, RepState& S, int r, int32_t max
 #define PRED_PREFILL_LEFT 0
 __device__ SSG_WARM int32_t next_running(Unit& U, const RepState& S, int r, int32_t i, int pred) {
   const int32_t* a = RUN(U, r);
+#pragma unroll 1
   for (; i < S.run_n; i += 32) {
     const int32_t p = i + U.lane;
     bool hit = false;
@@ -576,6 +579,7 @@ __device__ SSG_COLD void schedule_ft(Unit& U, RepState& S, int r) {
   }
   // ... then every unfinished member decodes in lockstep (order = running order)
   const int32_t* a = RUN(U, r);
+#pragma unroll 1
   for (int32_t base = 0; base < S.run_n; base += 32) {
     const int32_t p = base + U.lane;
     bool live = false;
@@ -655,6 +659,7 @@ static __device__ void complete_batch(Unit& U, RepState& S, int r) {
   const bool emit_times = (U.u->flags & SSG_UF_EMISSIONS) != 0;
   int newly_finished = 0;
   bool bad = false;
+#pragma unroll 1
   for (int32_t k = U.lane; k < np + nd; k += 32) {
     int32_t j;
     bool emit;
@@ -702,6 +707,7 @@ static __device__ void complete_batch(Unit& U, RepState& S, int r) {
   int32_t write = 0;
   int64_t freed = 0;
   bool any_unfinished = false;
+#pragma unroll 1
   for (int32_t base = 0; base < S.run_n; base += 32) {
     const int32_t p = base + U.lane;
     int32_t j = -1;
@@ -909,6 +915,7 @@ __device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, doubl
     // with pp | 32 lane l only sees entries of microbatch l mod pp, so one pass
     // and a reduction over the lanes sharing l mod pp give every microbatch
     int64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0;
+#pragma unroll 1
     for (int32_t k = U.lane; k < total; k += 32) accumulate(k, a0, a1, a2, a3, a4, a5);
     // 32-lane sums of values below 2^26 fit in 31 bits: one REDUX each
     const bool small = ((a1 | a2 | a3 | a5) >> 26) == 0;
