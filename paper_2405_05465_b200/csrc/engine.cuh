@@ -497,35 +497,39 @@ __device__ SSG_WARM void schedule_chunked(Unit& U, RepState& S, int r) {
   int32_t budget = sar ? c.chunk : c.max_tokens;
   bool decodes = true;
 #pragma unroll 1
-  for (int ph = 0; ph < 3; ++ph) {
-    // 0 = decodes, 1 = in-flight chunks, 2 = admission, 3 = nothing
-    const int what = sar ? ph : (ph == 0 ? 2 : (ph == 1 ? 0 : 3));
-    if (what == 0) {
+  for (int ph = 0; ph < 2; ++ph) {
+    if (ph == (sar ? 0 : 1)) {
       if (decodes) schedule_decodes(U, S, r, c.max_batch, vl ? nullptr : &budget);
-    } else if (what == 1) {
-      // in-flight chunks in running order; a 32-entry window is scanned at once
-      // and only the requests with prefill left are visited one by one
-      for (int32_t i = 0; i < S.run_n;) {
-        if (budget < 1 || S.np + S.nd >= c.max_batch) break;
-        const int32_t k = next_running(U, S, r, i, PRED_PREFILL_LEFT);
-        if (k >= S.run_n) break;
-        const int32_t j = RUN(U, r)[k];
+      continue;
+    }
+    // prefills: Sarathi first continues in-flight chunks in running order (a
+    // 32-entry window is scanned at once; only requests with prefill left are
+    // visited), then every policy admits waiting heads -- one reservation site
+    bool inflight = sar;
+    int32_t i = 0;
+#pragma unroll 1
+    while (true) {
+      int32_t j, chunk, prior = 0, t = 0;
+      bool alone = false;
+      if (inflight) {
+        int32_t k = S.run_n;
+        if (budget >= 1 && S.np + S.nd < c.max_batch) k = next_running(U, S, r, i, PRED_PREFILL_LEFT);
+        if (k >= S.run_n) {
+          inflight = false;
+          continue;
+        }
+        j = RUN(U, r)[k];
         const ReqHot h = U.hot[j];
         const int32_t rem = h.target - h.done;
-        const int32_t chunk = budget < rem ? budget : rem;
-        if (!admit_reserve(U, S, r, j, (int64_t)h.done + chunk, false, false)) break;
-        mark_scheduled(U, j);
-        push_prefill(U, S, r, j, chunk, h.done);
-        budget -= chunk;
+        chunk = budget < rem ? budget : rem;
+        prior = h.done;
         i = k + 1;
-      }
-    } else if (what == 2) {
-      while (S.wait_n > 0 && S.run_n < c.max_batch) {
+      } else {
+        if (!(S.wait_n > 0 && S.run_n < c.max_batch)) break;
         if (sar && !(budget > 0 && S.np + S.nd < c.max_batch)) break;
-        const int32_t head = wait_front(U, S, r);
-        const int32_t t = U.hot[head].target;
-        int32_t chunk = t;
-        bool alone = false;
+        j = wait_front(U, S, r);
+        t = U.hot[j].target;
+        chunk = t;
         if (sar) {
           chunk = budget < t ? budget : t;
         } else {
@@ -533,21 +537,33 @@ __device__ SSG_WARM void schedule_chunked(Unit& U, RepState& S, int r) {
           if (alone && S.np > 0) break;
           if (!alone && t > budget) break;
         }
-        if (!admit_reserve(U, S, r, head, chunk, vl, true)) break;
-        wait_erase(U, S, r, head);
-        run_insert(U, S, r, head);
-        mark_scheduled(U, head);
-        push_prefill(U, S, r, head, chunk, 0);
-        budget -= sar ? chunk : (t < budget ? t : budget);
-        if (alone) {
-          decodes = false;
-          break;
-        }
-        if (!sar && budget == 0) break;
       }
-      __syncwarp();
-      if (vl && S.np > 0) decodes = false;
+      // in-flight chunks: no watermark, no preemption; admissions: watermark,
+      // preemption for vLLM only (scheduler.hpp:302-316)
+      if (!admit_reserve(U, S, r, j, (int64_t)prior + chunk, !inflight && vl, !inflight)) {
+        if (!inflight) break;
+        inflight = false;
+        continue;
+      }
+      if (!inflight) {
+        wait_erase(U, S, r, j);
+        run_insert(U, S, r, j);
+      }
+      mark_scheduled(U, j);
+      push_prefill(U, S, r, j, chunk, prior);
+      if (inflight) {
+        budget -= chunk;
+        continue;
+      }
+      budget -= sar ? chunk : (t < budget ? t : budget);
+      if (alone) {
+        decodes = false;
+        break;
+      }
+      if (!sar && budget == 0) break;
     }
+    __syncwarp();
+    if (vl && S.np > 0) decodes = false;
   }
   __syncwarp();
 }
