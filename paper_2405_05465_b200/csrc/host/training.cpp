@@ -11,13 +11,13 @@
 #include <algorithm>
 #include <cstdlib>
 #include <exception>
-#include <thread>
 #include <cmath>
 #include <random>
 
 #include "json.hpp"
 #include "runtime.h"
 #include "servesim_b200.hpp"
+#include "train.h"
 
 namespace servesim {
 
@@ -371,185 +371,6 @@ RegressorData fit_interp(const Rows& x, const std::vector<double>& y) {  // regr
   return g;
 }
 
-// Least squares plane of a leaf: normal equations + ridge 1e-9, Gaussian
-// elimination with partial pivoting (regressor.hpp:42-67, 234-254).
-std::vector<double> fit_plane(const Rows& x, const std::vector<double>& y,
-                              const std::vector<std::size_t>& idx, std::size_t nf) {
-  const std::size_t n = nf + 1;
-  std::vector<double> a(n * n, 0.0), b(n, 0.0);
-  std::vector<double> row(n);
-  for (auto i : idx) {
-    row[0] = 1.0;
-    for (std::size_t f = 0; f < nf; ++f) row[f + 1] = x[i][f];
-    for (std::size_t r = 0; r < n; ++r) {
-      b[r] += row[r] * y[i];
-      for (std::size_t c = 0; c < n; ++c) a[r * n + c] += row[r] * row[c];
-    }
-  }
-  for (std::size_t i = 0; i < n; ++i) a[i * n + i] += 1e-9;
-  bool ok = true;
-  for (std::size_t col = 0; col < n && ok; ++col) {
-    std::size_t piv = col;
-    for (std::size_t r = col + 1; r < n; ++r)
-      if (std::fabs(a[r * n + col]) > std::fabs(a[piv * n + col])) piv = r;
-    if (std::fabs(a[piv * n + col]) < 1e-30) {
-      ok = false;
-      break;
-    }
-    if (piv != col) {
-      for (std::size_t c = 0; c < n; ++c) std::swap(a[piv * n + c], a[col * n + c]);
-      std::swap(b[piv], b[col]);
-    }
-    for (std::size_t r = col + 1; r < n; ++r) {
-      const double m = a[r * n + col] / a[col * n + col];
-      for (std::size_t c = col; c < n; ++c) a[r * n + c] -= m * a[col * n + c];
-      b[r] -= m * b[col];
-    }
-  }
-  std::vector<double> w(n, 0.0);
-  if (ok) {
-    for (std::size_t i = n; i-- > 0;) {
-      double s = b[i];
-      for (std::size_t c = i + 1; c < n; ++c) s -= a[i * n + c] * w[c];
-      w[i] = s / a[i * n + i];
-    }
-    return w;
-  }
-  double m = 0.0;
-  for (auto i : idx) m += y[i];
-  w[0] = m / static_cast<double>(idx.size());
-  return w;
-}
-
-struct ForestBuilder {
-  const Rows& x;
-  const std::vector<double>& y;
-  const ForestConfig& cfg;
-  std::size_t nf;
-  std::size_t min_leaf;
-
-  int grow(ForestTree& t, const std::vector<std::size_t>& idx, int depth, std::mt19937_64& rng) {
-    const int node = static_cast<int>(t.feature.size());
-    t.feature.push_back(0);
-    t.threshold.push_back(0.0);
-    t.left.push_back(-1);
-    t.right.push_back(-1);
-    int split_f = -1;
-    double split_th = 0.0;
-    if (depth < cfg.max_depth && idx.size() >= 2 * min_leaf) pick_split(idx, rng, split_f, split_th);
-    if (split_f < 0) {
-      t.feature[node] = -static_cast<int>(t.leaf_weights.size()) - 1;
-      t.leaf_weights.push_back(fit_plane(x, y, idx, nf));
-      return node;
-    }
-    std::vector<std::size_t> lo_side, hi_side;
-    for (auto i : idx) (x[i][split_f] <= split_th ? lo_side : hi_side).push_back(i);
-    t.feature[node] = split_f;
-    t.threshold[node] = split_th;
-    const int l = grow(t, lo_side, depth + 1, rng);
-    t.left[node] = l;
-    const int r = grow(t, hi_side, depth + 1, rng);
-    t.right[node] = r;
-    return node;
-  }
-
-  // Random thresholds per feature, best variance-reduction surrogate wins
-  // (regressor.hpp:193-232).
-  void pick_split(const std::vector<std::size_t>& idx, std::mt19937_64& rng, int& best_f,
-                  double& best_th) const {
-    double best = -1.0;
-    const std::size_t n = idx.size();
-    double total = 0.0;
-    for (auto i : idx) total += y[i];
-    std::uniform_real_distribution<double> unit(0.0, 1.0);
-    for (std::size_t f = 0; f < nf; ++f) {
-      double lo = x[idx[0]][f], hi = lo;
-      for (auto i : idx) {
-        lo = std::min(lo, x[i][f]);
-        hi = std::max(hi, x[i][f]);
-      }
-      if (lo == hi) continue;
-      for (int k = 0; k < cfg.threshold_draws; ++k) {
-        const double th = lo + (hi - lo) * unit(rng);
-        std::size_t nl = 0;
-        double ls = 0.0;
-        for (auto i : idx)
-          if (x[i][f] <= th) {
-            ++nl;
-            ls += y[i];
-          }
-        const std::size_t nr = n - nl;
-        if (nl < min_leaf || nr < min_leaf) continue;
-        const double score = ls * ls / static_cast<double>(nl) +
-                             (total - ls) * (total - ls) / static_cast<double>(nr);
-        if (score > best + 1e-15) {
-          best = score;
-          best_f = static_cast<int>(f);
-          best_th = th;
-        }
-      }
-    }
-  }
-};
-
-RegressorData fit_forest(const Rows& x, const std::vector<double>& y, const ForestConfig& cfg) {
-  ssg::PhaseTimer timer("train: fit_forest");
-  require(!x.empty() && x.size() == y.size(), "forest train: empty or mismatched data");
-  RegressorData f;
-  f.type = "forest";
-  f.num_features = x.front().size();
-  f.y_lo = *std::min_element(y.begin(), y.end());
-  f.y_hi = *std::max_element(y.begin(), y.end());
-  const double pad = 0.1 * (f.y_hi - f.y_lo);
-  f.y_lo -= pad;
-  f.y_hi += pad;
-  std::size_t min_leaf = cfg.min_samples_leaf > 0 ? static_cast<std::size_t>(cfg.min_samples_leaf)
-                         : f.num_features <= 1    ? 2
-                                                  : f.num_features + 2;
-  std::vector<std::size_t> all(x.size());
-  for (std::size_t i = 0; i < all.size(); ++i) all[i] = i;
-  // Every tree draws from its own mt19937_64 seeded by (seed, t)
-  // (regressor.hpp:93-96), so trees are independent: grow them on host
-  // threads, each into its own slot -- the forest is the same for any thread count.
-  const int nt = cfg.num_trees;
-  f.trees.resize(static_cast<std::size_t>(std::max(0, nt)));
-  auto grow_range = [&](int t0, int t1) {
-    ForestBuilder fb{x, y, cfg, f.num_features, min_leaf};
-    for (int t = t0; t < t1; ++t) {
-      std::mt19937_64 rng(cfg.seed * 0x9e3779b97f4a7c15ULL + static_cast<std::uint64_t>(t) + 1);
-      fb.grow(f.trees[static_cast<std::size_t>(t)], all, 0, rng);
-    }
-  };
-  const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
-  int workers = std::max(1, std::min({nt, hw, 16}));
-  if (const char* e = std::getenv("SSG_TRAIN_THREADS")) workers = std::max(1, std::min(nt, std::atoi(e)));
-  if (workers <= 1) {
-    grow_range(0, nt);
-  } else {
-    std::vector<std::thread> pool;
-    std::vector<std::exception_ptr> err(static_cast<std::size_t>(workers));
-    for (int w = 0; w < workers; ++w)
-      pool.emplace_back([&, w] {
-        try {
-          grow_range(nt * w / workers, nt * (w + 1) / workers);
-        } catch (...) {
-          err[static_cast<std::size_t>(w)] = std::current_exception();
-        }
-      });
-    for (auto& th : pool) th.join();
-    for (auto& e : err)
-      if (e) std::rethrow_exception(e);
-  }
-  return f;
-}
-
-RegressorData fit(const std::string& kind, const Rows& x, const std::vector<double>& y,
-                  const ForestConfig& fc) {
-  if (kind == "forest") return fit_forest(x, y, fc);
-  if (kind == "interp") return fit_interp(x, y);
-  throw Error("train: unknown regressor kind '" + kind + "'");
-}
-
 // Host evaluation used only for the training-time hold-out score (estimator.hpp:261-270);
 // every runtime query goes through the device kernels.
 double host_regress(const RegressorData& r, const std::vector<double>& x) {
@@ -575,21 +396,32 @@ EstimatorModel train(const std::vector<ProfileRecord>& records, const TrainConfi
     groups[{r.op, static_cast<std::int64_t>(it->second)}].push_back(&r);
   }
   require(!groups.empty(), "train: no records");
-  EstimatorModel model;
+  const bool forest = cfg.regressor == "forest";
+  // per (op, tp): transformed rows (x = log1p(feature), y = log(runtime)) and
+  // the hold-out split (estimator.hpp:201-275); fitting happens afterwards
+  struct Group {
+    OpModelKey key;
+    EstimatorModel::PerOpModel m;
+    Rows x, xt;
+    std::vector<double> y, yt;
+    std::vector<std::size_t> held;
+    ForestConfig fc;
+  };
+  std::vector<Group> todo;
   std::uint64_t group_index = 0;
   for (const auto& [key, recs] : groups) {
     require(recs.size() >= cfg.min_points_per_op,
             "train: op " + to_string(key) + " has only " + std::to_string(recs.size()) +
                 " points (need " + std::to_string(cfg.min_points_per_op) + ")");
-    EstimatorModel::PerOpModel m;
+    Group G;
+    G.key = key;
+    EstimatorModel::PerOpModel& m = G.m;
     m.schema = feature_schema(triage(key.op));
     m.n_points = recs.size();
     const std::size_t nf = m.schema.size();
     m.levels.assign(nf, {});
     m.bbox_lo.assign(nf, 0.0);
     m.bbox_hi.assign(nf, 0.0);
-    Rows x;
-    std::vector<double> y;
     for (const auto* r : recs) {
       std::vector<double> row(nf);
       for (std::size_t f = 0; f < nf; ++f) {
@@ -599,8 +431,8 @@ EstimatorModel train(const std::vector<ProfileRecord>& records, const TrainConfi
         row[f] = std::log1p(it->second);
         m.levels[f].push_back(it->second);
       }
-      x.push_back(std::move(row));
-      y.push_back(std::log(r->runtime));
+      G.x.push_back(std::move(row));
+      G.y.push_back(std::log(r->runtime));
     }
     for (std::size_t f = 0; f < nf; ++f) {
       auto& lv = m.levels[f];
@@ -609,37 +441,55 @@ EstimatorModel train(const std::vector<ProfileRecord>& records, const TrainConfi
       m.bbox_lo[f] = lv.front();
       m.bbox_hi[f] = lv.back();
     }
-    ForestConfig fc = cfg.forest;
-    fc.seed = cfg.seed * 1000003ULL + group_index++;
-    Rows xt;
-    std::vector<double> yt;
-    std::vector<std::size_t> held;
-    const bool can_hold = x.size() >= 2 * cfg.min_points_per_op;
-    for (std::size_t i = 0; i < x.size(); ++i) {
+    G.fc = cfg.forest;
+    G.fc.seed = cfg.seed * 1000003ULL + group_index++;
+    const bool can_hold = G.x.size() >= 2 * cfg.min_points_per_op;
+    for (std::size_t i = 0; i < G.x.size(); ++i) {
       if (can_hold && i % 5 == 2) {
-        held.push_back(i);
+        G.held.push_back(i);
       } else {
-        xt.push_back(x[i]);
-        yt.push_back(y[i]);
+        G.xt.push_back(G.x[i]);
+        G.yt.push_back(G.y[i]);
       }
     }
-    if (!held.empty() && cfg.regressor == "forest") {
-      RegressorData probe = fit(cfg.regressor, xt, yt, fc);
-      double ape = 0.0;
-      for (auto i : held) {
-        const double pred = std::exp(host_regress(probe, x[i]));
-        const double truth = std::exp(y[i]);
-        ape += std::fabs(pred - truth) / truth;
-      }
-      m.holdout_mape = ape / static_cast<double>(held.size());
+    if (!forest) {
+      // the interpolator is a grid reshape (host); its errors surface in group order
+      if (cfg.regressor != "interp") throw Error("train: unknown regressor kind '" + cfg.regressor + "'");
+      m.regressor = std::make_unique<GridInterpolator>(fit_interp(G.x, G.y));
     }
-    RegressorData fitted = fit(cfg.regressor, x, y, fc);
-    if (fitted.type == "forest")
-      m.regressor = std::make_unique<ForestRegressor>(std::move(fitted));
-    else
-      m.regressor = std::make_unique<GridInterpolator>(std::move(fitted));
-    model.insert(key, std::move(m));
+    todo.push_back(std::move(G));
   }
+  if (forest) {
+    // every forest of the call -- hold-out probes and final models -- grows in
+    // one device launch, one warp per tree (train.cu)
+    std::vector<ssg::ForestFit> fits;
+    std::vector<std::pair<std::size_t, bool>> what;  // (group, is hold-out probe)
+    for (std::size_t g = 0; g < todo.size(); ++g) {
+      if (!todo[g].held.empty()) {
+        fits.push_back({&todo[g].xt, &todo[g].yt, todo[g].fc});
+        what.push_back({g, true});
+      }
+      fits.push_back({&todo[g].x, &todo[g].y, todo[g].fc});
+      what.push_back({g, false});
+    }
+    std::vector<RegressorData> grown = ssg::grow_forests(fits);
+    for (std::size_t k = 0; k < grown.size(); ++k) {
+      Group& G = todo[what[k].first];
+      if (what[k].second) {
+        double ape = 0.0;
+        for (auto i : G.held) {
+          const double pred = std::exp(host_regress(grown[k], G.x[i]));
+          const double truth = std::exp(G.y[i]);
+          ape += std::fabs(pred - truth) / truth;
+        }
+        G.m.holdout_mape = ape / static_cast<double>(G.held.size());
+      } else {
+        G.m.regressor = std::make_unique<ForestRegressor>(std::move(grown[k]));
+      }
+    }
+  }
+  EstimatorModel model;
+  for (auto& G : todo) model.insert(G.key, std::move(G.m));
   return model;
 }
 
@@ -715,7 +565,7 @@ GridInterpolator::GridInterpolator(RegressorData d) : Regressor(std::move(d)) {
 }
 ForestRegressor ForestRegressor::train(const std::vector<std::vector<double>>& x,
                                        const std::vector<double>& y, const ForestConfig& cfg) {
-  return ForestRegressor(fit_forest(x, y, cfg));
+  return ForestRegressor(std::move(ssg::grow_forests({{&x, &y, cfg}}).at(0)));  // on the GPU
 }
 ForestRegressor ForestRegressor::from_json(const json& j) {
   require(j.at("type").get<std::string>() == "forest", "forest model: wrong type");

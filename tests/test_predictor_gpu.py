@@ -133,3 +133,39 @@ def test_predict_mixed_chunked_pinned(ssg, ref):
     slots_p[i + 5] = slots[i + 5]
     with pytest.raises(ssg.InputError, match="two-feature models need f1"):
         mine.predict_mixed(slots_p, f0, None, out=out)
+
+
+@pytest.mark.parametrize("model,dev,tps,seed", [
+    ("llama2_7b", "a100_80g", [1], 42),          # the golden case small_forest
+    ("llama2_70b", "h100_80g", [4], 3),          # cfg #3's estimator
+    ("internlm_20b", "h100_80g", [1, 2], 21),
+    ("qwen_72b", "a100_80g", [1, 2, 4], 7),
+])
+def test_device_forest_training_matches_reference(ssg, ref, model, dev, tps, seed):
+    """(f)3: every forest -- hold-out probes and final models -- grows on the
+    GPU (train.cu, one warp per tree) and the estimator JSON equals the
+    reference's train() byte for byte (regressor.hpp:82-254, estimator.hpp:201-275)."""
+    spec, device = catalog.MODELS[model], catalog.DEVICES[dev]
+    want = ref.train(spec, device, tps, "forest", seed)
+    got = ssg.Estimator.train(spec, device, tps, "forest", seed=seed).to_json()
+    assert got == want
+
+
+def test_device_forest_training_golden_sha():
+    """The forest cases of tests/golden (reference estimator sha256) reproduced by the GPU trainer."""
+    import hashlib
+    import json
+    import os
+
+    import paper_2405_05465_b200 as ssg
+
+    ssg.init(0)
+    gdir = os.path.join(os.path.dirname(__file__), "golden")
+    meta = json.load(open(os.path.join(gdir, "predict_golden.json")))
+    data = np.load(os.path.join(gdir, "predict_golden.npz"))
+    for case in meta["cases"]:
+        if case["regressor"] != "forest":
+            continue
+        text = ssg.Estimator.train(case["spec"], case["device"], case["tps"], "forest",
+                                   case["seed"]).to_json()
+        assert hashlib.sha256(text.encode()).digest() == bytes(data[case["name"] + "__est_sha"])
