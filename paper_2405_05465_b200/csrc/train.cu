@@ -71,7 +71,7 @@ __device__ __forceinline__ uint64_t mt_next(TreeSmem& g) {
   }
   uint64_t z = g.mt[g.mti++];
   z ^= (z >> 29) & 0x5555555555555555ULL;
-  z ^= (z << 17) & 0x71d67fffeb88c000ULL;
+  z ^= (z << 17) & 0x71d67fffeda60000ULL;
   z ^= (z << 37) & 0xfff7eee000000000ULL;
   z ^= (z >> 43);
   return z;
