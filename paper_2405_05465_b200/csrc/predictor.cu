@@ -314,6 +314,21 @@ void upload_pools(DeviceEstimator& d, std::vector<double>& dpool, std::vector<Ss
   d.view.models = d.models.ptr;
   d.view.dpool = d.dpool.ptr;
   d.view.nodes = d.nodes.ptr;
+#if SSG_FOREST_SOA
+  {
+    std::vector<double> a(nodes.size());
+    std::vector<int2> fr(nodes.size());
+    for (std::size_t i = 0; i < nodes.size(); ++i) {
+      a[i] = nodes[i].a;
+      fr[i] = make_int2(nodes[i].feat, nodes[i].right);
+    }
+    d.node_a.upload(a, ctx.stream);
+    d.node_fr.upload(fr, ctx.stream);
+    ssg::cuda_check(cudaStreamSynchronize(ctx.stream), "SoA upload");
+    d.view.node_a = d.node_a.ptr;
+    d.view.node_fr = d.node_fr.ptr;
+  }
+#endif
   d.view.roots = d.roots.ptr;
   d.view.nmodels = static_cast<int32_t>(d.host_models.size());
   d.view.math_fma = ctx.math_fma;

@@ -32,6 +32,21 @@ __device__ __forceinline__ int32_t ssg_node_right(double2 n) {
   return (int32_t)((unsigned long long)__double_as_longlong(n.y) >> 32);
 }
 
+#ifndef SSG_FOREST_SOA
+#define SSG_FOREST_SOA 0  // 1: walk SoA node arrays (two 8 B loads per node) -- A/B build only
+#endif
+// One node (or a leaf's weight tail) of the forest pool.
+__device__ __forceinline__ double2 ssg_ld_node_v(const SsgEstView& E, int32_t i) {
+#if SSG_FOREST_SOA
+  const double a = __ldg(E.node_a + i);
+  const int2 fr = __ldg(E.node_fr + i);
+  return make_double2(a, __longlong_as_double((long long)(((unsigned long long)(unsigned)fr.y << 32) |
+                                                          (unsigned)fr.x)));
+#else
+  return ssg_ld_node(E.nodes, i);
+#endif
+}
+
 // Cell of one axis: lo index and clamped fraction (regressor.hpp:314-325).
 __device__ __forceinline__ void ssg_axis_cell(const double* __restrict__ ax, int32_t n, double x,
                                               int32_t* lo, double* frac) {
@@ -122,7 +137,6 @@ __device__ __forceinline__ double ssg_interp(const SsgEstView& E, const SsgModel
 __device__ __forceinline__ double ssg_forest(const SsgEstView& E, const SsgModelDesc& m,
                                              double x0, double x1) {
   const int32_t* roots = E.roots + m.roots_off;
-  const SsgNode* nodes = E.nodes;
   const int nt = m.ntrees;
   double sum = 0.0;
   for (int t0 = 0; t0 < nt; t0 += FOREST_ILP) {
@@ -131,7 +145,7 @@ __device__ __forceinline__ double ssg_forest(const SsgEstView& E, const SsgModel
 #pragma unroll
     for (int g = 0; g < FOREST_ILP; ++g) {
       idx[g] = (t0 + g < nt) ? __ldg(roots + t0 + g) : -1;
-      nd[g] = idx[g] >= 0 ? ssg_ld_node(nodes, idx[g]) : make_double2(0.0, __longlong_as_double(-1ll));
+      nd[g] = idx[g] >= 0 ? ssg_ld_node_v(E, idx[g]) : make_double2(0.0, __longlong_as_double(-1ll));
     }
     bool walking = true;
     while (walking) {
@@ -142,7 +156,7 @@ __device__ __forceinline__ double ssg_forest(const SsgEstView& E, const SsgModel
         if (feat >= 0) {
           const double xf = feat ? x1 : x0;
           idx[g] = (xf <= nd[g].x) ? idx[g] + 1 : ssg_node_right(nd[g]);
-          nd[g] = ssg_ld_node(nodes, idx[g]);
+          nd[g] = ssg_ld_node_v(E, idx[g]);
           walking = true;
         }
       }
@@ -150,7 +164,7 @@ __device__ __forceinline__ double ssg_forest(const SsgEstView& E, const SsgModel
 #pragma unroll
     for (int g = 0; g < FOREST_ILP; ++g) {
       if (t0 + g < nt) {
-        const double2 w12 = ssg_ld_node(nodes, idx[g] + 1);
+        const double2 w12 = ssg_ld_node_v(E, idx[g] + 1);
         double v = __dadd_rn(nd[g].x, __dmul_rn(w12.x, x0));
         if (m.nf > 1) v = __dadd_rn(v, __dmul_rn(w12.y, x1));
         sum = __dadd_rn(sum, ssg_clamp(v, m.y_lo, m.y_hi));

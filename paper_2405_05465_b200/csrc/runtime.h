@@ -201,6 +201,8 @@ struct DeviceEstimator {
   ssg::DeviceBuffer<double> dpool;
   ssg::DeviceBuffer<SsgNode> nodes;
   ssg::DeviceBuffer<int32_t> roots;
+  ssg::DeviceBuffer<double> node_a;  // SoA mirror (SSG_FOREST_SOA A/B builds)
+  ssg::DeviceBuffer<int2> node_fr;
   std::vector<SsgModelDesc> host_models;
   std::map<OpModelKey, int32_t> index;  // (op, tp) -> model slot
   std::vector<int64_t> qbytes;          // algorithmic bytes of one query per slot

@@ -4,6 +4,7 @@
 // pointers, no C++ containers.  Offsets are element offsets into the pools.
 #pragma once
 #include <stdint.h>
+#include <vector_types.h>
 
 #define SSG_KIND_INTERP 0
 #define SSG_KIND_FOREST 1
@@ -49,6 +50,8 @@ struct SsgEstView {
   const double* dpool;
   const SsgNode* nodes;
   const int32_t* roots;
+  const double* node_a;    // SoA mirror of nodes (SSG_FOREST_SOA builds only): threshold / w
+  const int2* node_fr;     //   and (feature, right) -- A/B of the north-star layout
   int32_t nmodels;
   int32_t math_fma;  // SSG_MATH_FMA / SSG_MATH_PLAIN: which glibc contraction the host uses
 };
