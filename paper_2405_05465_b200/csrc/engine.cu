@@ -375,6 +375,7 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
     const bool active = k < max_iters;
     // ---- schedule: every runner reserves kv+k+1 tokens (no preemption allowed)
     int64_t need = 0;
+#pragma unroll 1
     for (int r = 0; r < nd; ++r) {
       const int32_t kv_r = __shfl_sync(SSG_FULL, kv, r);
       const int32_t held_r = __shfl_sync(SSG_FULL, held, r);
@@ -387,13 +388,16 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
       need += s > 0 ? s : 0;
     }
     // ---- cost: decode attention per microbatch, operator order, makespan
+    // one rolled pass over the microbatches: the attention query (log1p, cell,
+    // interpolation, exp) is emitted once, not once per microbatch slot
     double tim[SSG_FF_MAX_PP];
     double fl_tot = 0.0;
     int good = 1;
 #pragma unroll
-    for (int m = 0; m < SSG_FF_MAX_PP; ++m) {
-      tim[m] = 0.0;
-      if (m < nm) {
+    for (int m = 0; m < SSG_FF_MAX_PP; ++m) tim[m] = 0.0;
+#pragma unroll 1
+    for (int m = 0; m < nm; ++m) {
+      {
         const int64_t cm0 = __shfl_sync(SSG_FULL, ctx_m, m);
         const int ndm = __shfl_sync(SSG_FULL, nd_m, m);
         const int32_t lo0m = __shfl_sync(SSG_FULL, lo0, m);
@@ -448,21 +452,17 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
       double fin[SSG_FF_MAX_PP];
 #pragma unroll
       for (int m = 0; m < SSG_FF_MAX_PP; ++m) fin[m] = 0.0;
+#pragma unroll 1
       for (int st = 0; st < pp; ++st) {
         double prev = 0.0;
-#pragma unroll
-        for (int m = 0; m < SSG_FF_MAX_PP; ++m) {
-          if (m < nm) {
-            const double start = fin[m] < prev ? prev : fin[m];
-            prev = __dadd_rn(start, tim[m]);
-            fin[m] = prev;
-          }
+#pragma unroll 1
+        for (int m = 0; m < nm; ++m) {
+          const double start = fin[m] < prev ? prev : fin[m];
+          prev = __dadd_rn(start, tim[m]);
+          fin[m] = prev;
         }
       }
-      lat = 0.0;
-#pragma unroll
-      for (int m = 0; m < SSG_FF_MAX_PP; ++m)
-        if (m == nm - 1) lat = fin[m];
+      lat = fin[nm - 1];
     }
     lat = __dadd_rn(lat, c.cpu_overhead);
     // ---- the order-dependent parts, in iteration order
@@ -545,6 +545,7 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
       // batch start clock of iteration i = completion of iteration i-1
       const double t_prev = __shfl_up_sync(SSG_FULL, t_done, 1);
       if (lane < fit) U.log[used + lane * need_w + 1] = __double_as_longlong(lane == 0 ? U.clock : t_prev);
+#pragma unroll 1
       for (int r = 0; r < nd; ++r) {
         const int64_t id_r = U.ids[__shfl_sync(SSG_FULL, j, r)];
         const int32_t kv_r = __shfl_sync(SSG_FULL, kv, r);
@@ -558,6 +559,7 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
       wput(U, &U.out->log_used, used >= 0 && fit == K ? used + K * need_w : (int64_t)-1);
     }
     if (emit_times) {
+#pragma unroll 1
       for (int r = 0; r < nd; ++r) {
         const int64_t e = __shfl_sync(SSG_FULL, ebase, r);
         if (lane < K) U.emissions[e + k] = t_done;
