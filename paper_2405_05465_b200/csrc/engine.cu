@@ -334,7 +334,7 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
   // per-microbatch invariants on lane m < nm: size, context sum, decode model cell
   const SimOp& od = c.ops[c.idx_dec];
   const SsgModelDesc& md = U.E.models[od.slot];
-  if (md.kind != SSG_KIND_INTERP) return 0;
+  if (md.kind != SSG_KIND_INTERP || !c.tab_cells) return 0;
   const int my_m = lane % pp;
   int64_t ctx_m = 0;
   for (int m = 0; m < nm; ++m) {
@@ -356,7 +356,10 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
       if (k < c.ncomm) comm_sum[k] = tab[(int64_t)(2 + k) * T1 + nd_m];
     const double v0 = (double)nd_m;
     ok = v0 >= md.lower[0] && v0 <= md.upper[0];
-    ssg_axis_cell(U.E.dpool + md.axis_off[0], md.axis_len[0], ssg_log1p(v0, FMA), &lo0, &f0);
+    // the axis-0 cell at v0 = nd_m from the token tables (k_build_tables computes
+    // ssg_axis_cell(log1p(t)) with the same code; tab_cells is checked on entry)
+    f0 = tab[7LL * T1 + nd_m];
+    lo0 = (int32_t)tab[8LL * T1 + nd_m];
   }
   if (!__all_sync(SSG_FULL, ok)) { FFSTAT(11); return 0; }
   const int32_t n1 = md.axis_len[1];

@@ -132,12 +132,13 @@ __device__ __forceinline__ bool failed(Unit& U) { return U.out->code != SSG_OK; 
 
 // ---------------------------------------------------------------- blocks
 __device__ __forceinline__ int64_t units_for(const SimConfig& c, int64_t tokens) {
-  if (c.token_granular) return tokens;
-  const int64_t t = tokens + c.block_size - 1;  // ceil(tokens / block_size), tokens >= 0
-  // t < 2^32 (tokens < 2^31, block_size < 2^31, both checked on the host):
-  // floor(t / b) = mulhi(t, ceil(2^64 / b)) exactly; inlined at every
-  // block-accounting site, so no division sequence is
-  return c.bs_shift >= 0 ? (t >> c.bs_shift) : (int64_t)__umul64hi((uint64_t)t, c.bs_magic);
+  // ceil(tokens / block_size), tokens >= 0, as one 64-bit multiply-high of
+  // tokens + block_size - 1 by bs_magic (block_magic, sim_device.h): exact for
+  // every power of two and for numerators below 2^32 otherwise (tokens < 2^31,
+  // block_size < 2^31, both checked on the host).  bs_magic == 0: one unit per
+  // token (LightLLM, or block_size 1).  A single branch-free form keeps the
+  // dozen inlined block-accounting sites small (the kernel is fetch bound).
+  return c.bs_magic ? (int64_t)__umul64hi((uint64_t)(tokens + c.block_size - 1), c.bs_magic) : tokens;
 }
 __device__ __forceinline__ int64_t shortfall_held(const SimConfig& c, int32_t held, int64_t tokens) {
   int64_t s = units_for(c, tokens) - (int64_t)held;

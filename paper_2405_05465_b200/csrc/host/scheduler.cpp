@@ -64,10 +64,7 @@ SimConfig sched_config(const PolicyConfig& p, const MemoryPlan& m) {
   c.bs_shift = -1;
   for (int k = 0; k < 62; ++k)
     if ((int64_t(1) << k) == m.block_size) c.bs_shift = k;
-  if (c.bs_shift < 0) {
-    const unsigned __int128 one = static_cast<unsigned __int128>(1) << 64;
-    c.bs_magic = static_cast<uint64_t>(one / static_cast<uint64_t>(m.block_size)) + 1;
-  }
+  c.bs_magic = block_magic(m.block_size, c.token_granular != 0);
   c.total_units = c.token_granular ? m.kv_capacity_tokens : m.num_blocks;
   c.watermark_units = c.token_granular ? m.watermark_blocks * m.block_size : m.watermark_blocks;
   c.tab_off = -1;

@@ -127,13 +127,9 @@ SimConfig make_sim_config(const ClusterConfig& cl, const EstimatorModel& est, in
     if ((int64_t(1) << k) == plan.block_size) c.bs_shift = k;
   // block counts on the device: token counts stay below 2^31 (request lengths
   // are checked), so ceil-division by a block size below 2^31 is one 64-bit
-  // high multiply by ceil(2^64 / block_size), exact for numerators below 2^32
+  // high multiply (block_magic), exact for numerators below 2^32
   require(plan.block_size < (int64_t(1) << 31), "ssg: block_size above the device engine limit");
-  c.bs_magic = 0;
-  if (c.bs_shift < 0) {
-    const unsigned __int128 one = static_cast<unsigned __int128>(1) << 64;
-    c.bs_magic = static_cast<uint64_t>(one / static_cast<uint64_t>(plan.block_size)) + 1;
-  }
+  c.bs_magic = block_magic(plan.block_size, c.token_granular != 0);
   c.total_units = c.token_granular ? plan.kv_capacity_tokens : plan.num_blocks;
   c.watermark_units = c.token_granular ? plan.watermark_blocks * plan.block_size : plan.watermark_blocks;
   c.cpu_overhead = cl.cpu_overhead_per_iter;

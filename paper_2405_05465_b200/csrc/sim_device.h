@@ -79,6 +79,21 @@ struct SimConfig {
   SimOp ops[SSG_MAX_OPS];
 };
 
+// Multiplier of the device's block count ceil(t / b) = mulhi(t + b - 1, magic)
+// (engine.cuh units_for): 0 for one unit per token (token-granular LightLLM, or
+// b = 1); 2^64 / b for a power of two (exact for every t); ceil(2^64 / b)
+// otherwise (exact for t + b - 1 < 2^32).  Host only.
+static inline uint64_t block_magic(int64_t block_size, bool token_granular) {
+  if (token_granular || block_size <= 1) return 0;
+  if ((block_size & (block_size - 1)) == 0) {
+    int k = 0;
+    while ((int64_t(1) << k) != block_size) ++k;
+    return uint64_t(1) << (64 - k);
+  }
+  const unsigned __int128 one = static_cast<unsigned __int128>(1) << 64;
+  return static_cast<uint64_t>(one / static_cast<uint64_t>(block_size)) + 1;
+}
+
 // Per-request hot state (32 B, one sector).  Indices are unit-local and
 // ordered by (arrival, id), so "sorted by arrival then id" (scheduler.hpp:236)
 // is plain integer order on the device.
