@@ -567,10 +567,17 @@ def main():
                           "alg_bytes_per_launch": alg_bytes / max(1, st["launches_simulate"]),
                           "alg_bytes_per_step": alg_bytes / a.steps,
                           "kernel_ms_per_step": st["simulate_busy_ms"] / a.steps,
-                          "kernel_share_of_step": (st["simulate_busy_ms"] / a.steps) / (t_step * 1e3)},
+                          "kernel_share_of_step": (st["simulate_busy_ms"] / a.steps) / (t_step * 1e3),
+                          # the same over the bytes of the work the sequential reference
+                          # search does (its asked probes + SLO runs; the rest is speculation)
+                          "useful_achieved": st["useful_bytes"] / sim_s / 1e9 if sim_s > 0 else 0.0,
+                          "useful_frac": (st["useful_bytes"] / sim_s / 1e9) / peak if sim_s > 0 and peak else None},
                          **profiled_traffic("k_simulate")),
         "gpu_launches": launches,
-        "work": {k: st[k] // a.steps for k in ("units", "iterations", "entries", "events")},
+        "work": dict({k: st[k] // a.steps for k in ("units", "iterations", "entries", "events",
+                                                     "useful_iterations", "useful_entries")},
+                     speculative_over_sequential_iterations=st["iterations"] / max(1, st["useful_iterations"]),
+                     speculative_over_sequential_entries=st["entries"] / max(1, st["useful_entries"])),
         "clocks": clk,
     }
     if rank == 0 and outcome is not None:

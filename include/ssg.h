@@ -212,6 +212,10 @@ typedef struct ssg_run_stats {
   int64_t launches_setup;  /* probe-stream setup and SLO sample kernels */
   double simulate_busy_ms; /* union of k_simulate intervals: sweep launches of candidate groups
                               overlap on separate streams, so this is <= simulate_ms */
+  /* the sweep work the sequential reference search would do: the probes its
+     find_capacity replay asks for plus each SLO / static run (the rest of
+     iterations / entries is speculation) */
+  int64_t useful_iterations, useful_entries, useful_bytes;
 } ssg_run_stats;
 void ssg_stats_reset(void);
 void ssg_stats_get(ssg_run_stats* out);

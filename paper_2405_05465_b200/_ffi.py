@@ -121,7 +121,8 @@ class RunStats(C.Structure):
         "launches_simulate", "launches_select", "launches_predict", "launches_batch", "units",
         "iterations", "entries", "events", "predictor_bytes", "entry_bytes", "queries")] + [
         ("simulate_ms", C.c_double), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
-        ("launches_setup", C.c_int64), ("simulate_busy_ms", C.c_double)]
+        ("launches_setup", C.c_int64), ("simulate_busy_ms", C.c_double),
+        ("useful_iterations", C.c_int64), ("useful_entries", C.c_int64), ("useful_bytes", C.c_int64)]
 
 
 def exported_symbols():

@@ -631,6 +631,9 @@ void ssg_stats_get(ssg_run_stats* out) {
   out->launches_setup = r.launches_setup;
   out->d2h_bytes = r.d2h_bytes;
   out->simulate_busy_ms = r.simulate_busy_ms;
+  out->useful_iterations = r.useful_iterations;
+  out->useful_entries = r.useful_entries;
+  out->useful_bytes = r.useful_bytes;
 }
 
 int ssg_search_finalize(const char* config_path, const ssg_config_record* records, size_t n,

@@ -42,6 +42,9 @@ void RunStats::add(const RunStats& o) {
   h2d_bytes += o.h2d_bytes;
   d2h_bytes += o.d2h_bytes;
   simulate_busy_ms += o.simulate_busy_ms;
+  useful_iterations += o.useful_iterations;
+  useful_entries += o.useful_entries;
+  useful_bytes += o.useful_bytes;
 }
 
 StatsScope::StatsScope() : prev(t_stats) { t_stats = &local; }

@@ -140,6 +140,9 @@ struct ProbeAnswer {
   bool feasible = false;
   bool error = false;
   SimUnitOut err{};  // the failing unit (error == true)
+  // device work of the probe's simulation (its units summed): the sequential
+  // search's share of the sweep is the work of the rates its replay asks for
+  int64_t iters = 0, entries = 0, bytes = 0;
 };
 using ProbeMemo = std::unordered_map<double, ProbeAnswer>;
 
@@ -147,13 +150,21 @@ struct ProbeError {
   SimUnitOut err;
 };
 
+void add_work(ProbeAnswer& a, const SimUnitOut& o) {
+  a.iters += o.iterations;
+  a.entries += o.entries;
+  a.bytes += o.qbytes + 48 * o.entries;  // predictor bytes + 48 B per entry
+}
+
 // The reference's find_capacity (search.hpp:145-174) against a memo; throws
 // NeedProbe on the first unanswered rate and ProbeError when the asked rate's
 // simulation raised (the reference's feasible(q) throwing out of find_capacity).
-double replay_capacity(const ProbeMemo& memo, const CapacitySearchOptions& o) {
+double replay_capacity(const ProbeMemo& memo, const CapacitySearchOptions& o,
+                       std::vector<const ProbeAnswer*>* asked = nullptr) {
   auto ask = [&](double q, int phase, double lo, double hi) {
     auto it = memo.find(q);
     if (it == memo.end()) throw NeedProbe{q, phase, lo, hi};
+    if (asked) asked->push_back(&it->second);
     if (it->second.error) throw ProbeError{it->second.err};
     return it->second.feasible;
   };
@@ -230,6 +241,7 @@ struct Candidate {
   bool done = false;       // evaluation finished (capacity known, or failed)
   bool measured = false;   // SLO / static run taken
   int64_t probe_iters = 0; // longest probe unit so far (iterations): speculation budget
+  ProbeAnswer full_run;    // work of the SLO / static run (iters, entries, bytes)
   ConfigResult res;
 };
 
@@ -587,6 +599,8 @@ SweepKnobs knobs_from_env() {
 // Records a full run's SLO measurement (or an error) on its candidate.
 void take_measurement(Candidate& C, const std::vector<SimUnitOut>& out, const ProbeDesc& p,
                       const double* sel3, const ResidentWorkload& w) {
+  C.full_run = ProbeAnswer{};
+  for (int u = p.first_unit; u < p.first_unit + (p.decoupled ? p.R : 1); ++u) add_work(C.full_run, out[u]);
   if (const SimUnitOut* e = first_error(out, p)) {
     fail(C, *e);
     return;
@@ -669,15 +683,18 @@ void run_round(SweepLane& lane, std::vector<Candidate>& cands,
     int64_t late = 0, iters = 0;
     bool aborted = false;
     const int nu = p.decoupled ? p.R : 1;
+    ProbeAnswer work;
     for (int u = p.first_unit; u < p.first_unit + nu; ++u) {
       late += out[u].late;
       aborted |= out[u].aborted != 0;
       iters = std::max<int64_t>(iters, out[u].iterations);
+      add_work(work, out[u]);
     }
     C.probe_iters = std::max(C.probe_iters, iters);
     const SimUnitOut* e = first_error(out, p);
     if (!e) {
-      C.memo[p.qps] = ProbeAnswer{!aborted && late <= max_late};
+      work.feasible = !aborted && late <= max_late;
+      C.memo[p.qps] = work;
     } else if (p.decoupled && p.R <= kMaxCoupledReplicas) {
       // independent replicas cannot order an error against the global abort:
       // replay this probe with every replica in one unit
@@ -685,9 +702,11 @@ void run_round(SweepLane& lane, std::vector<Candidate>& cands,
       redo.add_probe(L.probe_cand[k], C, ci, p.qps, n, SSG_UF_ABORT, base.delay_p99_threshold,
                      max_late, true, false, -1);
     } else if (aborted && !p.decoupled) {
-      C.memo[p.qps] = ProbeAnswer{false};
+      C.memo[p.qps] = work;
     } else {
-      C.memo[p.qps] = ProbeAnswer{false, true, *e};
+      work.error = true;
+      work.err = *e;
+      C.memo[p.qps] = work;
     }
   }
   if (redo.probes.empty()) return;
@@ -696,12 +715,16 @@ void run_round(SweepLane& lane, std::vector<Candidate>& cands,
     const ProbeDesc& p = redo.probes[k];
     Candidate& C = cands[redo.probe_cand[k]];
     const SimUnitOut& o = out[p.first_unit];
-    if (o.aborted)
-      C.memo[p.qps] = ProbeAnswer{false};
-    else if (o.code == SSG_OK)
-      C.memo[p.qps] = ProbeAnswer{o.late <= max_late};
-    else
-      C.memo[p.qps] = ProbeAnswer{false, true, o};
+    ProbeAnswer work;
+    add_work(work, o);
+    if (o.aborted) {
+    } else if (o.code == SSG_OK) {
+      work.feasible = o.late <= max_late;
+    } else {
+      work.error = true;
+      work.err = o;
+    }
+    C.memo[p.qps] = work;
   }
 }
 
@@ -1190,6 +1213,27 @@ std::vector<ConfigResult> SearchSession::evaluate(int shard, int num_shards,
     if (open) busy += b - a;
     stats().simulate_busy_ms += busy;
     cudaEventDestroy(origin);
+  }
+  {
+    // the sequential search's share of the device work: the probes its
+    // find_capacity replay asks for, plus each SLO / static run
+    RunStats& st = stats();
+    for (auto& C : cands) {
+      std::vector<const ProbeAnswer*> asked;
+      try {
+        replay_capacity(C.memo, C.copts, &asked);
+      } catch (...) {
+        // errors, unfinished searches: the asked prefix is still the reference's work
+      }
+      for (const ProbeAnswer* a : asked) {
+        st.useful_iterations += a->iters;
+        st.useful_entries += a->entries;
+        st.useful_bytes += a->bytes;
+      }
+      st.useful_iterations += C.full_run.iters;
+      st.useful_entries += C.full_run.entries;
+      st.useful_bytes += C.full_run.bytes;
+    }
   }
   for (auto& C : cands) results[C.index] = std::move(C.res);
   for (std::size_t i = 0; i < configs.size(); ++i)

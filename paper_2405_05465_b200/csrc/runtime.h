@@ -75,6 +75,8 @@ struct RunStats {
   double predict_ms = 0.0;
   int64_t h2d_bytes = 0, d2h_bytes = 0;
   double simulate_busy_ms = 0.0;  // union of k_simulate intervals (launches overlap across streams)
+  // sweep work the sequential reference search would do (probes its replay asks + SLO runs)
+  int64_t useful_iterations = 0, useful_entries = 0, useful_bytes = 0;
   void add(const RunStats& o);
 };
 // The calling thread's counters: the process-wide ones, or a StatsScope's
