@@ -115,7 +115,7 @@ __device__ __forceinline__ int64_t warp_sum64(int64_t v) {
 }
 
 // ---------------------------------------------------------------- errors
-__device__ SSG_COLD void set_error(Unit& U, int code, int32_t i32, int64_t a, int64_t b,
+static __device__ SSG_COLD void set_error(Unit& U, int code, int32_t i32, int64_t a, int64_t b,
                                           double f) {
   __syncwarp();
   if (U.lane == 0 && U.out->code == SSG_OK) {
@@ -292,7 +292,7 @@ __device__ __forceinline__ void mark_scheduled(Unit& U, int32_t j) {
 }
 
 // preempt_latest (scheduler.hpp:269-285): returns the victim or -1.
-__device__ SSG_COLD int32_t preempt_latest(Unit& U, RepState& S, int r) {
+static __device__ SSG_COLD int32_t preempt_latest(Unit& U, RepState& S, int r) {
   int32_t* a = RUN(U, r);
   for (int32_t p = S.run_n - 1; p >= 0; --p) {
     const int32_t v = a[p];
@@ -463,7 +463,7 @@ static __device__ void schedule_decodes(Unit& U, RepState& S, int r, int32_t max
 // First position >= i of the running queue whose request matches `pred`
 // (warp-parallel 32-entry windows); run_n if none.
 #define PRED_PREFILL_LEFT 0
-__device__ SSG_WARM int32_t next_running(Unit& U, const RepState& S, int r, int32_t i, int pred) {
+static __device__ SSG_WARM int32_t next_running(Unit& U, const RepState& S, int r, int32_t i, int pred) {
   const int32_t* a = RUN(U, r);
 #pragma unroll 1
   for (; i < S.run_n; i += 32) {
@@ -492,7 +492,7 @@ __device__ SSG_WARM int32_t next_running(Unit& U, const RepState& S, int r, int3
 //            a prompt longer than the budget runs alone (no decodes)
 //   Sarathi: budget chunk_size; decodes first; then in-flight chunks in running
 //            order; then admission of chunk = min(budget, prompt)
-__device__ SSG_WARM void schedule_chunked(Unit& U, RepState& S, int r) {
+static __device__ SSG_WARM void schedule_chunked(Unit& U, RepState& S, int r) {
   const SimConfig& c = *U.cfg;
   const bool sar = c.policy == SSG_POL_SARATHI, vl = c.policy == SSG_POL_VLLM;
   int32_t budget = sar ? c.chunk : c.max_tokens;
@@ -569,7 +569,7 @@ __device__ SSG_WARM void schedule_chunked(Unit& U, RepState& S, int r) {
   __syncwarp();
 }
 
-__device__ SSG_COLD void schedule_ft(Unit& U, RepState& S, int r) {
+static __device__ SSG_COLD void schedule_ft(Unit& U, RepState& S, int r) {
   const SimConfig& c = *U.cfg;
   if (!S.ft_inflight) {
     while (S.wait_n > 0 && S.run_n < c.max_batch) {
@@ -770,7 +770,7 @@ static __device__ void complete_batch(Unit& U, RepState& S, int r) {
 // tables' range (or configs without tables): one lane per task, operator-order
 // accumulation.  Out of line -- it is the cold path of batch_latency.
 template <int FMA, int FOREST>
-__device__ SSG_COLD void batch_latency_full(Unit& U, const int64_t* st, int& err, int& err_task,
+static __device__ SSG_COLD void batch_latency_full(Unit& U, const int64_t* st, int& err, int& err_task,
                                                 int& err_feat, double& err_val, int64_t& qb) {
   const SimConfig& c = *U.cfg;
   const int pp = c.pp;
