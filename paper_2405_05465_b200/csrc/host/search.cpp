@@ -855,8 +855,30 @@ SearchSession::SearchSession(const ModelSpec& spec, const std::vector<Request>& 
   for (auto tp : opts.space.tp_degrees)
     if (spec.num_kv_heads % tp == 0) tps.push_back(tp);
   require(!tps.empty(), "search: no valid tp degree for this model");
-  for (const auto& sku : opts.space.skus)
-    S.owned.push_back(train(generate_synthetic_profile(spec, sku, tps), opts.train));
+  // SKUs are independent (own profile, own seed-identical training): build them
+  // on host threads; errors surface in SKU order, as the reference's loop raises
+  const std::size_t nsku = opts.space.skus.size();
+  std::vector<EstimatorModel> built(nsku);
+  std::vector<std::exception_ptr> err(nsku);
+  {
+    const int dev = context().device;
+    auto one = [&](std::size_t k) {
+      try {
+        StatsScope scope;  // counters merge into the process totals under the lock
+        cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+        built[k] = train(generate_synthetic_profile(spec, opts.space.skus[k], tps), opts.train);
+      } catch (...) {
+        err[k] = std::current_exception();
+      }
+    };
+    std::vector<std::thread> pool;
+    for (std::size_t k = 1; k < nsku; ++k) pool.emplace_back(one, k);
+    if (nsku) one(0);
+    for (auto& t : pool) t.join();
+  }
+  for (auto& e : err)
+    if (e) std::rethrow_exception(e);
+  for (auto& e : built) S.owned.push_back(std::move(e));
   for (const auto& e : S.owned) S.ests.push_back(&e);
   open_workload(workload);
 }
