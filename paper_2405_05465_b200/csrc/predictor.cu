@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 
 #include "predictor.cuh"
 #include "runtime.h"
@@ -350,6 +351,8 @@ struct DeviceRegressor {
 
 double Regressor::predict(std::span<const double> x) const {
   auto& ctx = ssg::context();
+  static std::mutex upload_mu;  // the first call uploads; predict is const and callable concurrently
+  std::unique_lock<std::mutex> up(upload_mu);
   if (!dev_) {
     auto d = std::make_shared<DeviceRegressor>();
     SsgModelDesc desc{};
@@ -363,17 +366,25 @@ double Regressor::predict(std::span<const double> x) const {
     upload_pools(d->est, dpool, nodes, roots);
     dev_ = std::move(d);
   }
-  const int nf = dev_->est.host_models[0].nf;
+  std::shared_ptr<DeviceRegressor> dr = dev_;
+  up.unlock();
+  const int nf = dr->est.host_models[0].nf;
   internal_check(x.size() >= static_cast<std::size_t>(nf), "regressor predict: feature count mismatch");
-  double v[3] = {x[0], nf > 1 ? x[1] : 0.0, 0.0};
-  ssg::DeviceBuffer<double> buf(3);
-  buf.upload(v, 2, ctx.stream);
-  k_regress<<<1, 1, 0, ctx.stream>>>(dev_->est.view, buf.ptr, buf.ptr + 2);
+  DeviceEstimator& de = dr->est;
+  std::lock_guard<std::mutex> lk(de.one_mu);
+  if (!de.one_host) {
+    ssg::cuda_check(cudaMallocHost(reinterpret_cast<void**>(&de.one_host), 4 * sizeof(double)), "pinned");
+    de.one_dev.resize(4);
+  }
+  double* h = de.one_host;
+  h[0] = x[0];
+  h[1] = nf > 1 ? x[1] : 0.0;
+  ssg::cuda_check(cudaMemcpyAsync(de.one_dev.ptr, h, 2 * sizeof(double), cudaMemcpyHostToDevice, ctx.stream), "H2D");
+  k_regress<<<1, 1, 0, ctx.stream>>>(de.view, de.one_dev.ptr, de.one_dev.ptr + 2);
   ssg::cuda_check(cudaGetLastError(), "k_regress launch");
-  double out = 0.0;
-  ssg::cuda_check(cudaMemcpyAsync(&out, buf.ptr + 2, 8, cudaMemcpyDeviceToHost, ctx.stream), "D2H");
+  ssg::cuda_check(cudaMemcpyAsync(h + 2, de.one_dev.ptr + 2, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream), "D2H");
   ssg::cuda_check(cudaStreamSynchronize(ctx.stream), "regressor predict");
-  return out;
+  return h[2];
 }
 
 const DeviceEstimator& EstimatorModel::device() const {
@@ -479,6 +490,21 @@ void launch_predict(const DeviceEstimator& de, int64_t n, const int32_t* slots, 
 
 namespace servesim {
 
+namespace {
+// One EstimatorModel::predict query: {v0, v1} in, {runtime, status code} out.
+__global__ void k_predict_one(SsgEstView E, int32_t slot, const double* in, double* out) {
+  double r = 0.0;
+  int bad = 0;
+  const int code = ssg_predict_one(E, slot, in[0], in[1], &r, &bad);
+  out[0] = r;
+  out[1] = (double)code;
+}
+}  // namespace
+
+DeviceEstimator::~DeviceEstimator() {
+  if (one_host) cudaFreeHost(one_host);
+}
+
 double EstimatorModel::predict(OpName op, std::int64_t tp, const FeatureMap& features) const {
   const PerOpModel& m = find(op, tp);
   double v[2] = {0.0, 0.0};
@@ -488,23 +514,29 @@ double EstimatorModel::predict(OpName op, std::int64_t tp, const FeatureMap& fea
                                       " missing feature " + m.schema[f]);
     v[f] = it->second;
   }
-  const auto& de = device();
+  auto& de = const_cast<DeviceEstimator&>(device());
   auto& ctx = ssg::context();
   const int32_t slot = de.slot(op, tp);
-  ssg::DeviceBuffer<double> buf(4);
-  ssg::DeviceBuffer<unsigned long long> err(1);
-  unsigned long long none = SSG_NO_ERROR;
-  err.upload(&none, 1, ctx.stream);
-  buf.upload(v, 2, ctx.stream);
-  ssg::launch_predict(de, 1, nullptr, slot, buf.ptr, buf.ptr + 1, buf.ptr + 2, err.ptr, ctx.stream,
-                      nullptr, nullptr);
-  double out = 0.0;
-  unsigned long long word = 0;
-  cudaMemcpyAsync(&out, buf.ptr + 2, 8, cudaMemcpyDeviceToHost, ctx.stream);
-  cudaMemcpyAsync(&word, err.ptr, 8, cudaMemcpyDeviceToHost, ctx.stream);
+  // a single query is latency: one 16 B copy in, one launch, one 16 B copy out,
+  // through buffers the estimator keeps (pinned host + HBM), one caller at a time
+  std::lock_guard<std::mutex> lk(de.one_mu);
+  if (!de.one_host) {
+    ssg::cuda_check(cudaMallocHost(reinterpret_cast<void**>(&de.one_host), 4 * sizeof(double)), "pinned");
+    de.one_dev.resize(4);
+  }
+  double* h = de.one_host;
+  h[0] = v[0];
+  h[1] = v[1];
+  ssg::cuda_check(cudaMemcpyAsync(de.one_dev.ptr, h, 2 * sizeof(double), cudaMemcpyHostToDevice, ctx.stream), "H2D");
+  k_predict_one<<<1, 1, 0, ctx.stream>>>(de.view, slot, de.one_dev.ptr, de.one_dev.ptr + 2);
+  ssg::cuda_check(cudaGetLastError(), "k_predict_one launch");
+  ssg::cuda_check(cudaMemcpyAsync(h + 2, de.one_dev.ptr + 2, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx.stream), "D2H");
   ssg::cuda_check(cudaStreamSynchronize(ctx.stream), "predict");
-  if (word != SSG_NO_ERROR) ssg::raise_predict_error(*this, word, nullptr, slot, v, v + 1);
-  return out;
+  ssg::stats().launches_predict += 1;
+  ssg::stats().queries += 1;
+  const int code = static_cast<int>(h[3]);
+  if (code != SSG_OK) ssg::raise_predict_error(*this, static_cast<unsigned long long>(code), nullptr, slot, v, v + 1);
+  return h[2];
 }
 
 }  // namespace servesim

@@ -4,6 +4,7 @@
 
 #include <cstddef>
 #include <cstring>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -203,6 +204,11 @@ struct DeviceEstimator {
   ssg::DeviceBuffer<double> dpool;
   ssg::DeviceBuffer<SsgNode> nodes;
   ssg::DeviceBuffer<int32_t> roots;
+  // single-query path (EstimatorModel::predict): kept buffers, one caller at a time
+  std::mutex one_mu;
+  ssg::DeviceBuffer<double> one_dev;
+  double* one_host = nullptr;  // pinned
+  ~DeviceEstimator();
   ssg::DeviceBuffer<double> node_a;  // SoA mirror (SSG_FOREST_SOA A/B builds)
   ssg::DeviceBuffer<int2> node_fr;
   std::vector<SsgModelDesc> host_models;
