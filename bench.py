@@ -575,7 +575,8 @@ def main():
                          **profiled_traffic("k_simulate")),
         "gpu_launches": launches,
         "work": dict({k: st[k] // a.steps for k in ("units", "iterations", "entries", "events",
-                                                     "useful_iterations", "useful_entries")},
+                                                     "useful_iterations", "useful_entries",
+                                                     "cancelled_probes")},
                      speculative_over_sequential_iterations=st["iterations"] / max(1, st["useful_iterations"]),
                      speculative_over_sequential_entries=st["entries"] / max(1, st["useful_entries"])),
         "clocks": clk,

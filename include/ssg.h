@@ -216,6 +216,7 @@ typedef struct ssg_run_stats {
      find_capacity replay asks for plus each SLO / static run (the rest of
      iterations / entries is speculation) */
   int64_t useful_iterations, useful_entries, useful_bytes;
+  int64_t cancelled_probes; /* speculative probes stopped once a lower rate of their candidate failed */
 } ssg_run_stats;
 void ssg_stats_reset(void);
 void ssg_stats_get(ssg_run_stats* out);

@@ -680,6 +680,7 @@ __device__ void run_unit(Unit& U) {
   // next event unless an arrival is due at or before it (arrivals carry lower
   // seq numbers): then the event selection is skipped (one call site each)
   bool direct = false;
+  int since_check = 0;  // BatchStarts since the last speculation-group check
   while (true) {
     // ---- next event: (time, seq) argmin over the arrival head and replica slots
     double bt = INFINITY;
@@ -821,6 +822,13 @@ __device__ void run_unit(Unit& U) {
       }
     }
     if (S.ev_kind == 1) {
+      // a speculative probe the capacity replay can no longer ask for (a probe
+      // it is only asked after, on a feasible outcome, failed): stop, result unused
+      if (U.group_fail && ++since_check >= 64 &&
+          (since_check = 0, (*(volatile const uint32_t*)U.group_fail & u.kill) != 0)) {
+        wput(U, &U.out->aborted, 2);
+        break;
+      }
       S.ev_kind = 0;
       const bool ok = batch_start<FMA, FOREST>(U, S, r);
       if (reg1)
@@ -854,6 +862,9 @@ __device__ void run_unit(Unit& U) {
     }
   }
   if (reg1) store_rep(U, 0, S1);
+  // an aborted or failed probe cancels the speculative probes behind its feasible branch
+  if (U.group_fail && U.lane == 0 && (U.out->aborted == 1 || U.out->code != SSG_OK))
+    atomicOr(U.group_fail, 1u << u.rung);
   U.qbytes += warp_sum64(U.qb_lane);
   if (U.lane == 0) {
     U.out->span = U.clock;
@@ -929,7 +940,7 @@ __global__ void SSG_SIM_BOUNDS(FAST) k_simulate(SimLaunch L) {
   U.smem_part = part[wib];
   U.tables = L.tables;
   U.fast = L.fast_forward;
-  U.group_late = nullptr;
+  U.group_fail = (L.group_fail && U.u->group >= 0) ? L.group_fail + U.u->group : nullptr;
   U.lane = threadIdx.x & 31;
   U.ax1_hint = 0;
   U.MB = U.cfg->max_batch;

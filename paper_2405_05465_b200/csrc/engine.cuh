@@ -56,7 +56,7 @@ struct Unit {
   int64_t* smem_stats;  // per-warp shared scratch [SSG_MAX_PP * 6]
   const double* tables; // token tables pool (SimConfig::tab_off)
   double* smem_part;    // per-warp shared scratch [4 * SSG_MAX_PP]
-  int* group_late;  // shared by the probe's units (may be null)
+  uint32_t* group_fail;  // this unit's speculation-group failure mask (may be null)
   int fast;         // pure-decode fast-forward enabled
   int lane;
   int64_t rep_stride;  // int32 words per replica in ws

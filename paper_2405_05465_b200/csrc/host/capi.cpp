@@ -634,6 +634,7 @@ void ssg_stats_get(ssg_run_stats* out) {
   out->useful_iterations = r.useful_iterations;
   out->useful_entries = r.useful_entries;
   out->useful_bytes = r.useful_bytes;
+  out->cancelled_probes = r.cancelled_probes;
 }
 
 int ssg_search_finalize(const char* config_path, const ssg_config_record* records, size_t n,

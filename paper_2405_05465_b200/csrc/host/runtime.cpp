@@ -45,6 +45,7 @@ void RunStats::add(const RunStats& o) {
   useful_iterations += o.useful_iterations;
   useful_entries += o.useful_entries;
   useful_bytes += o.useful_bytes;
+  cancelled_probes += o.cancelled_probes;
 }
 
 StatsScope::StatsScope() : prev(t_stats) { t_stats = &local; }

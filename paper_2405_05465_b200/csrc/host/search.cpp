@@ -192,31 +192,61 @@ double replay_capacity(const ProbeMemo& memo, const CapacitySearchOptions& o,
 }
 
 // Rates the search may ask right after `need` (speculation; never affects
-// the answer, only how many rounds it takes).
+// the answer, only how many rounds it takes), each with the indices (into
+// `out`) of the earlier rates that must come out feasible for the replay to
+// ask it: a failure of any of them cancels it on the device (SimUnit::kill).
+struct SpecRate {
+  double q;
+  std::vector<int> after_feasible;
+};
+
+// One candidate's unanswered rates for a round, with their cancel masks.
+struct SpecProbes {
+  std::size_t k = 0;  // candidate
+  std::vector<double> rates;
+  std::vector<uint32_t> kill;
+};
+
 void speculate(const NeedProbe& need, const CapacitySearchOptions& o, int ladder, int depth,
-               std::vector<double>& out) {
-  out.push_back(need.q);
+               std::vector<SpecRate>& out) {
+  out.push_back({need.q, {}});
   if (need.phase == 0) {
+    // doubling: rung k is asked only after rungs 0..k-1 were feasible
     double q = need.q;
     for (int k = 1; k < ladder; ++k) {
       q *= 2.0;
       if (q > o.max_qps) break;
-      out.push_back(q);
+      std::vector<int> prev(out.size());
+      for (std::size_t i = 0; i < prev.size(); ++i) prev[i] = static_cast<int>(i);
+      out.push_back({q, prev});
     }
   } else if (need.phase == 1) {
     // halving: each deeper rate is the slowest probe of its round (iterations
     // grow ~1/qps), and the first halving usually suffices -- no speculation
   } else {
-    // bisection sub-tree below (lo, hi) to `depth` levels
-    std::vector<std::pair<double, double>> level{{need.lo, need.hi}}, next;
+    // bisection sub-tree below (lo, hi) to `depth` levels: an interval's mid is
+    // asked once the interval is reached; its upper half is reached only when
+    // the mid is feasible (its lower half when it is not, which no early
+    // failure can tell, so that half inherits its parent's conditions only)
+    struct Interval {
+      double lo, hi;
+      std::vector<int> cond;  // indices into out that must be feasible
+    };
+    std::vector<Interval> level{{need.lo, need.hi, {}}}, next;
     for (int d = 0; d < depth; ++d) {
       next.clear();
-      for (auto [lo, hi] : level) {
-        if (!(hi - lo > o.tolerance * hi)) continue;
-        const double mid = 0.5 * (lo + hi);
-        if (d > 0) out.push_back(mid);
-        next.push_back({lo, mid});
-        next.push_back({mid, hi});
+      for (const Interval& iv : level) {
+        if (!(iv.hi - iv.lo > o.tolerance * iv.hi)) continue;
+        const double mid = 0.5 * (iv.lo + iv.hi);
+        int idx = 0;  // d == 0: the mid is need.q itself
+        if (d > 0) {
+          idx = static_cast<int>(out.size());
+          out.push_back({mid, iv.cond});
+        }
+        next.push_back({iv.lo, mid, iv.cond});
+        std::vector<int> up = iv.cond;
+        up.push_back(idx);
+        next.push_back({mid, iv.hi, up});
       }
       level.swap(next);
     }
@@ -259,6 +289,7 @@ struct SweepBuffers {
   DeviceBuffer<RepState> reps;
   DeviceBuffer<SimUnitOut> out;
   DeviceBuffer<SelectTask> tasks;
+  DeviceBuffer<uint32_t> group_fail;  // per speculation group: bits of its failed probes
 };
 
 // A launch under construction: per-candidate configs, probes and their units.
@@ -288,8 +319,11 @@ struct ProbeLaunch {
 
   // One probe of candidate `cand` (config `ci`): RR replicas become independent
   // units (replica r owns trace positions r, r+R, ...), otherwise one coupled unit.
+  int32_t ngroups = 0;  // speculation groups (SimUnit::group)
+
   void add_probe(std::size_t cand, const Candidate& C, int32_t ci, double qps, int32_t n, int flags,
-                 double thr, int32_t max_late, bool coupled, bool static_run, int64_t emis_base) {
+                 double thr, int32_t max_late, bool coupled, bool static_run, int64_t emis_base,
+                 int32_t group = -1, int32_t rung = 0, uint32_t kill = 0) {
     const SimConfig& cfg = configs[ci];
     const int R = static_cast<int>(C.cluster.par.num_replicas);
     ProbeDesc p{};
@@ -317,6 +351,9 @@ struct ProbeLaunch {
       nreps += u.R;
       u.abort_thr = thr;
       u.abort_max_late = max_late;
+      u.group = group;
+      u.rung = rung;
+      u.kill = kill;
       units.push_back(u);
     }
     if (emis_base >= 0) measured.push_back(static_cast<int32_t>(probes.size()));
@@ -457,6 +494,12 @@ void run_launch(SweepLane& lane, ProbeLaunch& L, const ResidentWorkload& w,
   K.fast_forward = sweep_fast_forward_enabled() ||
                    static_cast<int64_t>(L.units.size()) <= ff_units ? 1 : 0;
   K.has_forest = L.has_forest ? 1 : 0;
+  K.group_fail = nullptr;
+  if (L.ngroups > 0) {
+    B.group_fail.resize(L.ngroups);
+    cuda_check(cudaMemsetAsync(B.group_fail.ptr, 0, L.ngroups * sizeof(uint32_t), s), "memset");
+    K.group_fail = B.group_fail.ptr;
+  }
   cudaEvent_t e0, e1;
   cuda_check(cudaEventCreate(&e0), "event");
   cuda_check(cudaEventCreate(&e1), "event");
@@ -622,18 +665,24 @@ void take_measurement(Candidate& C, const std::vector<SimUnitOut>& out, const Pr
 // measurement at evaluation_fraction x capacity, or the static makespan run).
 // An error inside a probe ends that candidate's evaluation (the reference's
 // exception) unless the probe's abort came first in event order.
-void run_round(SweepLane& lane, std::vector<Candidate>& cands,
-               const std::vector<std::pair<std::size_t, std::vector<double>>>& probes,
+void run_round(SweepLane& lane, std::vector<Candidate>& cands, const std::vector<SpecProbes>& probes,
                const std::vector<std::pair<std::size_t, double>>& full, bool static_run,
                const ResidentWorkload& w, const CapacitySearchOptions& base) {
   const int32_t n = w.n;
   const int32_t max_late = max_late_of(static_cast<std::size_t>(n));
   ProbeLaunch L;
-  for (const auto& [k, rates] : probes) {
+  for (const SpecProbes& sp : probes) {
+    const std::size_t k = sp.k;
     const int32_t ci = L.add_config(cands[k]);
-    for (double q : rates)
-      L.add_probe(k, cands[k], ci, q, n, SSG_UF_ABORT, base.delay_p99_threshold, max_late, false,
-                  false, -1);
+    // a candidate's probes form one speculation group: once a probe fails
+    // (abort or error), the probes the replay would only ask after it came out
+    // feasible are cancelled on the device (SimUnit::kill).  Safe by
+    // construction: a cancelled rate stays unanswered in the memo, so a replay
+    // that does ask for it probes it in a later round.
+    const int32_t g = sp.rates.size() > 1 && sp.rates.size() <= 32 ? L.ngroups++ : -1;
+    for (std::size_t i = 0; i < sp.rates.size(); ++i)
+      L.add_probe(k, cands[k], ci, sp.rates[i], n, SSG_UF_ABORT, base.delay_p99_threshold, max_late,
+                  false, false, -1, g, static_cast<int32_t>(i), g >= 0 ? sp.kill[i] : 0u);
   }
   for (const auto& [k, q] : full) {
     const int32_t ci = L.add_config(cands[k]);
@@ -681,14 +730,19 @@ void run_round(SweepLane& lane, std::vector<Candidate>& cands,
     if (p.emis_base >= 0) continue;  // measured run, handled above
     Candidate& C = cands[L.probe_cand[k]];
     int64_t late = 0, iters = 0;
-    bool aborted = false;
+    bool aborted = false, cancelled = false;
     const int nu = p.decoupled ? p.R : 1;
     ProbeAnswer work;
     for (int u = p.first_unit; u < p.first_unit + nu; ++u) {
       late += out[u].late;
-      aborted |= out[u].aborted != 0;
+      aborted |= out[u].aborted == 1;
+      cancelled |= out[u].aborted == 2;
       iters = std::max<int64_t>(iters, out[u].iterations);
       add_work(work, out[u]);
+    }
+    if (cancelled) {  // not needed by the replay; leave the rate unanswered
+      stats().cancelled_probes += 1;
+      continue;
     }
     C.probe_iters = std::max(C.probe_iters, iters);
     const SimUnitOut* e = first_error(out, p);
@@ -736,7 +790,7 @@ void run_group(SweepLane& lane, std::vector<Candidate>& cands, const std::vector
                const SearchOptions& opts, const ResidentWorkload& w, const SweepKnobs& knobs,
                std::vector<std::size_t>& measured) {
   while (true) {
-    std::vector<std::pair<std::size_t, std::vector<double>>> probes;
+    std::vector<SpecProbes> probes;
     std::vector<std::pair<std::size_t, double>> full;
     int64_t longest = 1;
     for (auto k : live) longest = std::max(longest, cands[k].probe_iters);
@@ -751,13 +805,23 @@ void run_group(SweepLane& lane, std::vector<Candidate>& cands, const std::vector
           // candidates on the critical path (longest probes) speculate deeper,
           // so their bisection finishes in one round
           const bool critical = C.probe_iters * 100 >= longest * knobs.crit_pct;
-          std::vector<double> qs;
+          std::vector<SpecRate> qs;
           speculate(need, C.copts, knobs.ladder, critical ? knobs.depth + knobs.crit_extra : knobs.depth, qs);
-          std::vector<double> fresh;
-          for (double q : qs)
-            if (!C.memo.count(q) && std::find(fresh.begin(), fresh.end(), q) == fresh.end())
-              fresh.push_back(q);
-          probes.push_back({k, fresh});
+          // unanswered rates; each one's cancel mask over the others' positions
+          std::vector<int> pos(qs.size(), -1);
+          SpecProbes sp;
+          sp.k = k;
+          for (std::size_t i = 0; i < qs.size(); ++i) {
+            const double q = qs[i].q;
+            if (C.memo.count(q) || std::find(sp.rates.begin(), sp.rates.end(), q) != sp.rates.end()) continue;
+            pos[i] = static_cast<int>(sp.rates.size());
+            uint32_t kill = 0;
+            for (int a : qs[i].after_feasible)
+              if (pos[a] >= 0 && pos[a] < 32) kill |= 1u << pos[a];
+            sp.rates.push_back(q);
+            sp.kill.push_back(kill);
+          }
+          probes.push_back(std::move(sp));
           continue;
         } catch (const ProbeError& pe) {
           fail(C, pe.err);

@@ -78,6 +78,7 @@ struct RunStats {
   double simulate_busy_ms = 0.0;  // union of k_simulate intervals (launches overlap across streams)
   // sweep work the sequential reference search would do (probes its replay asks + SLO runs)
   int64_t useful_iterations = 0, useful_entries = 0, useful_bytes = 0;
+  int64_t cancelled_probes = 0;  // speculative probes stopped once a lower rate of their group failed
   void add(const RunStats& o);
 };
 // The calling thread's counters: the process-wide ones, or a StatsScope's

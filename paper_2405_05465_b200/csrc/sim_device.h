@@ -125,7 +125,9 @@ struct SimUnit {
   double abort_thr;
   int64_t log_off;    // into the batch-log arena (int64 words)
   int64_t log_cap;
-  int32_t group;      // late-schedule counter shared by the units of one probe
+  int32_t group;      // speculation group (a candidate's probes of one launch), -1: none
+  int32_t rung;       // this probe's bit in its group's failure mask
+  uint32_t kill;      // group failure bits that make this probe unnecessary
   int32_t pad;
 };
 
@@ -145,7 +147,8 @@ struct RepState {
 
 struct SimUnitOut {
   int32_t code;       // SSG_OK / SSG_ERR_*
-  int32_t aborted;    // probe stopped: late schedules exceeded the bound
+  int32_t aborted;    // 1: probe stopped, late schedules exceeded the bound;
+                      // 2: cancelled (the capacity replay cannot ask for it any more)
   int32_t late;       // late first-schedules counted (probe units)
   int32_t err_i32;    // error operand: op slot / replica
   int64_t err_i64[2]; // error operands: request id, needed units / feature index

@@ -30,6 +30,7 @@ struct SimLaunch {
   const double* tables;       // token tables pool, may be null
   int32_t fast_forward;       // 1: pure-decode stretches of lone replicas take the fast loop
   int32_t has_forest;         // any estimator of the launch has forest models
+  uint32_t* group_fail;       // per speculation group: bits of the probes that failed, may be null
 };
 
 namespace ssg {
