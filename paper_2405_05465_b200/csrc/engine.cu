@@ -419,7 +419,7 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
         } else {
           int32_t lo1;
           double f1;
-          ssg_axis_cell_hint(ax1, n1, ssg_log1p(v1, FMA), &U.ax1_hint, &lo1, &f1);
+          ssg_axis_cell_hint(ax1, n1, hot_log1p<FMA>(v1), &U.ax1_hint, &lo1, &f1);
           const int32_t h1 = n1 == 1 ? 0 : 1;
           const double g1 = __dsub_rn(1.0, f1);
           const double w1lo = g1, w1hi = h1 ? f1 : g1;
@@ -430,7 +430,7 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
           if (!ssg_exp_in_range(r)) {
             good = 0;
           } else {
-            const double pred = __dmul_rn(od.count, ssg_exp(r, FMA));
+            const double pred = __dmul_rn(od.count, hot_exp<FMA>(r));
             double acc = __dadd_rn(ts, pred);
 #pragma unroll
             for (int q = 0; q < 3; ++q)

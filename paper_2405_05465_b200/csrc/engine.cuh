@@ -38,6 +38,21 @@
 
 namespace ssgk {
 
+// The attention query's libm calls at the two per-iteration sites (batch
+// latency, fast-forward).  SSG_LIBM_CALLS=1 (A/B builds) emits them once as
+// out-of-line functions instead of inlining a copy at each site.
+#if defined(SSG_LIBM_CALLS) && SSG_LIBM_CALLS
+template <int FMA>
+__device__ __noinline__ double hot_log1p(double x) { return ssg_log1p(x, FMA); }
+template <int FMA>
+__device__ __noinline__ double hot_exp(double x) { return ssg_exp(x, FMA); }
+#else
+template <int FMA>
+__device__ __forceinline__ double hot_log1p(double x) { return ssg_log1p(x, FMA); }
+template <int FMA>
+__device__ __forceinline__ double hot_exp(double x) { return ssg_exp(x, FMA); }
+#endif
+
 struct Unit {
   const SimConfig* cfg;
   const SimUnit* u;
@@ -888,7 +903,7 @@ __device__ __forceinline__ int ssg_attn_interp(const SsgEstView& E, const SsgMod
   const int32_t n1 = m.axis_len[1];
   int32_t lo1;
   double f1;
-  ssg_axis_cell_hint(E.dpool + m.axis_off[1], n1, ssg_log1p(v1, FMA), &hint, &lo1, &f1);
+  ssg_axis_cell_hint(E.dpool + m.axis_off[1], n1, hot_log1p<FMA>(v1), &hint, &lo1, &f1);
   const int32_t n0 = m.axis_len[0];
   const double* vals = E.dpool + m.values_off;
   const int32_t h0 = n0 == 1 ? 0 : 1;
@@ -902,7 +917,7 @@ __device__ __forceinline__ int ssg_attn_interp(const SsgEstView& E, const SsgMod
   acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(w1hi, w0lo), __ldg(vals + r0 + lo1 + h1)));
   acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(w1hi, w0hi), __ldg(vals + r1 + lo1 + h1)));
   if (!ssg_exp_in_range(acc)) return SSG_ERR_EXP_RANGE;
-  *out = ssg_exp(acc, FMA);
+  *out = hot_exp<FMA>(acc);
   return SSG_OK;
 }
 
