@@ -624,12 +624,16 @@ __device__ SSG_FFWD int fast_forward(Unit& U, RepState& S, int32_t* next_arrival
   return fast_forward_t<FMA>(U, S, next_arrival, next_arrival_time, flops_acc);
 }
 
-template <int FMA, int FOREST, int FAST>
+// LONE = 1: every unit of the launch is one replica with round-robin or
+// least-outstanding routing (the sweep's decoupled probes), so the multi-replica
+// event selection, routing argmins, deferred pool and replica-state spills are
+// compiled out of the body (the kernel is instruction-fetch bound).
+template <int FMA, int FOREST, int FAST, int LONE>
 __device__ void run_unit(Unit& U) {
   const long long t_start = clock64();
   const SimUnit& u = *U.u;
   const SimConfig& c = *U.cfg;
-  const int R = u.R;
+  const int R = LONE ? 1 : u.R;
   // ---- reset per-request state and replicas
 #pragma unroll 1
   for (int32_t j = U.lane; j < u.n; j += 32) {
@@ -673,7 +677,7 @@ __device__ void run_unit(Unit& U) {
   double next_arrival_time =
       u.n > 0 ? U.tm[U.arr_order ? U.arr_order[0] : 0].arrival : INFINITY;
   // a lone replica (no deferred pool) keeps its scheduler state in registers
-  const bool reg1 = R == 1 && c.routing != SSG_ROUTE_DEFERRED;
+  const bool reg1 = LONE ? true : (R == 1 && c.routing != SSG_ROUTE_DEFERRED);
   RepState S1;
   memset(&S1, 0, sizeof S1);
   // a lone replica's BatchStart queued by BatchComplete at the same clock is the
@@ -752,7 +756,9 @@ __device__ void run_unit(Unit& U) {
       if (next_arrival < u.n)
         next_arrival_time = U.tm[U.arr_order ? U.arr_order[next_arrival] : next_arrival].arrival;
       int dest = 0;
-      if (c.routing == SSG_ROUTE_RR) {
+      if (LONE) {
+        // the lone replica takes every arrival
+      } else if (c.routing == SSG_ROUTE_RR) {
         dest = rr_next;
         rr_next = (rr_next + 1) % R;
       } else if (c.routing == SSG_ROUTE_LO) {
@@ -854,7 +860,7 @@ __device__ void run_unit(Unit& U) {
       if (reg1) {
         S1 = S;
         direct = !FAST && S.ev_kind == 1 && !(next_arrival < u.n && next_arrival_time <= U.clock);
-      } else {
+      } else if (!LONE) {
         store_rep(U, r, S);
         drain_pool(U);
       }
@@ -905,7 +911,7 @@ __device__ void run_unit(Unit& U) {
 #else
 #define SSG_SIM_BOUNDS(FAST) __launch_bounds__(SSG_SIM_WARPS * 32, FAST ? SSG_SIM_FAST_MINB : SSG_SIM_MINB)
 #endif
-template <int FMA, int FOREST, int FAST>
+template <int FMA, int FOREST, int FAST, int LONE>
 __global__ void SSG_SIM_BOUNDS(FAST) k_simulate(SimLaunch L) {
   __shared__ int64_t stats[SSG_SIM_WARPS][SSG_MAX_PP * 6];
   __shared__ double part[SSG_SIM_WARPS][4 * SSG_MAX_PP];
@@ -946,7 +952,7 @@ __global__ void SSG_SIM_BOUNDS(FAST) k_simulate(SimLaunch L) {
   U.MB = U.cfg->max_batch;
   U.WC = U.u->wait_cap;
   U.rep_stride = 6LL * U.MB + U.WC;
-  run_unit<FMA, FOREST, FAST>(U);
+  run_unit<FMA, FOREST, FAST, LONE>(U);
 }
 
 // predict_batch / batch_device_flops for standalone compositions (the
@@ -1052,15 +1058,28 @@ void launch_simulate(const SimLaunch& L, cudaStream_t s) {
                  "k_simulate smem");
     kern<<<grid, block, smem, s>>>(L);
   };
-  switch (key) {
-    case 0: go(ssgk::k_simulate<0, 0, 0>); break;
-    case 1: go(ssgk::k_simulate<0, 0, 1>); break;
-    case 2: go(ssgk::k_simulate<0, 1, 0>); break;
-    case 3: go(ssgk::k_simulate<0, 1, 1>); break;
-    case 4: go(ssgk::k_simulate<1, 0, 0>); break;
-    case 5: go(ssgk::k_simulate<1, 0, 1>); break;
-    case 6: go(ssgk::k_simulate<1, 1, 0>); break;
-    default: go(ssgk::k_simulate<1, 1, 1>); break;
+  if (L.all_lone) {
+    switch (key) {
+      case 0: go(ssgk::k_simulate<0, 0, 0, 1>); break;
+      case 1: go(ssgk::k_simulate<0, 0, 1, 1>); break;
+      case 2: go(ssgk::k_simulate<0, 1, 0, 1>); break;
+      case 3: go(ssgk::k_simulate<0, 1, 1, 1>); break;
+      case 4: go(ssgk::k_simulate<1, 0, 0, 1>); break;
+      case 5: go(ssgk::k_simulate<1, 0, 1, 1>); break;
+      case 6: go(ssgk::k_simulate<1, 1, 0, 1>); break;
+      default: go(ssgk::k_simulate<1, 1, 1, 1>); break;
+    }
+  } else {
+    switch (key) {
+      case 0: go(ssgk::k_simulate<0, 0, 0, 0>); break;
+      case 1: go(ssgk::k_simulate<0, 0, 1, 0>); break;
+      case 2: go(ssgk::k_simulate<0, 1, 0, 0>); break;
+      case 3: go(ssgk::k_simulate<0, 1, 1, 0>); break;
+      case 4: go(ssgk::k_simulate<1, 0, 0, 0>); break;
+      case 5: go(ssgk::k_simulate<1, 0, 1, 0>); break;
+      case 6: go(ssgk::k_simulate<1, 1, 0, 0>); break;
+      default: go(ssgk::k_simulate<1, 1, 1, 0>); break;
+    }
   }
   cuda_check(cudaGetLastError(), "k_simulate launch");
 }

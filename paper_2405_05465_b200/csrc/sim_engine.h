@@ -31,6 +31,7 @@ struct SimLaunch {
   int32_t fast_forward;       // 1: pure-decode stretches of lone replicas take the fast loop
   int32_t has_forest;         // any estimator of the launch has forest models
   uint32_t* group_fail;       // per speculation group: bits of the probes that failed, may be null
+  int32_t all_lone;           // every unit is one replica without the deferred pool (LONE kernels)
 };
 
 namespace ssg {
@@ -40,6 +41,14 @@ int fast_forward_enabled();
 // probe warps are instruction-fetch bound); SSG_SWEEP_FASTFWD=1 turns it on.
 int sweep_fast_forward_enabled();
 void launch_simulate(const SimLaunch& L, cudaStream_t s);
+// True when every unit simulates one replica that does not route through the
+// deferred pool -- the launch may take the LONE kernel variant.
+template <class Units, class Configs>
+inline bool all_lone_units(const Units& units, const Configs& configs) {
+  for (const auto& u : units)
+    if (u.R != 1 || configs[u.config].routing == SSG_ROUTE_DEFERRED) return false;
+  return true;
+}
 // Builds the token tables of `n` configs (cfgs[i].tab_off / tab_stride set by
 // the caller); valid[i*stride + t] gets bit0 = token/comm terms valid, bit1 =
 // prefill-at-prior-0 valid.
