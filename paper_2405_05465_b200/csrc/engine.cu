@@ -81,7 +81,13 @@ __device__ SSG_COLD void drain_pool(Unit& U) {
 
 // One BatchStart event (sim.hpp:221-283).  Returns false when the unit must
 // stop (error or probe abort).
-template <int FMA, int FOREST>
+// request slot of the q-th arrival (LONE launches have no permutation)
+template <int LONE>
+__device__ __forceinline__ int32_t arrival_slot(const Unit& U, int32_t q) {
+  return (!LONE && U.arr_order) ? U.arr_order[q] : q;
+}
+
+template <int FMA, int FOREST, int LONE>
 __device__ bool batch_start(Unit& U, RepState& S, int r) {
   const SimConfig& c = *U.cfg;
   U.serial += 1;
@@ -103,7 +109,7 @@ __device__ bool batch_start(Unit& U, RepState& S, int r) {
   }
   // batch log (SimObserver::on_batch payload, before the abort check)
   int64_t log_hdr = -1;
-  if (U.u->flags & SSG_UF_BATCH_LOG) {
+  if (!LONE && (U.u->flags & SSG_UF_BATCH_LOG)) {
     // observer runs append the scheduler state the SimObserver may query:
     // outstanding, preemptions, ft_inflight, FT member count + ids (running order)
     const bool obs = (U.u->flags & SSG_UF_OBSERVER) != 0;
@@ -162,7 +168,7 @@ __device__ bool batch_start(Unit& U, RepState& S, int r) {
   }
   double lat = 0.0, flops = 0.0;
   if (batch_latency<FMA, FOREST>(U, S, r, &lat, &flops) != SSG_OK) return false;
-  if (log_hdr >= 0) wput(U, &U.log[log_hdr + 5], (int64_t)__double_as_longlong(lat));
+  if (!LONE && log_hdr >= 0) wput(U, &U.log[log_hdr + 5], (int64_t)__double_as_longlong(lat));
   S.busy_time = __dadd_rn(S.busy_time, lat);
   S.iterations += 1;
   S.tokens += tokens;
@@ -291,7 +297,7 @@ __global__ void k_build_tables(const SimConfig* __restrict__ cfgs, int32_t n, in
 // order, as the reference does).  The committed prefix ends before the first
 // iteration that breaks a condition, exactly where the one-iteration loop
 // stopped.
-template <int FMA>
+template <int FMA, int LONE>
 __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* next_arrival,
                                               double* next_arrival_time, double* flops_acc) {
   const SimConfig& c = *U.cfg;
@@ -367,7 +373,7 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
   const double* vals = U.E.dpool + md.values_off;
   const double* ax1 = U.E.dpool + md.axis_off[1];
   const bool emit_times = (U.u->flags & SSG_UF_EMISSIONS) != 0;
-  const bool logging = (U.u->flags & SSG_UF_BATCH_LOG) != 0;
+  const bool logging = !LONE && (U.u->flags & SSG_UF_BATCH_LOG) != 0;
   const double fa4 = od.fa;
   // emission slot of this runner's next token
   const int64_t ebase = (mine && emit_times) ? U.emit_base[j] + (U.hot[j].decode - rem) : 0;
@@ -503,14 +509,14 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
       double ta2 = ta;
       bool reject = false;
       while (ta2 <= c2) {  // arrivals during iteration K
-        const int32_t ja = U.arr_order ? U.arr_order[na2] : na2;
+        const int32_t ja = arrival_slot<LONE>(U, na2);
         const ReqHot h = U.hot[ja];
         if (units_for(c, (int64_t)h.prefill + h.decode) > c.total_units) {
           reject = true;  // enqueue raises: the event loop's
           break;
         }
         ++na2;
-        ta2 = na2 < U.u->n ? U.tm[U.arr_order ? U.arr_order[na2] : na2].arrival : INFINITY;
+        ta2 = na2 < U.u->n ? U.tm[arrival_slot<LONE>(U, na2)].arrival : INFINITY;
       }
       if (reject) break;
       clk = c2;
@@ -589,7 +595,7 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
     done += K;
     // the arrivals of the committed iterations: routed to the lone replica and
     // enqueued (sim.hpp:211-220); the replica is busy, so nothing starts
-    for (int32_t q = na0; q < na; ++q) enqueue(U, S, 0, U.arr_order ? U.arr_order[q] : q);
+    for (int32_t q = na0; q < na; ++q) enqueue(U, S, 0, arrival_slot<LONE>(U, q));
     *next_arrival = na;
     *next_arrival_time = ta;
     if (ends || K < 32) break;
@@ -605,7 +611,7 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
   return done;
 }
 
-template <int FMA>
+template <int FMA, int LONE>
 __device__ SSG_FFWD int fast_forward(Unit& U, RepState& S, int32_t* next_arrival,
                                      double* next_arrival_time, double* flops_acc) {
   const SimConfig& c = *U.cfg;
@@ -621,13 +627,14 @@ __device__ SSG_FFWD int fast_forward(Unit& U, RepState& S, int32_t* next_arrival
   const int nd = S.run_n, pp = c.pp;
   if (c.policy == SSG_POL_SARATHI ? nd > c.chunk : nd > c.max_tokens) return 0;
   if (nd > c.max_batch || (nd + pp - 1) / pp > c.tab_tmax) return 0;
-  return fast_forward_t<FMA>(U, S, next_arrival, next_arrival_time, flops_acc);
+  return fast_forward_t<FMA, LONE>(U, S, next_arrival, next_arrival_time, flops_acc);
 }
 
 // LONE = 1: every unit of the launch is one replica with round-robin or
-// least-outstanding routing (the sweep's decoupled probes), so the multi-replica
-// event selection, routing argmins, deferred pool and replica-state spills are
-// compiled out of the body (the kernel is instruction-fetch bound).
+// least-outstanding routing, without batch log or arrival permutation (the
+// sweep's decoupled probes), so the multi-replica event selection, routing
+// argmins, deferred pool, replica-state spills and log writers are compiled out
+// of the body (the kernel is instruction-fetch bound).
 template <int FMA, int FOREST, int FAST, int LONE>
 __device__ void run_unit(Unit& U) {
   const long long t_start = clock64();
@@ -675,7 +682,7 @@ __device__ void run_unit(Unit& U) {
   int32_t rr_next = 0;
   int64_t events = 0;
   double next_arrival_time =
-      u.n > 0 ? U.tm[U.arr_order ? U.arr_order[0] : 0].arrival : INFINITY;
+      u.n > 0 ? U.tm[arrival_slot<LONE>(U, 0)].arrival : INFINITY;
   // a lone replica (no deferred pool) keeps its scheduler state in registers
   const bool reg1 = LONE ? true : (R == 1 && c.routing != SSG_ROUTE_DEFERRED);
   RepState S1;
@@ -751,10 +758,10 @@ __device__ void run_unit(Unit& U) {
     ++events;
     if (bw == -1) {
       // ---- Arrival: route, enqueue, start_if_idle (sim.hpp:211-220)
-      const int32_t j = U.arr_order ? U.arr_order[next_arrival] : next_arrival;
+      const int32_t j = arrival_slot<LONE>(U, next_arrival);
       ++next_arrival;
       if (next_arrival < u.n)
-        next_arrival_time = U.tm[U.arr_order ? U.arr_order[next_arrival] : next_arrival].arrival;
+        next_arrival_time = U.tm[arrival_slot<LONE>(U, next_arrival)].arrival;
       int dest = 0;
       if (LONE) {
         // the lone replica takes every arrival
@@ -810,7 +817,7 @@ __device__ void run_unit(Unit& U) {
       // loop would reach; afterwards the replica is again "BatchStart at clock"
       double fl = U.out->flops;
       const int32_t na_before = next_arrival;
-      const int k = fast_forward<FMA>(U, S, &next_arrival, &next_arrival_time, &fl);
+      const int k = fast_forward<FMA, LONE>(U, S, &next_arrival, &next_arrival_time, &fl);
 #ifdef SSG_FF_STATS
       if (U.lane == 0) {
         atomicAdd(&g_ff_stats[0], 1ull);
@@ -836,7 +843,7 @@ __device__ void run_unit(Unit& U) {
         break;
       }
       S.ev_kind = 0;
-      const bool ok = batch_start<FMA, FOREST>(U, S, r);
+      const bool ok = batch_start<FMA, FOREST, LONE>(U, S, r);
       if (reg1)
         S1 = S;
       else

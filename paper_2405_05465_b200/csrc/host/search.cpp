@@ -494,7 +494,7 @@ void run_launch(SweepLane& lane, ProbeLaunch& L, const ResidentWorkload& w,
   K.fast_forward = sweep_fast_forward_enabled() ||
                    static_cast<int64_t>(L.units.size()) <= ff_units ? 1 : 0;
   K.has_forest = L.has_forest ? 1 : 0;
-  K.all_lone = all_lone_units(L.units, L.configs) ? 1 : 0;
+  K.all_lone = all_lone_units(K, L.units, L.configs) ? 1 : 0;
   K.group_fail = nullptr;
   if (L.ngroups > 0) {
     B.group_fail.resize(L.ngroups);

@@ -332,7 +332,7 @@ void run_jobs(const SimJobs& J, SimResults& R, bool want_requests) {
   for (const auto& u : J.units) observed = observed || (u.flags & SSG_UF_OBSERVER);
   L.fast_forward = fast_forward_enabled() && !observed;
   L.has_forest = J.has_forest ? 1 : 0;
-  L.all_lone = all_lone_units(J.units, J.configs) ? 1 : 0;
+  L.all_lone = all_lone_units(L, J.units, J.configs) ? 1 : 0;
   cudaEvent_t ev0, ev1;
   cuda_check(cudaEventCreate(&ev0), "event");
   cuda_check(cudaEventCreate(&ev1), "event");

@@ -42,11 +42,15 @@ int fast_forward_enabled();
 int sweep_fast_forward_enabled();
 void launch_simulate(const SimLaunch& L, cudaStream_t s);
 // True when every unit simulates one replica that does not route through the
-// deferred pool -- the launch may take the LONE kernel variant.
+// deferred pool and the launch has no batch log and no arrival permutation --
+// the launch may take the LONE kernel variant.
 template <class Units, class Configs>
-inline bool all_lone_units(const Units& units, const Configs& configs) {
+inline bool all_lone_units(const SimLaunch& L, const Units& units, const Configs& configs) {
+  if (L.log || L.arr_order) return false;
   for (const auto& u : units)
-    if (u.R != 1 || configs[u.config].routing == SSG_ROUTE_DEFERRED) return false;
+    if (u.R != 1 || configs[u.config].routing == SSG_ROUTE_DEFERRED ||
+        (u.flags & (SSG_UF_BATCH_LOG | SSG_UF_OBSERVER)))
+      return false;
   return true;
 }
 // Builds the token tables of `n` configs (cfgs[i].tab_off / tab_stride set by
