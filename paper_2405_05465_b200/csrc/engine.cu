@@ -95,7 +95,9 @@ __device__ bool batch_start(Unit& U, RepState& S, int r) {
   S.nd = 0;
   U.plan_tokens = 0;
   U.plan_late = 0;
+  SSG_PH_BEGIN(ph_s);
   schedule_batch(U, S, r);
+  SSG_PH_END(ph_s, 0);
   if (failed(U)) return false;
   if (S.np + S.nd == 0) {
     S.busy = 0;
@@ -167,7 +169,10 @@ __device__ bool batch_start(Unit& U, RepState& S, int r) {
     }
   }
   double lat = 0.0, flops = 0.0;
-  if (batch_latency<FMA, FOREST>(U, S, r, &lat, &flops) != SSG_OK) return false;
+  SSG_PH_BEGIN(ph_l);
+  const int lat_code = batch_latency<FMA, FOREST>(U, S, r, &lat, &flops);
+  SSG_PH_END(ph_l, 1);
+  if (lat_code != SSG_OK) return false;
   if (!LONE && log_hdr >= 0) wput(U, &U.log[log_hdr + 5], (int64_t)__double_as_longlong(lat));
   S.busy_time = __dadd_rn(S.busy_time, lat);
   S.iterations += 1;
@@ -342,9 +347,12 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
   const SsgModelDesc& md = U.E.models[od.slot];
   if (md.kind != SSG_KIND_INTERP || !c.tab_cells) return 0;
   const int my_m = lane % pp;
+  // context sums per microbatch: 32 contexts below 2^26 sum in 31 bits (one REDUX each)
+  if (!__all_sync(SSG_FULL, (kv >> 26) == 0)) return 0;
   int64_t ctx_m = 0;
+#pragma unroll 1
   for (int m = 0; m < nm; ++m) {
-    const int64_t cm = warp_sum64(mine && my_m == m ? (int64_t)kv + 1 : 0);
+    const unsigned cm = __reduce_add_sync(SSG_FULL, mine && my_m == m ? (unsigned)kv + 1u : 0u);
     if (lane == m) ctx_m = cm;
   }
   const int nd_m = lane < nm ? (nd - lane + pp - 1) / pp : 0;
@@ -368,10 +376,6 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
     lo0 = (int32_t)tab[8LL * T1 + nd_m];
   }
   if (!__all_sync(SSG_FULL, ok)) { FFSTAT(11); return 0; }
-  const int32_t n1 = md.axis_len[1];
-  const int32_t h0 = md.axis_len[0] == 1 ? 0 : 1;
-  const double* vals = U.E.dpool + md.values_off;
-  const double* ax1 = U.E.dpool + md.axis_off[1];
   const bool emit_times = (U.u->flags & SSG_UF_EMISSIONS) != 0;
   const bool logging = !LONE && (U.u->flags & SSG_UF_BATCH_LOG) != 0;
   const double fa4 = od.fa;
@@ -416,27 +420,16 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
         double cs[3];
 #pragma unroll
         for (int q = 0; q < 3; ++q) cs[q] = __shfl_sync(SSG_FULL, comm_sum[q], m);
-        const double g0 = __dsub_rn(1.0, f0m);
-        const double w0lo = g0, w0hi = h0 ? f0m : g0;
-        const int64_t r0 = (int64_t)lo0m * n1, r1 = (int64_t)(lo0m + h0) * n1;
         const double v1 = __dmul_rn((double)(cm0 + (int64_t)k * ndm), od.kvb);
-        if (!(v1 >= md.lower[1] && v1 <= md.upper[1])) {
+        // the batch latency's attention query (one out-of-line copy); v0 = ndm
+        // passed the bounding box on entry
+        const AttnQuery aq = ssg_attn_interp<FMA>(U.E.dpool, &md, (double)ndm, v1, lo0m, f0m, U.ax1_hint);
+        U.ax1_hint = aq.hint;
+        if (aq.code != SSG_OK) {
           good = 0;
         } else {
-          int32_t lo1;
-          double f1;
-          ssg_axis_cell_hint(ax1, n1, hot_log1p<FMA>(v1), &U.ax1_hint, &lo1, &f1);
-          const int32_t h1 = n1 == 1 ? 0 : 1;
-          const double g1 = __dsub_rn(1.0, f1);
-          const double w1lo = g1, w1hi = h1 ? f1 : g1;
-          double r = __dmul_rn(__dmul_rn(w1lo, w0lo), __ldg(vals + r0 + lo1));
-          r = __dadd_rn(r, __dmul_rn(__dmul_rn(w1lo, w0hi), __ldg(vals + r1 + lo1)));
-          r = __dadd_rn(r, __dmul_rn(__dmul_rn(w1hi, w0lo), __ldg(vals + r0 + lo1 + h1)));
-          r = __dadd_rn(r, __dmul_rn(__dmul_rn(w1hi, w0hi), __ldg(vals + r1 + lo1 + h1)));
-          if (!ssg_exp_in_range(r)) {
-            good = 0;
-          } else {
-            const double pred = __dmul_rn(od.count, hot_exp<FMA>(r));
+          {
+            const double pred = __dmul_rn(od.count, aq.pred);
             double acc = __dadd_rn(ts, pred);
 #pragma unroll
             for (int q = 0; q < 3; ++q)
@@ -794,8 +787,10 @@ __device__ void run_unit(Unit& U) {
         continue;
       }
       RepState S = reg1 ? S1 : load_rep(U, dest);
+      SSG_PH_BEGIN(ph_a);
       const bool ok = enqueue(U, S, dest, j);
       if (ok) start_if_idle(U, S);
+      SSG_PH_END(ph_a, 4);
       if (reg1)
         S1 = S;
       else
@@ -817,7 +812,13 @@ __device__ void run_unit(Unit& U) {
       // loop would reach; afterwards the replica is again "BatchStart at clock"
       double fl = U.out->flops;
       const int32_t na_before = next_arrival;
+      SSG_PH_BEGIN(ph_f);
       const int k = fast_forward<FMA, LONE>(U, S, &next_arrival, &next_arrival_time, &fl);
+      SSG_PH_END(ph_f, 3);
+#ifdef SSG_PHASE_CYCLES
+      U.ph[5] += k;
+      U.ph[7] += 1;
+#endif
 #ifdef SSG_FF_STATS
       if (U.lane == 0) {
         atomicAdd(&g_ff_stats[0], 1ull);
@@ -852,7 +853,9 @@ __device__ void run_unit(Unit& U) {
     } else {
       // ---- BatchComplete (sim.hpp:284-293)
       S.ev_kind = 0;
+      SSG_PH_BEGIN(ph_c);
       complete_batch(U, S, r);
+      SSG_PH_END(ph_c, 2);
       S.np = 0;
       S.nd = 0;
       S.busy = 0;
@@ -887,6 +890,9 @@ __device__ void run_unit(Unit& U) {
     U.out->qbytes = U.qbytes;
     U.out->cycles = clock64() - t_start;
   }
+#ifdef SSG_PHASE_CYCLES
+  U.ph[6] = clock64() - t_start;
+#endif
   __syncwarp();
   if (!failed(U) && !U.out->aborted) {
     // "simulation drained with unfinished request" (sim.hpp:305-306)
@@ -918,6 +924,11 @@ __device__ void run_unit(Unit& U) {
 #else
 #define SSG_SIM_BOUNDS(FAST) __launch_bounds__(SSG_SIM_WARPS * 32, FAST ? SSG_SIM_FAST_MINB : SSG_SIM_MINB)
 #endif
+#ifdef SSG_PHASE_CYCLES
+#define SSG_PHASE_MAX_UNITS 16384
+__device__ long long g_phase[SSG_PHASE_MAX_UNITS][8];
+#endif
+
 template <int FMA, int FOREST, int FAST, int LONE>
 __global__ void SSG_SIM_BOUNDS(FAST) k_simulate(SimLaunch L) {
   __shared__ int64_t stats[SSG_SIM_WARPS][SSG_MAX_PP * 6];
@@ -959,7 +970,14 @@ __global__ void SSG_SIM_BOUNDS(FAST) k_simulate(SimLaunch L) {
   U.MB = U.cfg->max_batch;
   U.WC = U.u->wait_cap;
   U.rep_stride = 6LL * U.MB + U.WC;
+#ifdef SSG_PHASE_CYCLES
+  for (int k = 0; k < 8; ++k) U.ph[k] = 0;
+#endif
   run_unit<FMA, FOREST, FAST, LONE>(U);
+#ifdef SSG_PHASE_CYCLES
+  if (U.lane == 0 && uid < SSG_PHASE_MAX_UNITS)
+    for (int k = 0; k < 8; ++k) g_phase[uid][k] = U.ph[k];
+#endif
 }
 
 // predict_batch / batch_device_flops for standalone compositions (the
@@ -1032,6 +1050,18 @@ void launch_build_tables(const SimConfig* d_cfgs, int32_t n, int32_t stride,
   ssgk::k_build_tables<<<grid, 128, 0, s>>>(d_cfgs, n, stride, d_ests, d_pool, d_valid);
   cuda_check(cudaGetLastError(), "k_build_tables launch");
   stats().launches_setup += 1;
+}
+
+bool phase_cycles(long long* dst, int64_t n) {
+#ifdef SSG_PHASE_CYCLES
+  n = n < SSG_PHASE_MAX_UNITS ? n : SSG_PHASE_MAX_UNITS;
+  cuda_check(cudaMemcpyFromSymbol(dst, ssgk::g_phase, n * 8 * sizeof(long long)), "phase cycles");
+  return true;
+#else
+  (void)dst;
+  (void)n;
+  return false;
+#endif
 }
 
 int fast_forward_enabled() {

@@ -86,7 +86,22 @@ struct Unit {
   // counted while the scheduler forms a batch (reset by batch_start):
   int32_t plan_tokens; // prefill chunk tokens pushed
   int32_t plan_late;   // requests first scheduled now, later than the abort threshold
+#ifdef SSG_PHASE_CYCLES
+  long long ph[8];     // diagnostic build: cycles per event-loop phase (SSG_PH_*)
+#endif
 };
+
+// Diagnostic builds (-DSSG_PHASE_CYCLES) charge clock64 deltas to phases:
+// 0 schedule, 1 batch latency, 2 batch complete, 3 fast-forward calls,
+// 4 arrivals, 5 fast-forwarded iterations (a count), 6 whole unit,
+// 7 fast-forward calls (a count).
+#ifdef SSG_PHASE_CYCLES
+#define SSG_PH_BEGIN(v) const long long v = clock64()
+#define SSG_PH_END(v, k) (U.ph[k] += clock64() - (v))
+#else
+#define SSG_PH_BEGIN(v)
+#define SSG_PH_END(v, k)
+#endif
 
 // ---------------------------------------------------------------- workspace
 __device__ __forceinline__ int32_t* rep_ws(Unit& U, int r) { return U.ws + r * U.rep_stride; }
@@ -881,6 +896,23 @@ static __device__ SSG_COLD void batch_latency_full(Unit& U, const int64_t* st, i
   __syncwarp();
 }
 
+// Result of one attention query: the prediction, SSG_OK or the error code
+// with the failing feature, and the axis-1 cell for the lane's next search.
+struct AttnQuery {
+  double pred;
+  int32_t code;
+  int32_t bad;
+  int32_t hint;
+};
+
+// One out-of-line copy serves the batch latency and the decode fast-forward
+// (the kernel is instruction-fetch bound: SSG_ATTN_INLINE=1 inlines both, A/B).
+#ifdef SSG_ATTN_INLINE
+#define SSG_ATTN_QUERY __forceinline__
+#else
+#define SSG_ATTN_QUERY __noinline__
+#endif
+
 // EstimatorModel::predict of one attention query on a 2-D interpolator whose
 // axis-0 cell at the integer v0 comes from the token tables (lo0, f0 =
 // ssg_axis_cell(log1p(v0)), computed by k_build_tables with the same code) and
@@ -889,23 +921,29 @@ static __device__ SSG_COLD void batch_latency_full(Unit& U, const int64_t* st, i
 // cell, the fraction and every later operation are the reference's.
 // estimator.hpp:105-123, regressor.hpp:308-341.
 template <int FMA>
-__device__ __forceinline__ int ssg_attn_interp(const SsgEstView& E, const SsgModelDesc& m, double v0,
-                                               double v1, int32_t lo0, double f0, int32_t& hint,
-                                               double* out, int* bad_feature) {
-  if (!(v0 >= m.lower[0] && v0 <= m.upper[0])) {
-    *bad_feature = 0;
-    return SSG_ERR_BBOX;
+__device__ SSG_ATTN_QUERY AttnQuery ssg_attn_interp(const double* __restrict__ dpool,
+                                                    const SsgModelDesc* __restrict__ m, double v0,
+                                                    double v1, int32_t lo0, double f0, int32_t hint) {
+  AttnQuery q;
+  q.pred = 0.0;
+  q.code = SSG_OK;
+  q.bad = 0;
+  q.hint = hint;
+  if (!(v0 >= m->lower[0] && v0 <= m->upper[0])) {
+    q.code = SSG_ERR_BBOX;
+    return q;
   }
-  if (!(v1 >= m.lower[1] && v1 <= m.upper[1])) {
-    *bad_feature = 1;
-    return SSG_ERR_BBOX;
+  if (!(v1 >= m->lower[1] && v1 <= m->upper[1])) {
+    q.code = SSG_ERR_BBOX;
+    q.bad = 1;
+    return q;
   }
-  const int32_t n1 = m.axis_len[1];
+  const int32_t n1 = m->axis_len[1];
   int32_t lo1;
   double f1;
-  ssg_axis_cell_hint(E.dpool + m.axis_off[1], n1, hot_log1p<FMA>(v1), &hint, &lo1, &f1);
-  const int32_t n0 = m.axis_len[0];
-  const double* vals = E.dpool + m.values_off;
+  ssg_axis_cell_hint(dpool + m->axis_off[1], n1, hot_log1p<FMA>(v1), &q.hint, &lo1, &f1);
+  const int32_t n0 = m->axis_len[0];
+  const double* vals = dpool + m->values_off;
   const int32_t h0 = n0 == 1 ? 0 : 1;
   const int32_t h1 = n1 == 1 ? 0 : 1;
   const double g0 = __dsub_rn(1.0, f0), g1 = __dsub_rn(1.0, f1);
@@ -916,9 +954,12 @@ __device__ __forceinline__ int ssg_attn_interp(const SsgEstView& E, const SsgMod
   acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(w1lo, w0hi), __ldg(vals + r1 + lo1)));
   acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(w1hi, w0lo), __ldg(vals + r0 + lo1 + h1)));
   acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(w1hi, w0hi), __ldg(vals + r1 + lo1 + h1)));
-  if (!ssg_exp_in_range(acc)) return SSG_ERR_EXP_RANGE;
-  *out = hot_exp<FMA>(acc);
-  return SSG_OK;
+  if (!ssg_exp_in_range(acc)) {
+    q.code = SSG_ERR_EXP_RANGE;
+    return q;
+  }
+  q.pred = hot_exp<FMA>(acc);
+  return q;
 }
 
 template <int FMA, int FOREST>
@@ -1055,7 +1096,11 @@ __device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, doubl
         const int64_t row = is_dec ? 7 : 9;
         const double f0 = tab[row * T1 + t0];
         const int32_t lo0 = (int32_t)tab[(row + 1) * T1 + t0];
-        code = ssg_attn_interp<FMA>(U.E, U.E.models[o.slot], v0, v1, lo0, f0, U.ax1_hint, &pred, &bad);
+        const AttnQuery aq = ssg_attn_interp<FMA>(U.E.dpool, U.E.models + o.slot, v0, v1, lo0, f0, U.ax1_hint);
+        code = aq.code;
+        bad = aq.bad;
+        pred = aq.pred;
+        U.ax1_hint = aq.hint;
       } else {
         code = ssg_predict_t<FMA, FOREST>(U.E, o.slot, v0, v1, &pred, &bad);
       }
