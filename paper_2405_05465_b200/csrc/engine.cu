@@ -309,18 +309,18 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
   const int nd = S.run_n, pp = c.pp;
   if (pp > SSG_FF_MAX_PP) return 0;  // deeper pipelines take the normal path
   const int nm = nd < pp ? nd : pp;  // non-empty microbatches
-  {
-    // cheapest exit first: iteration 0 completes no earlier than
-    // clock + S6[size of microbatch 0] + cpu overhead (every further term of
-    // the latency is a non-negative prediction, and round-to-nearest adds of
-    // non-negative terms never decrease), so an arrival at or before that
-    // point stops the stretch before it starts
-    const double lb = __dadd_rn(U.tables[c.tab_off + (nd + pp - 1) / pp], c.cpu_overhead);
-    if (!SSG_FF_ARRIVE_ONE && nd < c.max_batch && *next_arrival < U.u->n &&
-        *next_arrival_time <= __dadd_rn(U.clock, lb)) {
-      FFSTAT(9);
-      return 0;
-    }
+  // cheapest exit first: iteration 0 completes no earlier than
+  // clock + S6[size of microbatch 0] + cpu overhead (every further term of
+  // the latency is a non-negative prediction, and round-to-nearest adds of
+  // non-negative terms never decrease), so an arrival at or before that
+  // point stops the stretch before it starts.  The same bound holds for every
+  // iteration of the stretch (same microbatch sizes).
+  const double lb = __dadd_rn(U.tables[c.tab_off + (nd + pp - 1) / pp], c.cpu_overhead);
+  const bool arrivals_end = nd < c.max_batch;  // an arrival ends the stretch
+  if (!SSG_FF_ARRIVE_ONE && arrivals_end && *next_arrival < U.u->n &&
+      *next_arrival_time <= __dadd_rn(U.clock, lb)) {
+    FFSTAT(9);
+    return 0;
   }
   const int lane = U.lane;
   const bool mine = lane < nd;
@@ -342,38 +342,42 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
   }
   const int max_iters = min_rem - 1;
   if (max_iters < 1) { FFSTAT(10); return 0; }
-  // per-microbatch invariants on lane m < nm: size, context sum, decode model cell
   const SimOp& od = c.ops[c.idx_dec];
   const SsgModelDesc& md = U.E.models[od.slot];
   if (md.kind != SSG_KIND_INTERP || !c.tab_cells) return 0;
-  const int my_m = lane % pp;
-  // context sums per microbatch: 32 contexts below 2^26 sum in 31 bits (one REDUX each)
-  if (!__all_sync(SSG_FULL, (kv >> 26) == 0)) return 0;
-  int64_t ctx_m = 0;
+  // contexts and block counts below 2^26: every 32-lane sum below fits 31 bits
+  if (!__all_sync(SSG_FULL, (kv >> 26) == 0) || c.total_units >= (1LL << 26)) return 0;
+  // lane layout of a round: P lanes per iteration (lane = it * P + m), one
+  // lane per microbatch, so each lane makes one attention query per round
+  const int P = pp == 1 ? 1 : (pp == 2 ? 2 : 4);
+  const int lgP = pp == 1 ? 0 : (pp == 2 ? 1 : 2);
+  const int KI = 32 >> lgP;  // iterations per round
+  const int q_m = lane & (P - 1), q_it = lane >> lgP;
+  const bool q_on = q_m < nm;
+  // microbatch q_m's invariants: size, context sum, token-table terms, axis-0 cell
+  int64_t ctx_q = 0;
+  const int run_m = lane % pp;  // runner lane -> its microbatch
 #pragma unroll 1
   for (int m = 0; m < nm; ++m) {
-    const unsigned cm = __reduce_add_sync(SSG_FULL, mine && my_m == m ? (unsigned)kv + 1u : 0u);
-    if (lane == m) ctx_m = cm;
+    const unsigned cm = __reduce_add_sync(SSG_FULL, mine && run_m == m ? (unsigned)kv + 1u : 0u);
+    if (q_m == m) ctx_q = cm;
   }
-  const int nd_m = lane < nm ? (nd - lane + pp - 1) / pp : 0;
+  const int nd_q = q_on ? (nd - q_m + pp - 1) / pp : 0;
   const double* tab = U.tables + c.tab_off;
   const int T1 = c.tab_stride;
-  double tok_s = 0.0, tok_f = 0.0, comm_sum[3] = {0.0, 0.0, 0.0};
+  double tok_s = 0.0, tok_f = 0.0, comm_q = 0.0;
   int32_t lo0 = 0;
   double f0 = 0.0;
   bool ok = true;
-  if (lane < nm) {
-    tok_s = tab[nd_m];
-    tok_f = tab[(int64_t)T1 + nd_m];
-#pragma unroll
-    for (int k = 0; k < 3; ++k)
-      if (k < c.ncomm) comm_sum[k] = tab[(int64_t)(2 + k) * T1 + nd_m];
-    const double v0 = (double)nd_m;
+  if (q_on) {
+    tok_s = tab[nd_q];
+    tok_f = tab[(int64_t)T1 + nd_q];
+    const double v0 = (double)nd_q;
     ok = v0 >= md.lower[0] && v0 <= md.upper[0];
-    // the axis-0 cell at v0 = nd_m from the token tables (k_build_tables computes
+    // the axis-0 cell at v0 = nd_q from the token tables (k_build_tables computes
     // ssg_axis_cell(log1p(t)) with the same code; tab_cells is checked on entry)
-    f0 = tab[7LL * T1 + nd_m];
-    lo0 = (int32_t)tab[8LL * T1 + nd_m];
+    f0 = tab[7LL * T1 + nd_q];
+    lo0 = (int32_t)tab[8LL * T1 + nd_q];
   }
   if (!__all_sync(SSG_FULL, ok)) { FFSTAT(11); return 0; }
   const bool emit_times = (U.u->flags & SSG_UF_EMISSIONS) != 0;
@@ -382,96 +386,107 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
   // emission slot of this runner's next token
   const int64_t ebase = (mine && emit_times) ? U.emit_base[j] + (U.hot[j].decode - rem) : 0;
   const int64_t free0 = c.total_units;
+  const double tp_pp = (double)(c.tp * c.pp);
   int done = 0;
   while (done < max_iters) {
-    const int k = done + lane;  // this lane's iteration
-    const bool active = k < max_iters;
-    // ---- schedule: every runner reserves kv+k+1 tokens (no preemption allowed)
+    // iterations this round: at most KI, and (when an arrival ends the stretch)
+    // no more than can complete before the next arrival, each lasting >= lb
+    int KIr = max_iters - done < KI ? max_iters - done : KI;
+    if (arrivals_end && *next_arrival < U.u->n) {
+      const double gap = __dsub_rn(*next_arrival_time, U.clock);
+      const double est = gap / lb + 2.0;
+      if (est < (double)KIr) KIr = est < 1.0 ? 1 : (int)est;
+    }
+    const int k = done + q_it;  // this lane's iteration
+    const bool active = q_it < KIr;
+    // ---- schedule: every runner reserves kv+k+1 tokens (no preemption allowed);
+    // lanes over runners, one warp sum per iteration
     int64_t need = 0;
 #pragma unroll 1
-    for (int r = 0; r < nd; ++r) {
-      const int32_t kv_r = __shfl_sync(SSG_FULL, kv, r);
-      const int32_t held_r = __shfl_sync(SSG_FULL, held, r);
-      int64_t hk = held_r;
-      if (k > 0) {
-        const int64_t u = units_for(c, (int64_t)kv_r + k);
-        hk = hk < u ? u : hk;
+    for (int i = 0; i < KIr; ++i) {
+      const int ki = done + i;
+      uint32_t sr = 0;
+      if (mine) {
+        int64_t hk = held;
+        if (ki > 0) {
+          const int64_t u = units_for(c, (int64_t)kv + ki);
+          hk = hk < u ? u : hk;
+        }
+        const int64_t s = units_for(c, (int64_t)kv + ki + 1) - hk;
+        sr = s > 0 ? (uint32_t)s : 0u;
       }
-      const int64_t s = units_for(c, (int64_t)kv_r + k + 1) - hk;
-      need += s > 0 ? s : 0;
+      const unsigned tot = __reduce_add_sync(SSG_FULL, sr);
+      if (q_it == i) need = tot;
     }
-    // ---- cost: decode attention per microbatch, operator order, makespan
-    // one rolled pass over the microbatches: the attention query (log1p, cell,
-    // interpolation, exp) is emitted once, not once per microbatch slot
+    // ---- cost: lane (it, m) queries microbatch m's decode attention of iteration it
+    double tim_l = 0.0, fl_l = 0.0;
+    bool good_l = true;
+    if (active && q_on) {
+      const double v1 = __dmul_rn((double)(ctx_q + (int64_t)k * nd_q), od.kvb);
+      // the batch latency's attention query (one out-of-line copy); v0 = nd_q
+      // passed the bounding box on entry
+      const AttnQuery aq = ssg_attn_interp<FMA>(U.E.dpool, &md, (double)nd_q, v1, lo0, f0, U.ax1_hint);
+      U.ax1_hint = aq.hint;
+      if (aq.code != SSG_OK) {
+        good_l = false;
+      } else {
+        double acc = __dadd_rn(tok_s, __dmul_rn(od.count, aq.pred));
+        // comm ops (at most 3), op order
+        const double* comm = tab + 2 * (int64_t)T1 + nd_q;
+        if (c.ncomm > 0) acc = __dadd_rn(acc, comm[0]);
+        if (c.ncomm > 1) acc = __dadd_rn(acc, comm[T1]);
+        if (c.ncomm > 2) acc = __dadd_rn(acc, comm[2 * (int64_t)T1]);
+        const double ctx_tokens = v1 / od.kvb;
+        fl_l = __dadd_rn(tok_f, __dmul_rn(od.count, __dmul_rn(__dmul_rn(4.0, ctx_tokens), fa4)));
+        good_l = acc > 0.0;
+        tim_l = acc;
+      }
+    }
+    // ---- per iteration (its P lanes): flops in microbatch order, makespan
+    const int base = lane & ~(P - 1);
+    const unsigned badm = __ballot_sync(SSG_FULL, !good_l);
+    const bool good = ((badm >> base) & ((1u << P) - 1u)) == 0u;
     double tim[SSG_FF_MAX_PP];
     double fl_tot = 0.0;
-    int good = 1;
 #pragma unroll
-    for (int m = 0; m < SSG_FF_MAX_PP; ++m) tim[m] = 0.0;
-#pragma unroll 1
-    for (int m = 0; m < nm; ++m) {
-      {
-        const int64_t cm0 = __shfl_sync(SSG_FULL, ctx_m, m);
-        const int ndm = __shfl_sync(SSG_FULL, nd_m, m);
-        const int32_t lo0m = __shfl_sync(SSG_FULL, lo0, m);
-        const double f0m = __shfl_sync(SSG_FULL, f0, m);
-        const double ts = __shfl_sync(SSG_FULL, tok_s, m);
-        const double tf = __shfl_sync(SSG_FULL, tok_f, m);
-        double cs[3];
-#pragma unroll
-        for (int q = 0; q < 3; ++q) cs[q] = __shfl_sync(SSG_FULL, comm_sum[q], m);
-        const double v1 = __dmul_rn((double)(cm0 + (int64_t)k * ndm), od.kvb);
-        // the batch latency's attention query (one out-of-line copy); v0 = ndm
-        // passed the bounding box on entry
-        const AttnQuery aq = ssg_attn_interp<FMA>(U.E.dpool, &md, (double)ndm, v1, lo0m, f0m, U.ax1_hint);
-        U.ax1_hint = aq.hint;
-        if (aq.code != SSG_OK) {
-          good = 0;
-        } else {
-          {
-            const double pred = __dmul_rn(od.count, aq.pred);
-            double acc = __dadd_rn(ts, pred);
-#pragma unroll
-            for (int q = 0; q < 3; ++q)
-              if (q < c.ncomm) acc = __dadd_rn(acc, cs[q]);
-            const double ctx_tokens = v1 / od.kvb;
-            const double fl = __dadd_rn(tf, __dmul_rn(od.count, __dmul_rn(__dmul_rn(4.0, ctx_tokens), fa4)));
-            if (!(acc > 0.0)) good = 0;
-            tim[m] = acc;
-            if (pp == 1)
-              fl_tot = __dmul_rn(fl, (double)c.tp);
-            else
-              fl_tot = __dadd_rn(fl_tot, __dmul_rn(fl, (double)(c.tp * c.pp)));
-          }
-        }
-      }
+    for (int m = 0; m < SSG_FF_MAX_PP; ++m) {
+      const double tm = __shfl_sync(SSG_FULL, tim_l, (base + m) & 31);
+      const double fm = __shfl_sync(SSG_FULL, fl_l, (base + m) & 31);
+      tim[m] = tm;
+      if (m < nm) fl_tot = pp == 1 ? __dmul_rn(fm, (double)c.tp) : __dadd_rn(fl_tot, __dmul_rn(fm, tp_pp));
     }
     double lat;
     if (pp == 1) {
       lat = tim[0];
     } else {
-      // synchronous pipeline finish times (scheduler.hpp:566-579)
+      // synchronous pipeline finish times (scheduler.hpp:566-579), in registers
       double fin[SSG_FF_MAX_PP];
 #pragma unroll
       for (int m = 0; m < SSG_FF_MAX_PP; ++m) fin[m] = 0.0;
 #pragma unroll 1
       for (int st = 0; st < pp; ++st) {
         double prev = 0.0;
-#pragma unroll 1
-        for (int m = 0; m < nm; ++m) {
-          const double start = fin[m] < prev ? prev : fin[m];
-          prev = __dadd_rn(start, tim[m]);
-          fin[m] = prev;
+#pragma unroll
+        for (int m = 0; m < SSG_FF_MAX_PP; ++m) {
+          if (m < nm) {
+            const double start = fin[m] < prev ? prev : fin[m];
+            prev = __dadd_rn(start, tim[m]);
+            fin[m] = prev;
+          }
         }
       }
-      lat = fin[nm - 1];
+      lat = fin[0];
+#pragma unroll
+      for (int m = 1; m < SSG_FF_MAX_PP; ++m)
+        if (m < nm) lat = fin[m];
     }
     lat = __dadd_rn(lat, c.cpu_overhead);
     // ---- the order-dependent parts, in iteration order
     // allocation before this lane's iteration: exclusive prefix of the needs
+    // (a scan over the iteration groups: shifts by multiples of P)
     int64_t incl = need;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll 1
+    for (int o = P; o < 32; o <<= 1) {
       const int64_t t = __shfl_up_sync(SSG_FULL, incl, o);
       if (lane >= o) incl += t;
     }
@@ -480,14 +495,14 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
     // iterations that can happen as far as memory and the cost go
     const bool pre = active && fits && good && lat > 0.0;
     const unsigned bad = __ballot_sync(SSG_FULL, !pre);
-    const int C = bad ? __ffs(bad) - 1 : 32;
+    const int C = bad ? (__ffs(bad) - 1) >> lgP : KI;
     if (C == 0) { if (done == 0) FFSTAT(12); break; }
     // clock / busy time / flops: one fp64 add per iteration, in order; the
     // chain (warp-uniform) stops at the first completion at or after the next
     // arrival: an arrival at or before a completion is processed between the
     // batch's start and completion events, so that iteration is the loop's
     double clk = U.clock, busy = S.busy_time, fla = *flops_acc;
-    double t_done = 0.0;
+    double t_done = 0.0;  // on lane i: completion of the round's iteration i
     int K = 0;
     const int32_t na0 = *next_arrival;
     int32_t na = na0;                  // arrivals up to the last committed completion
@@ -495,8 +510,8 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
     double ta = na0 < U.u->n ? *next_arrival_time : INFINITY;
     bool ends = false;                 // an arrival ends the stretch after iteration K
     for (; K < C; ++K) {
-      const double li = __shfl_sync(SSG_FULL, lat, K);
-      const double fi = __shfl_sync(SSG_FULL, fl_tot, K);
+      const double li = __shfl_sync(SSG_FULL, lat, K << lgP);
+      const double fi = __shfl_sync(SSG_FULL, fl_tot, K << lgP);
       const double c2 = __dadd_rn(clk, li);
       int32_t na2 = na;
       double ta2 = ta;
@@ -519,7 +534,7 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
       const bool arrived = na2 != na;
       na = na2;
       ta = ta2;
-      if (arrived && nd < c.max_batch) {
+      if (arrived && arrivals_end) {
         ends = true;
         ++K;
         break;
@@ -527,7 +542,8 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
     }
     if (K == 0) { if (done == 0) FFSTAT(13); break; }
     const int last = K - 1;
-    // ---- commit iterations done .. done+K-1
+    // ---- commit iterations done .. done+K-1 (from here on lane i <-> iteration done+i)
+    const int kit = done + lane;
     if (logging) {
       const int64_t need_w = 6 + 2LL * nd;
       const int64_t used = U.out->log_used;
@@ -536,13 +552,15 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
         fit = (U.u->log_cap - used) / need_w;
         fit = fit < 0 ? 0 : (fit > K ? K : fit);
       }
+      const int64_t a_it = __shfl_sync(SSG_FULL, alloc_after, (lane << lgP) & 31);
+      const double lat_it = __shfl_sync(SSG_FULL, lat, (lane << lgP) & 31);
       if (lane < fit) {
         int64_t* L = U.log + used + lane * need_w;
         L[0] = 0;
-        L[2] = alloc_after;
+        L[2] = a_it;
         L[3] = 0;
         L[4] = nd;
-        L[5] = __double_as_longlong(lat);
+        L[5] = __double_as_longlong(lat_it);
       }
       // batch start clock of iteration i = completion of iteration i-1
       const double t_prev = __shfl_up_sync(SSG_FULL, t_done, 1);
@@ -554,7 +572,7 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
         if (lane < fit) {
           int64_t* L = U.log + used + lane * need_w;
           L[6 + 2 * r] = id_r;
-          L[7 + 2 * r] = (int64_t)kv_r + k + 1;
+          L[7 + 2 * r] = (int64_t)kv_r + kit + 1;
         }
       }
       __syncwarp();
@@ -564,18 +582,18 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
 #pragma unroll 1
       for (int r = 0; r < nd; ++r) {
         const int64_t e = __shfl_sync(SSG_FULL, ebase, r);
-        if (lane < K) U.emissions[e + k] = t_done;
+        if (lane < K) U.emissions[e + kit] = t_done;
       }
     }
     const double util = (double)alloc_after / (double)c.total_units;
-    double pk = lane < K ? util : 0.0;
+    double pk = q_it < K ? util : 0.0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const double t = __shfl_xor_sync(SSG_FULL, pk, o);
       pk = pk < t ? t : pk;
     }
     S.peak_kv = S.peak_kv < pk ? pk : S.peak_kv;
-    S.allocated = __shfl_sync(SSG_FULL, alloc_after, last);
+    S.allocated = __shfl_sync(SSG_FULL, alloc_after, last << lgP);
     S.busy_time = busy;
     *flops_acc = fla;
     U.clock = clk;
@@ -591,7 +609,7 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
     for (int32_t q = na0; q < na; ++q) enqueue(U, S, 0, arrival_slot<LONE>(U, q));
     *next_arrival = na;
     *next_arrival_time = ta;
-    if (ends || K < 32) break;
+    if (ends || K < KIr) break;
   }
   if (done > 0 && mine) {
     ReqHot& h = U.hot[j];
