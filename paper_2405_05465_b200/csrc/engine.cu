@@ -105,6 +105,9 @@ __device__ bool batch_start(Unit& U, RepState& S, int r) {
     return true;
   }
   const int32_t tokens = U.plan_tokens + S.nd;
+#ifdef SSG_PHASE_CYCLES
+  U.ph[15] += S.np > 0;
+#endif
   if (c.policy == SSG_POL_SARATHI && tokens > c.chunk) {
     set_error(U, SSG_ERR_INTERNAL, 5, tokens, 0, 0.0);  // sarathi: token budget exceeded
     return false;
@@ -278,6 +281,11 @@ __global__ void k_build_tables(const SimConfig* __restrict__ cfgs, int32_t n, in
 // 1/2 cfg #4 shard 0.696 vs 0.74 s, full sweep 1.128 vs 1.155 s)
 #define SSG_FF_MAX_PP 4
 #endif
+#ifndef SSG_FF_RUNNERS
+// runners of a fast-forwarded batch: one per lane, and with 64 a second slot
+// per lane (runner lane + 32)
+#define SSG_FF_RUNNERS 64
+#endif
 #ifndef SSG_FF_ARRIVE_ONE
 #define SSG_FF_ARRIVE_ONE 1  // a batch that is not full still runs the iteration an arrival lands in
 #endif
@@ -324,7 +332,8 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
   }
   const int lane = U.lane;
   const bool mine = lane < nd;
-  // runner state, one per lane (running order == decode entry order)
+  // runner state (running order == decode entry order): runner lane, and
+  // runner lane + 32 in the second slot
   int32_t j = 0, kv = 0, held = 0, rem = 0x7fffffff;
   if (mine) {
     j = RUN(U, 0)[lane];
@@ -332,6 +341,16 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
     kv = h.kv;
     held = h.held;
     rem = (h.done < h.target) ? 0 : h.decode - h.emitted;
+  }
+  const bool mine2 = SSG_FF_RUNNERS > 32 && lane + 32 < nd;
+  int32_t j2 = 0, kv2 = 0, held2 = 0;
+  if (mine2) {
+    j2 = RUN(U, 0)[lane + 32];
+    const ReqHot h = U.hot[j2];
+    kv2 = h.kv;
+    held2 = h.held;
+    const int32_t rem2 = (h.done < h.target) ? 0 : h.decode - h.emitted;
+    rem = rem2 < rem ? rem2 : rem;
   }
   // iterations before any runner would finish (the finishing one is left to the normal path)
   int min_rem = rem;
@@ -345,8 +364,8 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
   const SimOp& od = c.ops[c.idx_dec];
   const SsgModelDesc& md = U.E.models[od.slot];
   if (md.kind != SSG_KIND_INTERP || !c.tab_cells) return 0;
-  // contexts and block counts below 2^26: every 32-lane sum below fits 31 bits
-  if (!__all_sync(SSG_FULL, (kv >> 26) == 0) || c.total_units >= (1LL << 26)) return 0;
+  // contexts and block counts below 2^25: every 64-runner sum below fits 31 bits
+  if (!__all_sync(SSG_FULL, ((kv | kv2) >> 25) == 0) || c.total_units >= (1LL << 25)) return 0;
   // lane layout of a round: P lanes per iteration (lane = it * P + m), one
   // lane per microbatch, so each lane makes one attention query per round
   const int P = pp == 1 ? 1 : (pp == 2 ? 2 : 4);
@@ -356,10 +375,11 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
   const bool q_on = q_m < nm;
   // microbatch q_m's invariants: size, context sum, token-table terms, axis-0 cell
   int64_t ctx_q = 0;
-  const int run_m = lane % pp;  // runner lane -> its microbatch
+  const int run_m = lane % pp, run_m2 = (lane + 32) % pp;  // runner -> its microbatch
 #pragma unroll 1
   for (int m = 0; m < nm; ++m) {
-    const unsigned cm = __reduce_add_sync(SSG_FULL, mine && run_m == m ? (unsigned)kv + 1u : 0u);
+    const unsigned cm = __reduce_add_sync(SSG_FULL, (mine && run_m == m ? (unsigned)kv + 1u : 0u) +
+                                                        (mine2 && run_m2 == m ? (unsigned)kv2 + 1u : 0u));
     if (q_m == m) ctx_q = cm;
   }
   const int nd_q = q_on ? (nd - q_m + pp - 1) / pp : 0;
@@ -384,7 +404,9 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
   const bool logging = !LONE && (U.u->flags & SSG_UF_BATCH_LOG) != 0;
   const double fa4 = od.fa;
   // emission slot of this runner's next token
-  const int64_t ebase = (mine && emit_times) ? U.emit_base[j] + (U.hot[j].decode - rem) : 0;
+  // (every runner's prefill is complete here: rem = decode - emitted)
+  const int64_t ebase = (mine && emit_times) ? U.emit_base[j] + U.hot[j].emitted : 0;
+  const int64_t ebase2 = (mine2 && emit_times) ? U.emit_base[j2] + U.hot[j2].emitted : 0;
   const int64_t free0 = c.total_units;
   const double tp_pp = (double)(c.tp * c.pp);
   int done = 0;
@@ -406,14 +428,18 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
     for (int i = 0; i < KIr; ++i) {
       const int ki = done + i;
       uint32_t sr = 0;
-      if (mine) {
-        int64_t hk = held;
-        if (ki > 0) {
-          const int64_t u = units_for(c, (int64_t)kv + ki);
-          hk = hk < u ? u : hk;
+#pragma unroll
+      for (int sl = 0; sl < (SSG_FF_RUNNERS > 32 ? 2 : 1); ++sl) {
+        if (sl == 0 ? mine : mine2) {
+          const int32_t kvs = sl == 0 ? kv : kv2, hs = sl == 0 ? held : held2;
+          int64_t hk = hs;
+          if (ki > 0) {
+            const int64_t u = units_for(c, (int64_t)kvs + ki);
+            hk = hk < u ? u : hk;
+          }
+          const int64_t s = units_for(c, (int64_t)kvs + ki + 1) - hk;
+          sr += s > 0 ? (uint32_t)s : 0u;
         }
-        const int64_t s = units_for(c, (int64_t)kv + ki + 1) - hk;
-        sr = s > 0 ? (uint32_t)s : 0u;
       }
       const unsigned tot = __reduce_add_sync(SSG_FULL, sr);
       if (q_it == i) need = tot;
@@ -567,8 +593,8 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
       if (lane < fit) U.log[used + lane * need_w + 1] = __double_as_longlong(lane == 0 ? U.clock : t_prev);
 #pragma unroll 1
       for (int r = 0; r < nd; ++r) {
-        const int64_t id_r = U.ids[__shfl_sync(SSG_FULL, j, r)];
-        const int32_t kv_r = __shfl_sync(SSG_FULL, kv, r);
+        const int64_t id_r = U.ids[__shfl_sync(SSG_FULL, r < 32 ? j : j2, r & 31)];
+        const int32_t kv_r = __shfl_sync(SSG_FULL, r < 32 ? kv : kv2, r & 31);
         if (lane < fit) {
           int64_t* L = U.log + used + lane * need_w;
           L[6 + 2 * r] = id_r;
@@ -581,7 +607,7 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
     if (emit_times) {
 #pragma unroll 1
       for (int r = 0; r < nd; ++r) {
-        const int64_t e = __shfl_sync(SSG_FULL, ebase, r);
+        const int64_t e = __shfl_sync(SSG_FULL, r < 32 ? ebase : ebase2, r & 31);
         if (lane < K) U.emissions[e + kit] = t_done;
       }
     }
@@ -618,6 +644,13 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
     h.held = held < u ? (int32_t)u : held;
     h.emitted = h.emitted + done;
   }
+  if (done > 0 && mine2) {
+    ReqHot& h = U.hot[j2];
+    const int64_t u = units_for(c, (int64_t)kv2 + done);
+    h.kv = kv2 + done;
+    h.held = held2 < u ? (int32_t)u : held2;
+    h.emitted = h.emitted + done;
+  }
   __syncwarp();
   return done;
 }
@@ -632,7 +665,7 @@ __device__ SSG_FFWD int fast_forward(Unit& U, RepState& S, int32_t* next_arrival
   // requests may wait only while the batch is full: every policy's admission
   // loop requires running < max_batch_size before it looks at the queue
   // (scheduler.hpp:360-361, 387-388, 425-427)
-  if ((S.wait_n != 0 && S.run_n < c.max_batch) || S.run_n < 1 || S.run_n > 32 || c.tab_off < 0 ||
+  if ((S.wait_n != 0 && S.run_n < c.max_batch) || S.run_n < 1 || S.run_n > SSG_FF_RUNNERS || c.tab_off < 0 ||
       c.idx_dec < 0)
     return 0;
   const int nd = S.run_n, pp = c.pp;
@@ -824,8 +857,14 @@ __device__ void run_unit(Unit& U) {
       else if (!(S.wait_n == 0 || S.run_n >= c.max_batch)) FFSTAT(15);
     }
 #endif
+#ifdef SSG_PHASE_CYCLES
+    if (FAST && S.ev_kind == 1 && reg1) {
+      if (S.run_n > SSG_FF_RUNNERS) U.ph[12] += 1;
+      else if (!(S.wait_n == 0 || S.run_n >= c.max_batch)) U.ph[13] += 1;
+    }
+#endif
     if (FAST && S.ev_kind == 1 && reg1 && (S.wait_n == 0 || S.run_n >= c.max_batch) &&
-        S.run_n >= 1 && S.run_n <= 32) {
+        S.run_n >= 1 && S.run_n <= SSG_FF_RUNNERS) {
       // pure-decode stretch: iterations that end at the same state the event
       // loop would reach; afterwards the replica is again "BatchStart at clock"
       double fl = U.out->flops;
@@ -836,6 +875,7 @@ __device__ void run_unit(Unit& U) {
 #ifdef SSG_PHASE_CYCLES
       U.ph[5] += k;
       U.ph[7] += 1;
+      U.ph[14] += k == 0;
 #endif
 #ifdef SSG_FF_STATS
       if (U.lane == 0) {
@@ -944,7 +984,7 @@ __device__ void run_unit(Unit& U) {
 #endif
 #ifdef SSG_PHASE_CYCLES
 #define SSG_PHASE_MAX_UNITS 16384
-__device__ long long g_phase[SSG_PHASE_MAX_UNITS][8];
+__device__ long long g_phase[SSG_PHASE_MAX_UNITS][SSG_PH_N];
 #endif
 
 template <int FMA, int FOREST, int FAST, int LONE>
@@ -989,12 +1029,12 @@ __global__ void SSG_SIM_BOUNDS(FAST) k_simulate(SimLaunch L) {
   U.WC = U.u->wait_cap;
   U.rep_stride = 6LL * U.MB + U.WC;
 #ifdef SSG_PHASE_CYCLES
-  for (int k = 0; k < 8; ++k) U.ph[k] = 0;
+  for (int k = 0; k < SSG_PH_N; ++k) U.ph[k] = 0;
 #endif
   run_unit<FMA, FOREST, FAST, LONE>(U);
 #ifdef SSG_PHASE_CYCLES
   if (U.lane == 0 && uid < SSG_PHASE_MAX_UNITS)
-    for (int k = 0; k < 8; ++k) g_phase[uid][k] = U.ph[k];
+    for (int k = 0; k < SSG_PH_N; ++k) g_phase[uid][k] = U.ph[k];
 #endif
 }
 
@@ -1073,7 +1113,7 @@ void launch_build_tables(const SimConfig* d_cfgs, int32_t n, int32_t stride,
 bool phase_cycles(long long* dst, int64_t n) {
 #ifdef SSG_PHASE_CYCLES
   n = n < SSG_PHASE_MAX_UNITS ? n : SSG_PHASE_MAX_UNITS;
-  cuda_check(cudaMemcpyFromSymbol(dst, ssgk::g_phase, n * 8 * sizeof(long long)), "phase cycles");
+  cuda_check(cudaMemcpyFromSymbol(dst, ssgk::g_phase, n * SSG_PH_N * sizeof(long long)), "phase cycles");
   return true;
 #else
   (void)dst;

@@ -87,14 +87,18 @@ struct Unit {
   int32_t plan_tokens; // prefill chunk tokens pushed
   int32_t plan_late;   // requests first scheduled now, later than the abort threshold
 #ifdef SSG_PHASE_CYCLES
-  long long ph[8];     // diagnostic build: cycles per event-loop phase (SSG_PH_*)
+  long long ph[SSG_PH_N];  // diagnostic build: cycles per event-loop phase (SSG_PH_*)
 #endif
 };
 
 // Diagnostic builds (-DSSG_PHASE_CYCLES) charge clock64 deltas to phases:
 // 0 schedule, 1 batch latency, 2 batch complete, 3 fast-forward calls,
 // 4 arrivals, 5 fast-forwarded iterations (a count), 6 whole unit,
-// 7 fast-forward calls (a count).
+// 7 fast-forward calls (a count); inside the batch latency (table path):
+// 8 per-microbatch sums, 9 query setup and attention queries, 11 operator-order
+// sums, 10 makespan; counts: 12 BatchStarts with more than 32 runners, 13 with
+// requests waiting and room in the batch, 14 fast-forward calls that ran no
+// iteration, 15 batches with a prefill chunk.
 #ifdef SSG_PHASE_CYCLES
 #define SSG_PH_BEGIN(v) const long long v = clock64()
 #define SSG_PH_END(v, k) (U.ph[k] += clock64() - (v))
@@ -969,6 +973,7 @@ __device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, doubl
   int64_t* st = U.smem_stats;  // [pp][6]: prefills, tokens, sum p^2, sum prior, decodes, sum ctx
   const int32_t total = S.np + S.nd;
   // per-microbatch sums: prefills, tokens, sum p^2, sum prior, decodes, sum ctx
+  SSG_PH_BEGIN(ph_a);
   auto accumulate = [&](int32_t k, int64_t& a0, int64_t& a1, int64_t& a2, int64_t& a3, int64_t& a4,
                         int64_t& a5) {
     if (k < S.np) {
@@ -1041,6 +1046,8 @@ __device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, doubl
     }
   }
   __syncwarp();
+  SSG_PH_END(ph_a, 8);
+  SSG_PH_BEGIN(ph_q);
   const int nops = c.nops;
   double* secs_part = U.smem_part;       // [pp]
   double* flop_part = U.smem_part + SSG_MAX_PP;
@@ -1106,6 +1113,8 @@ __device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, doubl
       }
       pred = __dmul_rn(o.count, pred);
     }
+    SSG_PH_END(ph_q, 9);
+    SSG_PH_BEGIN(ph_e);
     const unsigned em = __ballot_sync(SSG_FULL, code != SSG_OK);
     if (em) {
       const int src = __ffs(em) - 1;  // lanes are in (microbatch, prefill < decode) order
@@ -1149,9 +1158,11 @@ __device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, doubl
       flop_part[U.lane] = acc_f;
     }
     __syncwarp();
+    SSG_PH_END(ph_e, 11);
   } else {
     batch_latency_full<FMA, FOREST>(U, st, err, err_task, err_feat, err_val, qb);
   }
+  SSG_PH_BEGIN(ph_m);
   if (err != SSG_OK) {  // first failing (microbatch, op) in order -- either path
     const SimOp& o = c.ops[err_task % nops];
     set_error(U, err, o.slot, err_feat, 0, err_val);
@@ -1245,6 +1256,7 @@ __device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, doubl
   }
   *latency = lat;
   *flops_out = flops;
+  SSG_PH_END(ph_m, 10);
   return SSG_OK;
 }
 

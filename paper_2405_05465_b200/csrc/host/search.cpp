@@ -573,13 +573,13 @@ void run_launch(SweepLane& lane, ProbeLaunch& L, const ResidentWorkload& w,
       std::vector<double> qps_of(L.units.size(), 0.0);
       for (const auto& p : L.probes)
         for (int u = p.first_unit; u < p.first_unit + (p.decoupled ? p.R : 1); ++u) qps_of[u] = p.qps;
-      std::vector<long long> ph(out.size() * 8, 0);
+      std::vector<long long> ph(out.size() * SSG_PH_N, 0);
       const bool have_ph = phase_cycles(ph.data(), static_cast<int64_t>(out.size()));
       for (std::size_t u = 0; u < out.size(); ++u) {
         const SimConfig& cf = L.configs[L.units[u].config];
         if (have_ph && u < 16384) {
           std::fprintf(f, "P %d %zu", launch_no, u);
-          for (int k = 0; k < 8; ++k) std::fprintf(f, " %lld", ph[u * 8 + k]);
+          for (int k = 0; k < SSG_PH_N; ++k) std::fprintf(f, " %lld", ph[u * SSG_PH_N + k]);
           std::fprintf(f, "\n");
         }
         std::fprintf(f, "%d %zu %d %d %d %lld %lld %.17g %d %d %lld %d %d %d %lld %d\n", launch_no, u,

@@ -31,6 +31,7 @@
 #define SSG_UF_BATCH_LOG 2  // record every scheduled batch (SimObserver payload)
 #define SSG_UF_ABORT 4      // capacity probe: stop once late schedules exceed the bound
 #define SSG_UF_OBSERVER 8   // batch log carries the SimObserver's scheduler view (needs BATCH_LOG)
+#define SSG_PH_N 16         // phase counters per unit of -DSSG_PHASE_CYCLES builds (engine.cuh)
 
 #define SSG_TAB_ROWS 11     // token-table rows per table (see SimConfig)
 

@@ -42,7 +42,7 @@ int fast_forward_enabled();
 int sweep_fast_forward_enabled();
 void launch_simulate(const SimLaunch& L, cudaStream_t s);
 // Diagnostic builds (-DSSG_PHASE_CYCLES): per-unit phase cycles of the last
-// k_simulate launch, 8 per unit (engine.cuh SSG_PH_*); false otherwise.
+// k_simulate launch, SSG_PH_N per unit (engine.cuh SSG_PH_*); false otherwise.
 bool phase_cycles(long long* dst, int64_t n);
 // True when every unit simulates one replica that does not route through the
 // deferred pool and the launch has no batch log and no arrival permutation --
