@@ -1020,6 +1020,7 @@ __global__ void SSG_SIM_BOUNDS(FAST) k_simulate(SimLaunch L) {
   U.out = L.out + uid;
   U.smem_stats = stats[wib];
   U.smem_part = part[wib];
+  U.pcap = SSG_MAX_PP;
   U.tables = L.tables;
   U.fast = L.fast_forward;
   U.group_fail = (L.group_fail && U.u->group >= 0) ? L.group_fail + U.u->group : nullptr;
@@ -1028,6 +1029,14 @@ __global__ void SSG_SIM_BOUNDS(FAST) k_simulate(SimLaunch L) {
   U.MB = U.cfg->max_batch;
   U.WC = U.u->wait_cap;
   U.rep_stride = 6LL * U.MB + U.WC;
+  if (U.cfg->pp > SSG_MAX_PP) {
+    // deep pipelines: microbatch scratch after the unit's queues and pool
+    // (SSG_PP_SCRATCH_WORDS; the host sizes and 8-byte aligns it)
+    int32_t* x = U.ws + (int64_t)U.u->R * U.rep_stride + U.WC + 2;
+    U.smem_stats = reinterpret_cast<int64_t*>(x);
+    U.smem_part = reinterpret_cast<double*>(x + 12LL * U.cfg->pp);
+    U.pcap = U.cfg->pp;
+  }
 #ifdef SSG_PHASE_CYCLES
   for (int k = 0; k < SSG_PH_N; ++k) U.ph[k] = 0;
 #endif
@@ -1065,6 +1074,7 @@ __global__ void __launch_bounds__(SSG_SIM_WARPS * 32)
   U.out = out + c;
   U.smem_stats = stats[wib];
   U.smem_part = part[wib];
+  U.pcap = SSG_MAX_PP;
   U.tables = nullptr;
   U.lane = threadIdx.x & 31;
   U.ax1_hint = 0;

@@ -68,9 +68,10 @@ struct Unit {
   int32_t* ws;
   int64_t* log;
   SimUnitOut* out;
-  int64_t* smem_stats;  // per-warp shared scratch [SSG_MAX_PP * 6]
+  int64_t* smem_stats;  // per-warp scratch [pcap * 6] (shared memory, HBM for deep pipelines)
   const double* tables; // token tables pool (SimConfig::tab_off)
-  double* smem_part;    // per-warp shared scratch [4 * SSG_MAX_PP]
+  double* smem_part;    // per-warp scratch [4 * pcap]
+  int32_t pcap;         // microbatches the scratch holds (SSG_MAX_PP, or pp above it)
   uint32_t* group_fail;  // this unit's speculation-group failure mask (may be null)
   int fast;         // pure-decode fast-forward enabled
   int lane;
@@ -810,7 +811,7 @@ static __device__ SSG_COLD void batch_latency_full(Unit& U, const int64_t* st, i
   const int pp = c.pp;
   const int nops = c.nops;
   double* secs_part = U.smem_part;
-  double* flop_part = U.smem_part + SSG_MAX_PP;
+  double* flop_part = U.smem_part + U.pcap;
   const int work = pp * nops;
   double acc_s = 0.0, acc_f = 0.0;
   int cur_m = 0;
@@ -1050,13 +1051,13 @@ __device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, doubl
   SSG_PH_BEGIN(ph_q);
   const int nops = c.nops;
   double* secs_part = U.smem_part;       // [pp]
-  double* flop_part = U.smem_part + SSG_MAX_PP;
+  double* flop_part = U.smem_part + U.pcap;
   int err = SSG_OK, err_task = 0, err_feat = 0;
   double err_val = 0.0;
   int64_t qb = 0;
   // token-table fast path: every non-empty microbatch within the tables' range
   const bool use_tab =
-      c.tab_off >= 0 && !__any_sync(SSG_FULL, U.lane < pp && st[U.lane * 6 + 1] > c.tab_tmax);
+      c.tab_off >= 0 && pp <= SSG_MAX_PP && !__any_sync(SSG_FULL, U.lane < pp && st[U.lane * 6 + 1] > c.tab_tmax);
   if (use_tab) {
     const int T1 = c.tab_stride;
     const double* tab = U.tables + c.tab_off;
@@ -1216,8 +1217,8 @@ __device__ int batch_latency(Unit& U, RepState& S, int r, double* latency, doubl
     __syncwarp();
   } else {
     // compact the non-empty microbatches' times into part[2*MAX..]; makespan
-    double* times = U.smem_part + 2 * SSG_MAX_PP;
-    double* finish = U.smem_part + 3 * SSG_MAX_PP;
+    double* times = U.smem_part + 2 * U.pcap;
+    double* finish = U.smem_part + 3 * U.pcap;
     int nt = 0;
     for (int m = 0; m < pp; ++m) {
       if (st[m * 6 + 1] == 0) continue;

@@ -346,7 +346,8 @@ struct ProbeLaunch {
       while (wc <= u.n) wc <<= 1;
       u.wait_cap = static_cast<int32_t>(wc);
       u.ws_off = ws_words;
-      ws_words += static_cast<int64_t>(u.R) * (6LL * cfg.max_batch + wc) + wc + 2;
+      ws_words += static_cast<int64_t>(u.R) * (6LL * cfg.max_batch + wc) + wc + 2 +
+                  SSG_PP_SCRATCH_WORDS(cfg.pp);
       u.rep_off = nreps;
       nreps += u.R;
       u.abort_thr = thr;

@@ -112,8 +112,6 @@ SimConfig make_sim_config(const ClusterConfig& cl, const EstimatorModel& est, in
   c.policy = static_cast<int32_t>(cl.policy.policy);
   require(cl.policy.max_batch_size <= kMaxBatchEntries,
           "ssg: max_batch_size above the device engine limit (" + std::to_string(kMaxBatchEntries) + ")");
-  require(cl.par.pp_degree <= SSG_MAX_PP,
-          "ssg: pp_degree above the device engine limit (" + std::to_string(SSG_MAX_PP) + ")");
   c.max_batch = static_cast<int32_t>(cl.policy.max_batch_size);
   c.max_tokens = static_cast<int32_t>(std::min<std::int64_t>(cl.policy.max_tokens_per_iter, INT32_MAX));
   c.chunk = static_cast<int32_t>(std::min<std::int64_t>(cl.policy.chunk_size, INT32_MAX));
@@ -235,7 +233,8 @@ int32_t SimJobs::add_unit(const UnitSpec& spec, const std::vector<Request>& reqs
   u.req_off = static_cast<int64_t>(hot.size());
   u.wait_cap = pow2_above(u.n);
   u.ws_off = ws_words;
-  ws_words += static_cast<int64_t>(u.R) * (6LL * cfg.max_batch + u.wait_cap) + u.wait_cap + 2;
+  ws_words += static_cast<int64_t>(u.R) * (6LL * cfg.max_batch + u.wait_cap) + u.wait_cap + 2 +
+              SSG_PP_SCRATCH_WORDS(cfg.pp);
   u.rep_off = nreps;
   nreps += u.R;
   u.abort_thr = spec.abort_thr;

@@ -35,6 +35,7 @@ __global__ void __launch_bounds__(32) k_sched_op(SchedArgs A) {
   U.smem_stats = nullptr;
   U.tables = nullptr;
   U.smem_part = nullptr;
+  U.pcap = SSG_MAX_PP;
   U.group_fail = nullptr;
   U.fast = 0;
   U.lane = threadIdx.x & 31;

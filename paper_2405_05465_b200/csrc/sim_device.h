@@ -24,7 +24,12 @@
 #define SSG_CLS_COMM 2
 
 #define SSG_MAX_OPS 11
-#define SSG_MAX_PP 16  // microbatch m uses lanes 2m, 2m + 1 of the batch-latency step
+#define SSG_MAX_PP 16  // microbatch m uses lanes 2m, 2m + 1 of the batch-latency step; deeper
+                       // pipelines take the general latency path with per-unit scratch in HBM
+// int32 words of per-unit microbatch scratch (6 int64 sums + 4 doubles per
+// microbatch) appended to a unit's workspace when pp exceeds the shared-memory
+// scratch
+#define SSG_PP_SCRATCH_WORDS(pp) ((pp) > SSG_MAX_PP ? 20LL * (pp) : 0LL)
 
 // Unit flags
 #define SSG_UF_EMISSIONS 1  // write per-token emission times (CSR)

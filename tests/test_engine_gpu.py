@@ -165,9 +165,11 @@ def test_routing(ssg, ref, routing, replicas, n, qps):
 
 
 @pytest.mark.parametrize("tp,pp,policy", [(4, 1, "sarathi_serve"), (2, 2, "vllm"), (1, 4, "orca_plus"),
-                                         (1, 5, "sarathi_serve"), (1, 16, "vllm")])
+                                         (1, 5, "sarathi_serve"), (1, 16, "vllm"),
+                                         (1, 20, "sarathi_serve"), (2, 40, "vllm"), (1, 80, "orca_plus")])
 def test_70b_parallelism(ssg, ref, tp, pp, policy):
-    """cfg #2 shape (70B, Sarathi cs512) plus pipeline microbatching."""
+    """cfg #2 shape (70B, Sarathi cs512) plus pipeline microbatching; pp above 16
+    takes the general latency path with its microbatch scratch in HBM."""
     m, t = estimators(ssg, ref, "llama2_70b", "h100_80g", [1, 2, 4])
     cluster = catalog.cluster_doc("llama2_70b", "h100_80g", tp=tp, pp=pp, policy=policy,
                                   max_batch_size=128, chunk_size=512, cpu_overhead=1e-4)
