@@ -1026,7 +1026,7 @@ __global__ void SSG_SIM_BOUNDS(FAST) k_simulate(SimLaunch L) {
   U.group_fail = (L.group_fail && U.u->group >= 0) ? L.group_fail + U.u->group : nullptr;
   U.lane = threadIdx.x & 31;
   U.ax1_hint = 0;
-  U.MB = U.cfg->max_batch;
+  U.MB = U.u->mb_ws;
   U.WC = U.u->wait_cap;
   U.rep_stride = 6LL * U.MB + U.WC;
   if (U.cfg->pp > SSG_MAX_PP) {

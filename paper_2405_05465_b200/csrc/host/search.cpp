@@ -345,8 +345,9 @@ struct ProbeLaunch {
       int64_t wc = 2;
       while (wc <= u.n) wc <<= 1;
       u.wait_cap = static_cast<int32_t>(wc);
+      u.mb_ws = static_cast<int32_t>(std::min<int64_t>(cfg.max_batch, std::max<int32_t>(u.n, 1)));
       u.ws_off = ws_words;
-      ws_words += static_cast<int64_t>(u.R) * (6LL * cfg.max_batch + wc) + wc + 2 +
+      ws_words += static_cast<int64_t>(u.R) * (6LL * u.mb_ws + wc) + wc + 2 +
                   SSG_PP_SCRATCH_WORDS(cfg.pp);
       u.rep_off = nreps;
       nreps += u.R;

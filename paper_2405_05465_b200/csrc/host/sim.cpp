@@ -110,9 +110,9 @@ SimConfig make_sim_config(const ClusterConfig& cl, const EstimatorModel& est, in
   const auto& de = est.device();
   SimConfig c{};
   c.policy = static_cast<int32_t>(cl.policy.policy);
-  require(cl.policy.max_batch_size <= kMaxBatchEntries,
-          "ssg: max_batch_size above the device engine limit (" + std::to_string(kMaxBatchEntries) + ")");
-  c.max_batch = static_cast<int32_t>(cl.policy.max_batch_size);
+  // queues are sized by min(max_batch_size, requests) per unit (SimUnit::mb_ws), so
+  // any batch cap is exact; one above INT32_MAX never binds (a unit holds fewer requests)
+  c.max_batch = static_cast<int32_t>(std::min<std::int64_t>(cl.policy.max_batch_size, INT32_MAX));
   c.max_tokens = static_cast<int32_t>(std::min<std::int64_t>(cl.policy.max_tokens_per_iter, INT32_MAX));
   c.chunk = static_cast<int32_t>(std::min<std::int64_t>(cl.policy.chunk_size, INT32_MAX));
   c.token_granular = cl.policy.policy == SchedulerPolicy::LightLLM ? 1 : 0;
@@ -232,8 +232,9 @@ int32_t SimJobs::add_unit(const UnitSpec& spec, const std::vector<Request>& reqs
   u.flags = spec.flags;
   u.req_off = static_cast<int64_t>(hot.size());
   u.wait_cap = pow2_above(u.n);
+  u.mb_ws = static_cast<int32_t>(std::min<int64_t>(cfg.max_batch, std::max<int32_t>(u.n, 1)));
   u.ws_off = ws_words;
-  ws_words += static_cast<int64_t>(u.R) * (6LL * cfg.max_batch + u.wait_cap) + u.wait_cap + 2 +
+  ws_words += static_cast<int64_t>(u.R) * (6LL * u.mb_ws + u.wait_cap) + u.wait_cap + 2 +
               SSG_PP_SCRATCH_WORDS(cfg.pp);
   u.rep_off = nreps;
   nreps += u.R;

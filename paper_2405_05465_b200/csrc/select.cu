@@ -8,7 +8,7 @@
 // smallest key is fixed -- an exact selection, so the returned double is the
 // very element std::sort would have put at that index.  Histograms live in
 // shared memory; the segment is streamed from HBM/L2 once per pass with
-// coalesced loads.
+// coalesced loads; the digit's bin is found by a warp scan.
 #include <cmath>
 #include <vector>
 
@@ -27,16 +27,20 @@ __device__ __forceinline__ double key_value(unsigned long long k) {
 }
 
 constexpr int kSelectThreads = 512;
+constexpr int kSelectWarps = kSelectThreads / 32;
 
 // tasks[t] = {segment, rank (0-based)}; seg_off[s]..seg_off[s+1] spans the samples
 __global__ void __launch_bounds__(kSelectThreads)
     k_select(const double* __restrict__ samples, const int64_t* __restrict__ seg_off,
              const SelectTask* __restrict__ tasks, int64_t ntasks, double* __restrict__ out) {
+  // per-warp histograms (atomics contend within a warp only), summed per pass
+  __shared__ unsigned int whist[kSelectWarps][256];
   __shared__ unsigned int hist[256];
   __shared__ unsigned long long s_prefix;
   __shared__ long long s_rank;
   const int64_t t = blockIdx.x;
   if (t >= ntasks) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const SelectTask task = tasks[t];
   const int64_t lo = seg_off[task.segment], hi = seg_off[task.segment + 1];
   if (threadIdx.x == 0) {
@@ -45,24 +49,51 @@ __global__ void __launch_bounds__(kSelectThreads)
   }
   for (int pass = 0; pass < 8; ++pass) {
     const int shift = 56 - 8 * pass;
-    for (int b = threadIdx.x; b < 256; b += blockDim.x) hist[b] = 0;
+    for (int b = lane; b < 256; b += 32) whist[warp][b] = 0;
     __syncthreads();
     const unsigned long long prefix = s_prefix;
     const unsigned long long pmask = pass == 0 ? 0ull : (~0ull << (shift + 8));
     for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
       const unsigned long long k = order_key(__ldg(samples + i));
-      if ((k & pmask) == prefix) atomicAdd(&hist[(k >> shift) & 0xff], 1u);
+      if ((k & pmask) == prefix) atomicAdd(&whist[warp][(k >> shift) & 0xff], 1u);
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      long long r = s_rank;
-      int b = 0;
-      for (; b < 256; ++b) {
-        if (r < (long long)hist[b]) break;
-        r -= hist[b];
+    if (threadIdx.x < 256) {
+      unsigned int c = 0;
+#pragma unroll
+      for (int w = 0; w < kSelectWarps; ++w) c += whist[w][threadIdx.x];
+      hist[threadIdx.x] = c;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      // the digit: first bin whose inclusive count exceeds the rank -- lane l
+      // owns bins 8l..8l+7, a warp scan gives each lane the count before them
+      unsigned int own[8], sum = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        own[q] = hist[8 * lane + q];
+        sum += own[q];
       }
-      s_rank = r;
-      s_prefix = prefix | ((unsigned long long)b << shift);
+      unsigned long long incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const long long r = s_rank;
+      const unsigned long long before = incl - sum;
+      const unsigned hit = __ballot_sync(0xffffffffu, (long long)incl > r);
+      const int L = __ffs(hit) - 1;  // the rank lies in the segment, so some lane hits
+      if (lane == L) {
+        long long rr = r - (long long)before;
+        int b = 0;
+        for (; b < 7; ++b) {
+          if (rr < (long long)own[b]) break;
+          rr -= own[b];
+        }
+        s_rank = rr;
+        s_prefix = prefix | ((unsigned long long)(8 * L + b) << shift);
+      }
     }
     __syncthreads();
   }

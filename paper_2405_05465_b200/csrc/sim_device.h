@@ -134,7 +134,8 @@ struct SimUnit {
   int32_t group;      // speculation group (a candidate's probes of one launch), -1: none
   int32_t rung;       // this probe's bit in its group's failure mask
   uint32_t kill;      // group failure bits that make this probe unnecessary
-  int32_t pad;
+  int32_t mb_ws;      // workspace entries per queue / plan array: min(max_batch, n)
+                      // (no replica ever runs or plans more than the unit's requests)
 };
 
 struct RepState {

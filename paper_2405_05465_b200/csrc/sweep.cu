@@ -1,6 +1,6 @@
 // sweep.cu -- device-side setup and measurement for the capacity sweep.
 //
-// k_probe_setup   one thread per probe rebuilds the probe's Poisson arrivals
+// k_probe_setup   one warp per probe rebuilds the probe's Poisson arrivals
 //                 t_i = t_{i-1} + max(E_i / qps, 1e-12) from the resident unit
 //                 exponentials (workload.hpp:96-103) and scatters the request
 //                 stream into the probe's simulation units (RR replica r owns
@@ -16,22 +16,37 @@
 
 namespace ssgk {
 
+// One warp per probe: lanes take 32 trace positions at a time (gaps, request
+// records, emission bases in parallel); the arrival times are the exact
+// left-to-right fp64 running sum, a chain of one add per request that reads
+// the gaps through shuffles issued ahead of it.
 __global__ void k_probe_setup(const ProbeDesc* __restrict__ probes, int32_t nprobes,
                               const SimUnit* __restrict__ units, const int32_t* __restrict__ pre,
                               const int32_t* __restrict__ dec, const double* __restrict__ unit_exp,
                               const int64_t* __restrict__ dec_prefix, int32_t n, ReqHot* hot,
                               ReqTimes* tm, int64_t* ids, int64_t* emit_base) {
-  const int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= nprobes) return;
+  const int32_t p = (int32_t)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (p >= nprobes) return;  // warp-uniform
   const ProbeDesc P = probes[p];
   double t = 0.0;
-  for (int32_t i = 0; i < n; ++i) {
-    if (P.static_run) {
-      t = 0.0;
-    } else {
-      const double gap = __ddiv_rn(unit_exp[i], P.qps);
-      t = __dadd_rn(t, gap < 1e-12 ? 1e-12 : gap);  // std::max(gap, 1e-12)
+  for (int32_t base = 0; base < n; base += 32) {
+    const int32_t i = base + lane;
+    const bool on = i < n;
+    double gap = 0.0;
+    if (on && !P.static_run) {
+      gap = __ddiv_rn(unit_exp[i], P.qps);
+      gap = gap < 1e-12 ? 1e-12 : gap;  // std::max(gap, 1e-12)
     }
+    double arrival = 0.0;
+    const int32_t kmax = n - base < 32 ? n - base : 32;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const double gk = __shfl_sync(0xffffffffu, gap, k);
+      if (k < kmax) t = P.static_run ? 0.0 : __dadd_rn(t, gk);
+      if (k == lane) arrival = t;
+    }
+    if (!on) continue;
     const int32_t u = P.first_unit + (P.decoupled ? i % P.R : 0);
     const int32_t local = P.decoupled ? i / P.R : i;
     const int64_t g = units[u].req_off + local;
@@ -46,7 +61,7 @@ __global__ void k_probe_setup(const ProbeDesc* __restrict__ probes, int32_t npro
     h.prefill = pre[i];
     hot[g] = h;
     ReqTimes r;
-    r.arrival = t;
+    r.arrival = arrival;
     r.first_sched = -1.0;
     r.first_tok = -1.0;
     r.completion = -1.0;
@@ -90,8 +105,9 @@ void launch_probe_setup(const ProbeDesc* d_probes, int32_t nprobes, const SimUni
                         const ResidentWorkload& w, ReqHot* hot, ReqTimes* tm, int64_t* ids,
                         int64_t* emit_base, cudaStream_t s) {
   if (nprobes <= 0) return;
-  const int threads = 64;
-  ssgk::k_probe_setup<<<(nprobes + threads - 1) / threads, threads, 0, s>>>(
+  const int threads = 128;  // 4 probes (warps) per block
+  const int64_t blocks = ((int64_t)nprobes * 32 + threads - 1) / threads;
+  ssgk::k_probe_setup<<<(unsigned)blocks, threads, 0, s>>>(
       d_probes, nprobes, d_units, w.pre.ptr, w.dec.ptr, w.unit_exp.ptr, w.dec_prefix.ptr, w.n, hot,
       tm, ids, emit_base);
   cuda_check(cudaGetLastError(), "k_probe_setup launch");

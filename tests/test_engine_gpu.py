@@ -177,6 +177,16 @@ def test_70b_parallelism(ssg, ref, tp, pp, policy):
     assert_same(mine, theirs)
 
 
+@pytest.mark.parametrize("max_batch", [3_000_000, 1 << 40])
+def test_unbounded_max_batch(ssg, ref, max_batch):
+    """A batch cap above any unit's request count (the reference accepts any
+    int64 >= 1): queues are sized by min(max_batch_size, requests)."""
+    m, t = estimators(ssg, ref, "llama2_7b", "a100_80g", [1])
+    cluster = catalog.cluster_doc("llama2_7b", "a100_80g", policy="vllm", max_batch_size=max_batch)
+    mine, theirs = run_both(ssg, m, t, cluster, trace_fixture(300, 20.0, 9))
+    assert_same(mine, theirs)
+
+
 def test_forest_regressor_sim(ssg, ref):
     m, t = estimators(ssg, ref, "llama2_7b", "a100_80g", [1], reg="forest")
     cluster = catalog.cluster_doc("llama2_7b", "a100_80g", policy="sarathi_serve", chunk_size=1024)
