@@ -409,6 +409,10 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
   const int64_t ebase2 = (mine2 && emit_times) ? U.emit_base[j2] + U.hot[j2].emitted : 0;
   const int64_t free0 = c.total_units;
   const double tp_pp = (double)(c.tp * c.pp);
+  // block needs in closed form when units(x) = ceil(x / B) through the block
+  // magic and every kv + k (< 2^31) and held * B stay below 2^32
+  const int64_t B = c.block_size;
+  const bool closed_needs = c.bs_magic != 0 && c.total_units * B < (1LL << 31);
   int done = 0;
   while (done < max_iters) {
     // iterations this round: at most KI, and (when an arrival ends the stretch)
@@ -421,9 +425,37 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
     }
     const int k = done + q_it;  // this lane's iteration
     const bool active = q_it < KIr;
-    // ---- schedule: every runner reserves kv+k+1 tokens (no preemption allowed);
-    // lanes over runners, one warp sum per iteration
+    // ---- schedule: every runner reserves kv+k+1 tokens (no preemption allowed)
     int64_t need = 0;
+    if (closed_needs) {
+      // runner (kv, held) needs units(kv+1) - held blocks at k = 0 (if positive)
+      // and, at k >= 1, one block exactly when kv + k is a multiple of B and
+      // kv + k >= held * B (units(kv+k+1) exceeds both held and units(kv+k));
+      // each runner adds its needs of the round to per-iteration counters
+      int32_t* cnt = reinterpret_cast<int32_t*>(U.smem_stats);
+      cnt[lane] = 0;
+      __syncwarp();
+#pragma unroll
+      for (int sl = 0; sl < (SSG_FF_RUNNERS > 32 ? 2 : 1); ++sl) {
+        if (sl == 0 ? mine : mine2) {
+          const int64_t kvs = sl == 0 ? kv : kv2, hs = sl == 0 ? held : held2;
+          if (done == 0) {
+            const int64_t s0 = units_for(c, kvs + 1) - hs;
+            if (s0 > 0) atomicAdd(&cnt[0], (int32_t)s0);
+          }
+          int64_t kmin = done > 1 ? done : 1;
+          if (hs * B - kvs > kmin) kmin = hs * B - kvs;
+          const uint64_t x = (uint64_t)(kvs + kmin);
+          const int64_t rr = (int64_t)(x - __umul64hi(x, c.bs_magic) * (uint64_t)B);
+#pragma unroll 1
+          for (int64_t k = rr == 0 ? kmin : kmin + (B - rr); k < done + KIr; k += B)
+            atomicAdd(&cnt[k - done], 1);
+        }
+      }
+      __syncwarp();
+      need = cnt[q_it];
+      __syncwarp();
+    } else
 #pragma unroll 1
     for (int i = 0; i < KIr; ++i) {
       const int ki = done + i;
@@ -605,10 +637,12 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
       wput(U, &U.out->log_used, used >= 0 && fit == K ? used + K * need_w : (int64_t)-1);
     }
     if (emit_times) {
+      // runner lanes write their token of each committed iteration
 #pragma unroll 1
-      for (int r = 0; r < nd; ++r) {
-        const int64_t e = __shfl_sync(SSG_FULL, r < 32 ? ebase : ebase2, r & 31);
-        if (lane < K) U.emissions[e + kit] = t_done;
+      for (int k = 0; k < K; ++k) {
+        const double tk = __shfl_sync(SSG_FULL, t_done, k);
+        if (mine) U.emissions[ebase + done + k] = tk;
+        if (mine2) U.emissions[ebase2 + done + k] = tk;
       }
     }
     const double util = (double)alloc_after / (double)c.total_units;
