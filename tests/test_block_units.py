@@ -58,3 +58,49 @@ def test_block_magic_is_exact(tmp_path):
     out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
     bad, n = map(int, out.stdout.split())
     assert bad == 0 and n > 10_000_000, out.stdout
+
+
+def _units(x, b):
+    return -(-x // b)
+
+
+def _closed_form_needs(kv, held, done, kir, b):
+    """engine.cu fast_forward_t's block needs of one runner over iterations
+    done .. done+kir-1: units(kv+1) - held at k = 0 (if positive), then one
+    block exactly at the k >= 1 where kv + k is a multiple of b and
+    kv + k >= held * b; the remainder uses floor(x / b) = mulhi(x, magic)."""
+    got = [0] * kir
+    if done == 0:
+        got[0] += max(0, _units(kv + 1, b) - held)
+    kmin = max(max(1, done), held * b - kv)
+    x = kv + kmin
+    m = _magic(b)
+    rr = x - ((x * m) >> 64) * b
+    k = kmin if rr == 0 else kmin + (b - rr)
+    while k < done + kir:
+        got[k - done] += 1
+        k += b
+    return got
+
+
+def _magic(b):
+    if b & (b - 1) == 0:
+        return 1 << (64 - (b.bit_length() - 1))
+    return (1 << 64) // b + 1
+
+
+@pytest.mark.parametrize("b", [2, 3, 7, 16, 24, 32, 48])
+def test_fast_forward_closed_form_block_needs(b):
+    """The closed form equals the per-iteration definition the event loop
+    applies (reserve kv+k+1 tokens holding max(held, units(kv+k)) for k >= 1),
+    for every context, high-water mark and round start in range."""
+    for kv in range(0, 5 * b + 3):
+        for held in range(0, _units(kv, b) + 3):
+            for done in (0, 1, 2, b - 1, b, 3 * b + 1):
+                kir = 32
+                ref = []
+                for i in range(kir):
+                    k = done + i
+                    hk = held if k == 0 else max(held, _units(kv + k, b))
+                    ref.append(max(0, _units(kv + k + 1, b) - hk))
+                assert _closed_form_needs(kv, held, done, kir, b) == ref, (kv, held, done)
