@@ -182,9 +182,11 @@ __device__ bool batch_start(Unit& U, RepState& S, int r) {
   S.tokens += tokens;
   U.iters += 1;
   U.entries += S.np + S.nd;
-  const double util = (double)S.allocated / (double)c.total_units;
-  S.peak_kv = S.peak_kv < util ? util : S.peak_kv;
-  wput(U, &U.out->flops, __dadd_rn(U.out->flops, flops));
+  // peak_kv holds the peak allocated units until the unit ends (the division by
+  // total_units is monotone, so max of the quotients = quotient of the max)
+  const double alloc = (double)S.allocated;
+  S.peak_kv = S.peak_kv < alloc ? alloc : S.peak_kv;
+  U.flops = __dadd_rn(U.flops, flops);
   S.ev_kind = 2;
   S.ev_time = __dadd_rn(U.clock, lat);
   S.ev_seq = U.seq++;
@@ -419,9 +421,9 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
     // no more than can complete before the next arrival, each lasting >= lb
     int KIr = max_iters - done < KI ? max_iters - done : KI;
     if (arrivals_end && *next_arrival < U.u->n) {
-      const double gap = __dsub_rn(*next_arrival_time, U.clock);
-      const double est = gap / lb + 2.0;
-      if (est < (double)KIr) KIr = est < 1.0 ? 1 : (int)est;
+      // (a cap only: rounds split where it is low, so an approximate quotient is enough)
+      const float est = __fdividef((float)__dsub_rn(*next_arrival_time, U.clock), (float)lb) + 2.0f;
+      if (est < (float)KIr) KIr = est < 1.0f ? 1 : (int)est;
     }
     const int k = done + q_it;  // this lane's iteration
     const bool active = q_it < KIr;
@@ -645,13 +647,8 @@ __device__ __forceinline__ int fast_forward_t(Unit& U, RepState& S, int32_t* nex
         if (mine2) U.emissions[ebase2 + done + k] = tk;
       }
     }
-    const double util = (double)alloc_after / (double)c.total_units;
-    double pk = q_it < K ? util : 0.0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double t = __shfl_xor_sync(SSG_FULL, pk, o);
-      pk = pk < t ? t : pk;
-    }
+    // peak allocated units of the committed iterations (below 2^25 here)
+    const double pk = (double)__reduce_max_sync(SSG_FULL, q_it < K ? (unsigned)alloc_after : 0u);
     S.peak_kv = S.peak_kv < pk ? pk : S.peak_kv;
     S.allocated = __shfl_sync(SSG_FULL, alloc_after, last << lgP);
     S.busy_time = busy;
@@ -749,6 +746,7 @@ __device__ void run_unit(Unit& U) {
     *U.out = o;
   }
   __syncwarp();
+  U.flops = 0.0;
   U.clock = 0.0;
   U.seq = (uint64_t)u.n;
   U.serial = 0;
@@ -901,7 +899,7 @@ __device__ void run_unit(Unit& U) {
         S.run_n >= 1 && S.run_n <= SSG_FF_RUNNERS) {
       // pure-decode stretch: iterations that end at the same state the event
       // loop would reach; afterwards the replica is again "BatchStart at clock"
-      double fl = U.out->flops;
+      double fl = U.flops;
       const int32_t na_before = next_arrival;
       SSG_PH_BEGIN(ph_f);
       const int k = fast_forward<FMA, LONE>(U, S, &next_arrival, &next_arrival_time, &fl);
@@ -919,7 +917,7 @@ __device__ void run_unit(Unit& U) {
       }
 #endif
       if (k > 0) {
-        wput(U, &U.out->flops, fl);
+        U.flops = fl;
         events += 2 * k + (next_arrival - na_before);
         S.ev_time = U.clock;
         S.ev_seq = U.seq++;
@@ -970,11 +968,18 @@ __device__ void run_unit(Unit& U) {
     }
   }
   if (reg1) store_rep(U, 0, S1);
+  __syncwarp();
+#pragma unroll 1
+  for (int r = U.lane; r < R; r += 32) {
+    const double p = U.reps[r].peak_kv;  // 0 stays 0 (no units ever allocated)
+    if (p > 0.0) U.reps[r].peak_kv = p / (double)c.total_units;
+  }
   // an aborted or failed probe cancels the speculative probes behind its feasible branch
   if (U.group_fail && U.lane == 0 && (U.out->aborted == 1 || U.out->code != SSG_OK))
     atomicOr(U.group_fail, 1u << u.rung);
   U.qbytes += warp_sum64(U.qb_lane);
   if (U.lane == 0) {
+    U.out->flops = U.flops;
     U.out->span = U.clock;
     U.out->events = events;
     U.out->iterations = U.iters;

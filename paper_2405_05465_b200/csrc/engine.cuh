@@ -87,6 +87,7 @@ struct Unit {
   // counted while the scheduler forms a batch (reset by batch_start):
   int32_t plan_tokens; // prefill chunk tokens pushed
   int32_t plan_late;   // requests first scheduled now, later than the abort threshold
+  double flops;        // total_model_flops so far (written to SimUnitOut at the end)
 #ifdef SSG_PHASE_CYCLES
   long long ph[SSG_PH_N];  // diagnostic build: cycles per event-loop phase (SSG_PH_*)
 #endif

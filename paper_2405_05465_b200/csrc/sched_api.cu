@@ -47,6 +47,7 @@ __global__ void __launch_bounds__(32) k_sched_op(SchedArgs A) {
   U.iters = 0;
   U.entries = 0;
   U.clock = A.now;
+  U.flops = 0.0;
   U.seq = 0;
   U.ax1_hint = 0;
   U.qb_lane = 0;
