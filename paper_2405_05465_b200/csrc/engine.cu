@@ -701,7 +701,8 @@ __device__ SSG_FFWD int fast_forward(Unit& U, RepState& S, int32_t* next_arrival
     return 0;
   const int nd = S.run_n, pp = c.pp;
   if (c.policy == SSG_POL_SARATHI ? nd > c.chunk : nd > c.max_tokens) return 0;
-  if (nd > c.max_batch || (nd + pp - 1) / pp > c.tab_tmax) return 0;
+  // microbatch 0 (ceil(nd / pp) runners) within the token tables: nd <= tab_tmax * pp
+  if (nd > c.max_batch || nd > (int64_t)c.tab_tmax * pp) return 0;
   return fast_forward_t<FMA, LONE>(U, S, next_arrival, next_arrival_time, flops_acc);
 }
 
