@@ -636,8 +636,10 @@ struct SweepKnobs {
                    // kernel diet (DESIGN 6.4): 0.83 s vs 0.96 s at 3, 0.94 s at 1
   int crit_extra = 2;  // extra levels for the candidates with the longest probes
   int crit_pct = 95;   // "longest": probes within this % of the group's longest (A/B: DESIGN 6.4)
-  int lanes = 1;   // candidate groups advancing independently (streams); measured: no gain
-                   // (the sweep is issue-bound, not tail-bound), so one lane by default
+  int lanes = 2;   // candidate groups advancing independently (streams): one group's
+                   // launch tail overlaps the other's next round.  1 until the round-2
+                   // v5 kernels (no gain then); now 2 lanes 0.453 s, 3: 0.462, 4: 0.461,
+                   // 1: 0.474 (DESIGN 6.7)
   bool block = false;  // groups = contiguous blocks of the capacity order (else dealt)
 };
 

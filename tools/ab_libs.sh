@@ -7,5 +7,5 @@ for spec in $1; do
   [ "$envs" = "$rest" ] && envs=""
   [ "$lib" = "default" ] && lib=paper_2405_05465_b200/libssg.so
   echo "== $label ($lib) $envs"
-  env $(echo $envs | tr ',' ' ') SSG_LIB=$PWD/$lib REPS=3 timeout 300 python tools/time_sweep.py 2>&1 | grep -E "^sweep" | cut -c1-40
+  env $(echo $envs | tr ',' ' ') SSG_LIB=$PWD/$lib REPS=3 timeout 300 python tools/time_sweep.py 2>&1 | grep -E "^sweep" | cut -c1-42
 done

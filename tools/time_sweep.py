@@ -12,6 +12,6 @@ print("setup %.2fs configs %d" % (t1 - t0, s.num_configs), flush=True)
 for rep in range(int(os.environ.get("REPS", "2"))):
     ssg.stats_reset(); t0 = time.time(); recs = s.run(); t1 = time.time()
     st = ssg.stats()
-    print("sweep %.2fs  %.1f configs/s  stats %s" % (t1 - t0, s.num_configs / (t1 - t0), json.dumps(st)), flush=True)
+    print("sweep %.3fs  %.1f configs/s  stats %s" % (t1 - t0, s.num_configs / (t1 - t0), json.dumps(st)), flush=True)
 out = ssg.search_finalize(path, recs)
 print(out["summary"])
