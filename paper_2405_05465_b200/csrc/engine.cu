@@ -886,7 +886,7 @@ __device__ void run_unit(Unit& U) {
     RepState S = reg1 ? S1 : load_rep(U, r);
 #ifdef SSG_FF_STATS
     if (FAST && S.ev_kind == 1 && reg1) {
-      if (S.run_n > 32) FFSTAT(14);
+      if (S.run_n > SSG_FF_RUNNERS) FFSTAT(14);
       else if (!(S.wait_n == 0 || S.run_n >= c.max_batch)) FFSTAT(15);
     }
 #endif
