@@ -575,7 +575,11 @@ int ssg_search_shard(const char* config_path, int shard, int num_shards, ssg_con
                      size_t capacity, size_t* count, ssg_status* st) {
   return guarded(st, [&] {
     require(num_shards >= 1 && shard >= 0 && shard < num_shards, "ssg_search_shard: bad shard");
-    auto cfg = load_search_config(config_path);
+    ssg::PhaseTimer timer("ssg_search_shard");
+    auto cfg = [&] {
+      ssg::PhaseTimer t("ssg_search_shard: load config");
+      return load_search_config(config_path);
+    }();
     std::vector<size_t> owned;
     auto results =
         evaluate_configs_shard(cfg.spec, cfg.workload, cfg.options, shard, num_shards, &owned);

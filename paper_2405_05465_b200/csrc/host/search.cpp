@@ -945,6 +945,7 @@ SearchSession::SearchSession(const ModelSpec& spec, const std::vector<Request>& 
       try {
         StatsScope scope;  // counters merge into the process totals under the lock
         cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+        PhaseTimer t("search: profile + train SKU");
         built[k] = train(generate_synthetic_profile(spec, opts.space.skus[k], tps), opts.train);
       } catch (...) {
         err[k] = std::current_exception();
@@ -983,6 +984,7 @@ SearchSession::SearchSession(const ModelSpec& spec, std::vector<CandidateConfig>
 }
 
 void SearchSession::open_workload(const std::vector<Request>& workload) {
+  PhaseTimer timer("search: open workload");
   State& S = *st_;
   const SearchOptions& opts = S.opts;
   for (const auto* e : S.ests) e->device();  // resident in HBM before any timed work

@@ -13,6 +13,9 @@
 #include <exception>
 #include <cmath>
 #include <random>
+#include <cstring>
+#include <unordered_map>
+#include <vector>
 
 #include "json.hpp"
 #include "runtime.h"
@@ -135,6 +138,26 @@ double synthetic_oracle(const OperatorDescriptor& d, const FeatureMap& f, const 
 // ------------------------------------------------------------------ grids
 namespace {
 
+// synthetic_oracle at a grid point given in feature_schema order, without
+// building the FeatureMap (same Work functions, same arithmetic)
+double oracle_at(const OperatorDescriptor& d, const std::vector<double>& pt, const DeviceProfile& dev) {
+  switch (d.op_class) {
+    case OpClass::TokenLevel: {
+      Work w = token_work(d, pt[0]);
+      return std::max(w.flops / dev.peak_flops, w.bytes / dev.mem_bandwidth) + dev.kernel_overhead;
+    }
+    case OpClass::SequenceLevel: {
+      Work w = attention_work(d, pt[0], pt[1]);
+      return std::max(w.flops / dev.peak_flops, w.bytes / dev.mem_bandwidth) + dev.kernel_overhead;
+    }
+    case OpClass::Communication: {
+      Work w = comm_work(d, pt[0]);
+      return w.wire_bytes / dev.link_bandwidth + static_cast<double>(w.hops) * dev.kernel_overhead;
+    }
+  }
+  throw InternalError("synthetic_oracle: bad op class");
+}
+
 std::vector<std::int64_t> doubling_levels(std::int64_t lo, std::int64_t hi) {
   std::vector<std::int64_t> v;
   for (std::int64_t x = lo; x < hi; x *= 2) v.push_back(x);
@@ -206,6 +229,24 @@ std::vector<std::vector<double>> refine_axes(const OperatorDescriptor& d,
   const int max_extra = 24;
   const auto schema = feature_schema(d.op_class);
   const std::size_t nf = axes.size();
+  // the error of one (axis, gap, cross-section) never changes between rounds:
+  // memoised by its exact coordinates, each round re-reads the old ones and
+  // evaluates the oracle only where the last inserted level made new gaps or
+  // sections (same errors, same scan order, same strict-max choice)
+  struct KeyHash {
+    std::size_t operator()(const std::vector<std::uint64_t>& k) const {
+      std::uint64_t h = 0x9e3779b97f4a7c15ull;
+      for (auto v : k) h = (h ^ v) * 0x100000001b3ull;
+      return static_cast<std::size_t>(h ^ (h >> 29));
+    }
+  };
+  std::unordered_map<std::vector<std::uint64_t>, double, KeyHash> memo;
+  auto bits = [](double v) {
+    std::uint64_t u;
+    std::memcpy(&u, &v, sizeof u);
+    return u;
+  };
+  std::vector<std::uint64_t> key;
   for (int round = 0; round < max_extra; ++round) {
     double worst = 0.0, worst_mid = 0.0;
     std::size_t worst_axis = 0;
@@ -227,13 +268,23 @@ std::vector<std::vector<double>> refine_axes(const OperatorDescriptor& d,
         const double a = axes[f][i], b = axes[f][i + 1];
         const double mid = std::expm1(0.5 * (std::log1p(a) + std::log1p(b)));
         for (auto sec : sections) {
-          sec[f] = a;
-          const double ya = std::log(synthetic_oracle(d, feature_point(schema, sec), dev));
-          sec[f] = b;
-          const double yb = std::log(synthetic_oracle(d, feature_point(schema, sec), dev));
-          sec[f] = mid;
-          const double truth = synthetic_oracle(d, feature_point(schema, sec), dev);
-          const double err = std::fabs(std::exp(0.5 * (ya + yb)) - truth) / truth;
+          key.assign({static_cast<std::uint64_t>(f), bits(a), bits(b)});
+          for (std::size_t g = 0; g < nf; ++g)
+            if (g != f) key.push_back(bits(sec[g]));
+          auto it = memo.find(key);
+          double err;
+          if (it != memo.end()) {
+            err = it->second;
+          } else {
+            sec[f] = a;
+            const double ya = std::log(oracle_at(d, sec, dev));
+            sec[f] = b;
+            const double yb = std::log(oracle_at(d, sec, dev));
+            sec[f] = mid;
+            const double truth = oracle_at(d, sec, dev);
+            err = std::fabs(std::exp(0.5 * (ya + yb)) - truth) / truth;
+            memo.emplace(key, err);
+          }
           if (err > worst) {
             worst = err;
             worst_axis = f;
@@ -283,7 +334,7 @@ std::vector<ProfileRecord> generate_synthetic_profile(const ModelSpec& spec,
         ProfileRecord r;
         r.op = d.op;
         r.features = feature_point(schema, pt);
-        r.runtime = synthetic_oracle(d, r.features, dev);
+        r.runtime = oracle_at(d, pt, dev);
         r.features[kFeatTpDegree] = static_cast<double>(tp);
         out.push_back(std::move(r));
       }
