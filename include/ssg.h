@@ -217,6 +217,9 @@ typedef struct ssg_run_stats {
      iterations / entries is speculation) */
   int64_t useful_iterations, useful_entries, useful_bytes;
   int64_t cancelled_probes; /* speculative probes stopped once a lower rate of their candidate failed */
+  /* SLO runs taken in the round that settles a capacity, one per capacity it can end
+     with; spec_slo_used of them are the runs the sequential search makes next */
+  int64_t spec_slo_runs, spec_slo_used;
 } ssg_run_stats;
 void ssg_stats_reset(void);
 void ssg_stats_get(ssg_run_stats* out);

@@ -123,7 +123,7 @@ class RunStats(C.Structure):
         ("simulate_ms", C.c_double), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
         ("launches_setup", C.c_int64), ("simulate_busy_ms", C.c_double),
         ("useful_iterations", C.c_int64), ("useful_entries", C.c_int64), ("useful_bytes", C.c_int64),
-        ("cancelled_probes", C.c_int64)]
+        ("cancelled_probes", C.c_int64), ("spec_slo_runs", C.c_int64), ("spec_slo_used", C.c_int64)]
 
 
 def exported_symbols():

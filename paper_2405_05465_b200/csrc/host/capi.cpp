@@ -639,6 +639,8 @@ void ssg_stats_get(ssg_run_stats* out) {
   out->useful_entries = r.useful_entries;
   out->useful_bytes = r.useful_bytes;
   out->cancelled_probes = r.cancelled_probes;
+  out->spec_slo_runs = r.spec_slo_runs;
+  out->spec_slo_used = r.spec_slo_used;
 }
 
 int ssg_search_finalize(const char* config_path, const ssg_config_record* records, size_t n,

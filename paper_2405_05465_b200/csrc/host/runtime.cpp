@@ -46,6 +46,8 @@ void RunStats::add(const RunStats& o) {
   useful_entries += o.useful_entries;
   useful_bytes += o.useful_bytes;
   cancelled_probes += o.cancelled_probes;
+  spec_slo_runs += o.spec_slo_runs;
+  spec_slo_used += o.spec_slo_used;
 }
 
 StatsScope::StatsScope() : prev(t_stats) { t_stats = &local; }

@@ -15,6 +15,7 @@
 // ladder, or a bisection sub-tree), become the round's probes.  The replay
 // then selects exactly the capacity the sequential reference would.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -271,6 +272,17 @@ struct Candidate {
   bool done = false;       // evaluation finished (capacity known, or failed)
   bool measured = false;   // SLO / static run taken
   int64_t probe_iters = 0; // longest probe unit so far (iterations): speculation budget
+  int rounds = 0;          // rounds with probes so far
+  int bisect_from = -1;    // rounds before its first bisection round
+  // speculative SLO runs: taken in the round whose probes settle the capacity, at
+  // evaluation_fraction x every capacity the replay can still end with; the one the
+  // replay does end with is the SLO run the sequential search would make next
+  struct SpecFull {
+    std::vector<SimUnitOut> out;  // the run's units (ProbeDesc::first_unit = 0)
+    ProbeDesc p;
+    double sel3[3];
+  };
+  std::unordered_map<double, SpecFull> spec_full;
   ProbeAnswer full_run;    // work of the SLO / static run (iters, entries, bytes)
   ConfigResult res;
 };
@@ -630,17 +642,76 @@ void fail(Candidate& C, const SimUnitOut& o) {
   }
 }
 
+// Capacities find_capacity can return once `rates` are answered, over every
+// feasible / infeasible outcome of them.  False when some outcome asks a rate
+// outside `rates` (the search would go on past this round) or more than `max`
+// capacities are possible.  `memo` is restored on return.
+bool possible_capacities(ProbeMemo& memo, const CapacitySearchOptions& o,
+                         const std::vector<double>& rates, std::size_t max, std::vector<double>& caps) {
+  try {
+    const double c = replay_capacity(memo, o);
+    if (std::find(caps.begin(), caps.end(), c) == caps.end()) caps.push_back(c);
+    return caps.size() <= max;
+  } catch (const NeedProbe& need) {
+    if (std::find(rates.begin(), rates.end(), need.q) == rates.end()) return false;
+    for (int f = 1; f >= 0; --f) {
+      ProbeAnswer a;
+      a.feasible = f != 0;
+      memo.emplace(need.q, a);
+      const bool ok = possible_capacities(memo, o, rates, max, caps);
+      memo.erase(need.q);
+      if (!ok) return false;
+    }
+    return true;
+  } catch (const ProbeError&) {
+    return true;  // no capacity on this branch
+  } catch (const Error&) {
+    return true;
+  }
+}
+
+// Live candidates of every sweep in flight in this process (concurrent sessions,
+// e.g. cfg #5's twelve sweeps): the under-loaded test of the speculation knobs.
+std::atomic<int64_t> g_live_candidates{0};
+struct LiveCandidates {
+  int64_t n;
+  explicit LiveCandidates(int64_t k) : n(k) { g_live_candidates += n; }
+  ~LiveCandidates() { g_live_candidates -= n; }
+};
+std::atomic<int> g_sweeps_in_flight{0};
+struct SweepInFlight {
+  SweepInFlight() { ++g_sweeps_in_flight; }
+  ~SweepInFlight() { --g_sweeps_in_flight; }
+};
+
+// ~4 probes per live candidate fit the SMs' warp slots (8 per SM)
+bool sweeps_underloaded() {
+  return g_live_candidates.load() * 4 <= 8 * static_cast<int64_t>(context().num_sms);
+}
+
 struct SweepKnobs {
   int ladder = 4;  // doubling rates probed per round
   int depth = 2;   // bisection levels probed per round (2^depth - 1 rates); 3 until the
                    // kernel diet (DESIGN 6.4): 0.83 s vs 0.96 s at 3, 0.94 s at 1
   int crit_extra = 2;  // extra levels for the candidates with the longest probes
   int crit_pct = 95;   // "longest": probes within this % of the group's longest (A/B: DESIGN 6.4)
-  int lanes = 2;   // candidate groups advancing independently (streams): one group's
+  int lanes = -1;  // candidate groups advancing independently (streams): one group's
                    // launch tail overlaps the other's next round.  1 until the round-2
                    // v5 kernels (no gain then); now 2 lanes 0.453 s, 3: 0.462, 4: 0.461,
-                   // 1: 0.474 (DESIGN 6.7)
+                   // 1: 0.474 (DESIGN 6.7).  -1 = auto: 2 for a sweep running alone, 1
+                   // when other sweeps are in flight (cfg #5's twelve: 1/8 shards 3.99 s
+                   // on 2 lanes, 2.95 s on 1)
   bool block = false;  // groups = contiguous blocks of the capacity order (else dealt)
+  // Under-loaded sweeps (a multi-GPU rank's shard: few candidates, chain-bound
+  // rounds) trade work for rounds; -1 = auto: on when the live candidates' ~4
+  // probes each fit the SMs' warp slots (8 per SM), off for a full one-GPU sweep
+  // (DESIGN 6.7: 1/8 shard 0.254 -> 0.212 s, full sweep 0.455 -> 0.51 s if forced on).
+  int spec_slo = -1;     // speculative SLO runs per candidate and round (0: off, auto 8)
+  int slo_pct = 0;       // for candidates whose probes are within this % of the longest
+  int64_t slo_bytes = int64_t(1) << 31;  // device bytes of a launch's measured runs
+  int lag = -1;          // extra bisection levels for candidates whose bisection started
+                         // this many rounds late at most (they set the sweep's round
+                         // count; auto 2)
 };
 
 SweepKnobs knobs_from_env() {
@@ -651,6 +722,10 @@ SweepKnobs knobs_from_env() {
   if (const char* s = std::getenv("SSG_SPEC_CRIT_PCT")) k.crit_pct = std::max(0, std::atoi(s));
   if (const char* s = std::getenv("SSG_LANES")) k.lanes = std::max(1, std::atoi(s));
   if (const char* s = std::getenv("SSG_LANE_BLOCK")) k.block = s[0] == '1';
+  if (const char* s = std::getenv("SSG_SPEC_SLO")) k.spec_slo = std::atoi(s);
+  if (const char* s = std::getenv("SSG_SPEC_SLO_BYTES")) k.slo_bytes = std::atoll(s);
+  if (const char* s = std::getenv("SSG_SPEC_SLO_PCT")) k.slo_pct = std::max(0, std::atoi(s));
+  if (const char* s = std::getenv("SSG_SPEC_LAG")) k.lag = std::atoi(s);
   return k;
 }
 
@@ -682,7 +757,8 @@ void take_measurement(Candidate& C, const std::vector<SimUnitOut>& out, const Pr
 // exception) unless the probe's abort came first in event order.
 void run_round(SweepLane& lane, std::vector<Candidate>& cands, const std::vector<SpecProbes>& probes,
                const std::vector<std::pair<std::size_t, double>>& full, bool static_run,
-               const ResidentWorkload& w, const CapacitySearchOptions& base) {
+               const ResidentWorkload& w, const CapacitySearchOptions& base,
+               const std::vector<std::pair<std::size_t, double>>& spec = {}) {
   const int32_t n = w.n;
   const int32_t max_late = max_late_of(static_cast<std::size_t>(n));
   ProbeLaunch L;
@@ -704,6 +780,11 @@ void run_round(SweepLane& lane, std::vector<Candidate>& cands, const std::vector
     L.add_probe(k, cands[k], ci, static_run ? 0.0 : q, n, SSG_UF_EMISSIONS, 0.0, 0, false,
                 static_run, L.next_emis_base(w.emis_per_probe));
   }
+  for (const auto& [k, q] : spec) {  // measured after the real ones (L.measured order)
+    const int32_t ci = L.add_config(cands[k]);
+    L.add_probe(k, cands[k], ci, q, n, SSG_UF_EMISSIONS, 0.0, 0, false, false,
+                L.next_emis_base(w.emis_per_probe));
+  }
   if (L.probes.empty()) return;
   std::vector<SimUnitOut> out;
   std::vector<double> sel;
@@ -721,6 +802,19 @@ void run_round(SweepLane& lane, std::vector<Candidate>& cands, const std::vector
     int errors = 0;
     for (int u = p.first_unit; u < p.first_unit + (p.decoupled ? p.R : 1); ++u)
       errors += out[u].code != SSG_OK ? 1 : 0;
+    if (m >= full.size()) {
+      // speculative SLO run: kept for the replay (a run that would need the coupled
+      // redo is dropped; the sequential order then takes it in a later round)
+      if (errors > 1 && p.decoupled) continue;
+      Candidate::SpecFull sf;
+      const int nu = p.decoupled ? p.R : 1;
+      sf.out.assign(out.begin() + p.first_unit, out.begin() + p.first_unit + nu);
+      sf.p = p;
+      sf.p.first_unit = 0;
+      std::copy(sel.begin() + 3 * m, sel.begin() + 3 * m + 3, sf.sel3);
+      C.spec_full[p.qps] = std::move(sf);
+      continue;
+    }
     if (errors > 1 && p.decoupled && p.R <= kMaxCoupledReplicas) {
       const int32_t ci = redo_full.add_config(C);
       redo_full.add_probe(L.probe_cand[L.measured[m]], C, ci, p.qps, n, SSG_UF_EMISSIONS, 0.0, 0,
@@ -806,9 +900,12 @@ void run_group(SweepLane& lane, std::vector<Candidate>& cands, const std::vector
                std::vector<std::size_t>& measured) {
   while (true) {
     std::vector<SpecProbes> probes;
-    std::vector<std::pair<std::size_t, double>> full;
+    std::vector<std::pair<std::size_t, double>> full, spec;
     int64_t longest = 1;
     for (auto k : live) longest = std::max(longest, cands[k].probe_iters);
+    const bool under = (knobs.spec_slo < 0 || knobs.lag < 0) && sweeps_underloaded();
+    const int spec_slo = knobs.spec_slo >= 0 ? knobs.spec_slo : (under ? 8 : 0);
+    const int lag = knobs.lag >= 0 ? knobs.lag : (under ? 2 : 0);
     for (auto k : live) {
       Candidate& C = cands[k];
       if (C.res.failed() || C.measured) continue;
@@ -821,7 +918,14 @@ void run_group(SweepLane& lane, std::vector<Candidate>& cands, const std::vector
           // so their bisection finishes in one round
           const bool critical = C.probe_iters * 100 >= longest * knobs.crit_pct;
           std::vector<SpecRate> qs;
-          speculate(need, C.copts, knobs.ladder, critical ? knobs.depth + knobs.crit_extra : knobs.depth, qs);
+          int depth = critical ? knobs.depth + knobs.crit_extra : knobs.depth;
+          if (need.phase == 2) {
+            if (C.bisect_from < 0) C.bisect_from = C.rounds;
+            // the first ladder round settles most candidates' brackets; one that is
+            // still climbing then would need an extra round at the end
+            depth = std::max(depth, knobs.depth + std::min(lag, C.bisect_from - 1));
+          }
+          speculate(need, C.copts, knobs.ladder, depth, qs);
           // unanswered rates; each one's cancel mask over the others' positions
           std::vector<int> pos(qs.size(), -1);
           SpecProbes sp;
@@ -835,6 +939,20 @@ void run_group(SweepLane& lane, std::vector<Candidate>& cands, const std::vector
               if (pos[a] >= 0 && pos[a] < 32) kill |= 1u << pos[a];
             sp.rates.push_back(q);
             sp.kill.push_back(kill);
+          }
+          C.rounds += 1;
+          if (spec_slo > 0 && C.probe_iters * 100 >= longest * knobs.slo_pct) {
+            // this round may settle the capacity: SLO runs at every capacity it can end with
+            std::vector<double> caps;
+            const bool ok = possible_capacities(C.memo, C.copts, sp.rates, spec_slo, caps);
+            if (std::getenv("SSG_SPEC_DEBUG"))
+              std::fprintf(stderr, "try %zu round %d ok %d caps %zu rates %zu\n", C.index, C.rounds, ok ? 1 : 0,
+                           caps.size(), sp.rates.size());
+            if (ok)
+              for (double cap : caps) {
+                const double q = opts.evaluation_fraction * cap;
+                if (cap > C.copts.min_qps && q > 0.0 && !C.spec_full.count(q)) spec.push_back({k, q});
+              }
           }
           probes.push_back(std::move(sp));
           continue;
@@ -861,11 +979,51 @@ void run_group(SweepLane& lane, std::vector<Candidate>& cands, const std::vector
         C.res.error = e.what();
         continue;
       }
+      if (auto it = C.spec_full.find(q); it != C.spec_full.end()) {
+        // taken speculatively in the round that settled the capacity
+        take_measurement(C, it->second.out, it->second.p, it->second.sel3, w);
+        stats().spec_slo_used += 1;
+        C.spec_full.clear();
+        measured.push_back(k);
+        continue;
+      }
+      if (std::getenv("SSG_SPEC_DEBUG")) {
+        std::fprintf(stderr, "miss %zu rounds %d bisect_from %d iters %lld q %.17g spec", C.index, C.rounds,
+                     C.bisect_from, static_cast<long long>(C.probe_iters), q);
+        for (const auto& kv : C.spec_full) std::fprintf(stderr, " %.17g", kv.first);
+        std::fprintf(stderr, "\n");
+      }
       full.push_back({k, q});
       measured.push_back(k);
     }
     if (probes.empty() && full.empty()) break;
-    run_round(lane, cands, probes, full, false, w, opts.capacity);
+    if (std::getenv("SSG_ROUND_LOG")) {
+      int ph[3] = {0, 0, 0}, rates = 0;
+      for (const SpecProbes& sp : probes) rates += static_cast<int>(sp.rates.size());
+      for (auto k : live) {
+        const Candidate& C = cands[k];
+        if (C.done || C.res.failed()) continue;
+        try {
+          replay_capacity(C.memo, C.copts);
+        } catch (const NeedProbe& nd) {
+          ph[nd.phase] += 1;
+        } catch (...) {
+        }
+      }
+      std::fprintf(stderr, "round lane %p cands %zu ladder %d halving %d bisect %d rates %d full %zu longest %lld\n",
+                   static_cast<void*>(&lane), probes.size(), ph[0], ph[1], ph[2], rates, full.size(),
+                   static_cast<long long>(longest));
+    }
+    // every measured run keeps its emission times and SLO samples on the device
+    // (~16 B per decode token): speculative runs stay within a per-launch budget,
+    // longest-probe candidates first (the group's order)
+    if (!spec.empty()) {
+      const int64_t per_run = 16 * std::max<int64_t>(1, w.emis_per_probe + 2 * w.n);
+      const int64_t room = knobs.slo_bytes / per_run - static_cast<int64_t>(full.size());
+      spec.resize(static_cast<std::size_t>(std::clamp<int64_t>(room, 0, static_cast<int64_t>(spec.size()))));
+    }
+    stats().spec_slo_runs += static_cast<int64_t>(spec.size());
+    run_round(lane, cands, probes, full, false, w, opts.capacity, spec);
   }
 }
 
@@ -1049,6 +1207,7 @@ std::vector<ConfigResult> evaluate_configs_shard(const ModelSpec& spec,
 std::vector<ConfigResult> SearchSession::evaluate(int shard, int num_shards,
                                                   std::vector<std::size_t>* owned) {
   StatsScope stats_scope;  // counters merge into the process totals when the evaluation ends
+  SweepInFlight in_flight;
   PhaseTimer timer("search: evaluate");
   const State& S = *st_;
   const ModelSpec& spec = S.spec;
@@ -1218,8 +1377,12 @@ std::vector<ConfigResult> SearchSession::evaluate(int shard, int num_shards,
   PhaseTimer t_rounds("search: rounds");
   // lanes: streams + buffers; every lane waits for the token tables
   const SweepKnobs knobs = knobs_from_env();
+  LiveCandidates live_scope(static_cast<int64_t>(live.size()));
   const std::size_t nlanes =
-      makespan ? 1 : std::max<std::size_t>(1, std::min<std::size_t>(knobs.lanes, live.size()));
+      makespan ? 1
+               : std::max<std::size_t>(1, std::min<std::size_t>(
+                                              knobs.lanes >= 0 ? knobs.lanes : (g_sweeps_in_flight.load() > 1 ? 1 : 2),
+                                              live.size()));
   while (SS.lanes.size() < nlanes) SS.lanes.push_back(borrow_lane());
   auto& ctx = context();
   cudaEvent_t origin;

@@ -79,6 +79,7 @@ struct RunStats {
   // sweep work the sequential reference search would do (probes its replay asks + SLO runs)
   int64_t useful_iterations = 0, useful_entries = 0, useful_bytes = 0;
   int64_t cancelled_probes = 0;  // speculative probes stopped once a lower rate of their group failed
+  int64_t spec_slo_runs = 0, spec_slo_used = 0;  // speculative SLO runs taken / used by the replay
   void add(const RunStats& o);
 };
 // The calling thread's counters: the process-wide ones, or a StatsScope's

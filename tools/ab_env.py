@@ -26,8 +26,10 @@ for st in settings:
         ref = ref or h
         assert h == ref, ("records differ", st, h, ref)
     x = ssg.stats()
-    print("%-40s sweep %s s | launches %d units %d iters %.1fM" % (st, " ".join("%.3f" % t for t in ts),
-          x["launches_simulate"], x["units"] // reps, x["iterations"] / reps / 1e6), flush=True)
+    print("%-40s sweep %s s | last sweep: launches %d units %d iters %.1fM | spec SLO %d used %d" % (
+          st, " ".join("%.3f" % t for t in ts), x["launches_simulate"], x["units"],
+          x["iterations"] / 1e6, x.get("spec_slo_runs", 0), x.get("spec_slo_used", 0)),
+          flush=True)
     for k, v in old.items():
         if v is None: os.environ.pop(k, None)
         else: os.environ[k] = v
