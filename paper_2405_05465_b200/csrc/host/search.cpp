@@ -720,7 +720,7 @@ SweepKnobs knobs_from_env() {
   if (const char* s = std::getenv("SSG_SPEC_DEPTH")) k.depth = std::max(1, std::atoi(s));
   if (const char* s = std::getenv("SSG_SPEC_CRIT")) k.crit_extra = std::max(0, std::atoi(s));
   if (const char* s = std::getenv("SSG_SPEC_CRIT_PCT")) k.crit_pct = std::max(0, std::atoi(s));
-  if (const char* s = std::getenv("SSG_LANES")) k.lanes = std::max(1, std::atoi(s));
+  if (const char* s = std::getenv("SSG_LANES")) k.lanes = std::atoi(s) >= 1 ? std::atoi(s) : -1;
   if (const char* s = std::getenv("SSG_LANE_BLOCK")) k.block = s[0] == '1';
   if (const char* s = std::getenv("SSG_SPEC_SLO")) k.spec_slo = std::atoi(s);
   if (const char* s = std::getenv("SSG_SPEC_SLO_BYTES")) k.slo_bytes = std::atoll(s);
