@@ -208,49 +208,66 @@ struct SpecProbes {
   std::vector<uint32_t> kill;
 };
 
+// Bisection sub-tree below (lo, hi) to `depth` levels: an interval's mid is
+// asked once the interval is reached; its upper half is reached only when the
+// mid is feasible (its lower half when it is not, which no early failure can
+// tell, so that half inherits its parent's conditions only).  `root` is the
+// index of the root's mid when it is already in `out` (-1: add it).
+void speculate_subtree(double lo, double hi, const std::vector<int>& cond, int root, int depth,
+                       const CapacitySearchOptions& o, std::vector<SpecRate>& out) {
+  struct Interval {
+    double lo, hi;
+    std::vector<int> cond;  // indices into out that must be feasible
+  };
+  std::vector<Interval> level{{lo, hi, cond}}, next;
+  for (int d = 0; d < depth; ++d) {
+    next.clear();
+    for (const Interval& iv : level) {
+      if (!(iv.hi - iv.lo > o.tolerance * iv.hi)) continue;
+      const double mid = 0.5 * (iv.lo + iv.hi);
+      int idx = root;
+      if (d > 0 || root < 0) {
+        idx = static_cast<int>(out.size());
+        out.push_back({mid, iv.cond});
+      }
+      next.push_back({iv.lo, mid, iv.cond});
+      std::vector<int> up = iv.cond;
+      up.push_back(idx);
+      next.push_back({mid, iv.hi, up});
+    }
+    level.swap(next);
+  }
+}
+
 void speculate(const NeedProbe& need, const CapacitySearchOptions& o, int ladder, int depth,
-               std::vector<SpecRate>& out) {
+               int pre_depth, std::vector<SpecRate>& out) {
   out.push_back({need.q, {}});
   if (need.phase == 0) {
     // doubling: rung k is asked only after rungs 0..k-1 were feasible
     double q = need.q;
+    std::vector<int> rung{0};
     for (int k = 1; k < ladder; ++k) {
       q *= 2.0;
       if (q > o.max_qps) break;
       std::vector<int> prev(out.size());
       for (std::size_t i = 0; i < prev.size(); ++i) prev[i] = static_cast<int>(i);
+      rung.push_back(static_cast<int>(out.size()));
       out.push_back({q, prev});
+    }
+    // under-loaded sweeps: the first bisection levels of every bracket the ladder
+    // can end in (rung k-1 feasible, rung k not), asked after rungs 0..k-1; the
+    // bracket below rung 0 exists once an earlier round found a feasible rate
+    if (pre_depth <= 0) return;
+    if (need.lo > 0.0) speculate_subtree(need.lo, need.q, {}, -1, pre_depth, o, out);
+    for (std::size_t k = 1; k < rung.size(); ++k) {
+      std::vector<int> cond(rung.begin(), rung.begin() + static_cast<std::ptrdiff_t>(k));
+      speculate_subtree(out[rung[k - 1]].q, out[rung[k]].q, cond, -1, pre_depth, o, out);
     }
   } else if (need.phase == 1) {
     // halving: each deeper rate is the slowest probe of its round (iterations
     // grow ~1/qps), and the first halving usually suffices -- no speculation
   } else {
-    // bisection sub-tree below (lo, hi) to `depth` levels: an interval's mid is
-    // asked once the interval is reached; its upper half is reached only when
-    // the mid is feasible (its lower half when it is not, which no early
-    // failure can tell, so that half inherits its parent's conditions only)
-    struct Interval {
-      double lo, hi;
-      std::vector<int> cond;  // indices into out that must be feasible
-    };
-    std::vector<Interval> level{{need.lo, need.hi, {}}}, next;
-    for (int d = 0; d < depth; ++d) {
-      next.clear();
-      for (const Interval& iv : level) {
-        if (!(iv.hi - iv.lo > o.tolerance * iv.hi)) continue;
-        const double mid = 0.5 * (iv.lo + iv.hi);
-        int idx = 0;  // d == 0: the mid is need.q itself
-        if (d > 0) {
-          idx = static_cast<int>(out.size());
-          out.push_back({mid, iv.cond});
-        }
-        next.push_back({iv.lo, mid, iv.cond});
-        std::vector<int> up = iv.cond;
-        up.push_back(idx);
-        next.push_back({mid, iv.hi, up});
-      }
-      level.swap(next);
-    }
+    speculate_subtree(need.lo, need.hi, {}, 0, depth, o, out);
   }
 }
 
@@ -709,6 +726,10 @@ struct SweepKnobs {
   int spec_slo = -1;     // speculative SLO runs per candidate and round (0: off, auto 8)
   int slo_pct = 0;       // for candidates whose probes are within this % of the longest
   int64_t slo_bytes = int64_t(1) << 31;  // device bytes of a launch's measured runs
+  int pre = 0;           // bisection levels speculated under every ladder bracket in the
+                         // ladder's own round (-1: auto, 1 when under-loaded).  Measured
+                         // (DESIGN 6.7): 1/2 shard 0.342 -> 0.332 s at 1, 1/4 and 1/8 shards
+                         // unchanged at 1, mixed at 2, slower at 3: off by default
   int lag = -1;          // extra bisection levels for candidates whose bisection started
                          // this many rounds late at most (they set the sweep's round
                          // count; auto 2)
@@ -723,6 +744,7 @@ SweepKnobs knobs_from_env() {
   if (const char* s = std::getenv("SSG_LANES")) k.lanes = std::atoi(s) >= 1 ? std::atoi(s) : -1;
   if (const char* s = std::getenv("SSG_LANE_BLOCK")) k.block = s[0] == '1';
   if (const char* s = std::getenv("SSG_SPEC_SLO")) k.spec_slo = std::atoi(s);
+  if (const char* s = std::getenv("SSG_SPEC_PRE")) k.pre = std::atoi(s);
   if (const char* s = std::getenv("SSG_SPEC_SLO_BYTES")) k.slo_bytes = std::atoll(s);
   if (const char* s = std::getenv("SSG_SPEC_SLO_PCT")) k.slo_pct = std::max(0, std::atoi(s));
   if (const char* s = std::getenv("SSG_SPEC_LAG")) k.lag = std::atoi(s);
@@ -903,9 +925,10 @@ void run_group(SweepLane& lane, std::vector<Candidate>& cands, const std::vector
     std::vector<std::pair<std::size_t, double>> full, spec;
     int64_t longest = 1;
     for (auto k : live) longest = std::max(longest, cands[k].probe_iters);
-    const bool under = (knobs.spec_slo < 0 || knobs.lag < 0) && sweeps_underloaded();
+    const bool under = (knobs.spec_slo < 0 || knobs.lag < 0 || knobs.pre < 0) && sweeps_underloaded();
     const int spec_slo = knobs.spec_slo >= 0 ? knobs.spec_slo : (under ? 8 : 0);
     const int lag = knobs.lag >= 0 ? knobs.lag : (under ? 2 : 0);
+    const int pre = knobs.pre >= 0 ? knobs.pre : (under ? 1 : 0);
     for (auto k : live) {
       Candidate& C = cands[k];
       if (C.res.failed() || C.measured) continue;
@@ -925,7 +948,7 @@ void run_group(SweepLane& lane, std::vector<Candidate>& cands, const std::vector
             // still climbing then would need an extra round at the end
             depth = std::max(depth, knobs.depth + std::min(lag, C.bisect_from - 1));
           }
-          speculate(need, C.copts, knobs.ladder, depth, qs);
+          speculate(need, C.copts, knobs.ladder, depth, pre, qs);
           // unanswered rates; each one's cancel mask over the others' positions
           std::vector<int> pos(qs.size(), -1);
           SpecProbes sp;
