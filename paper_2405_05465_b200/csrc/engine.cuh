@@ -269,6 +269,13 @@ __device__ __forceinline__ void wait_insert(Unit& U, RepState& S, int r, int32_t
 __device__ __forceinline__ void wait_erase(Unit& U, RepState& S, int r, int32_t j) {
   int32_t* w = WAIT(U, r);
   const int32_t mask = U.WC - 1;
+  if (S.wait_n > 0 && w[S.wait_head & mask] == j) {
+    // the admitted head (every admission): no search, no shift
+    if (S.wait_n > 1) S.wait_head = (S.wait_head + 1) & mask;
+    S.wait_n -= 1;
+    __syncwarp();
+    return;
+  }
   int32_t pos = ring_upper(w, mask, S.wait_head, S.wait_n, j - 1);
   if (pos >= S.wait_n || w[(S.wait_head + pos) & mask] != j) {
     set_error(U, SSG_ERR_INTERNAL, 1, j, 0, 0.0);  // "request not in waiting queue"
