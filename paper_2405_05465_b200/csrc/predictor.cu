@@ -107,17 +107,22 @@ __global__ void k_predict(SsgEstView E, int64_t n, const int32_t* __restrict__ s
 // ---- query grouping for mixed-model launches --------------------------------
 // Queries of one model with nearby features walk the same tree nodes, so a
 // warp of them shares cache lines and branches (measured: 10M mixed queries
-// 8.2 ms as given, 3.6 ms grouped by model x 16 x 16 log-scale feature cells).
+// 8.2 ms as given, 4.4 ms grouped by model x 16 x 16 log-scale feature cells, 4.2 ms by
+// 32 x 32; the histograms of 64 x 64 cost more than they save: 5.3 ms).
 // A counting sort by that cell: per-block histograms, one scan, a scatter.
 // The grouping only reorders work: every query is still answered by the same
 // exact evaluation, at its own index.
-constexpr int kCells = 256;  // 16 x 16 feature cells per model
+#ifndef SSG_PRED_SIDE
+#define SSG_PRED_SIDE 32  // A/B on cfg #3 (10M queries): 16: 2.27, 32: 2.39, 64: 1.89 G queries/s
+#endif
+constexpr int kSide = SSG_PRED_SIDE;      // log-scale cells per feature axis
+constexpr int kCells = kSide * kSide;     // feature cells per model
 
 __device__ __forceinline__ int feature_cell(double v, double lo, double hi) {
   const float l = log2f(fmaxf((float)lo, 0.f) + 1.f), h = log2f(fmaxf((float)hi, 0.f) + 1.f);
   const float x = log2f(fmaxf((float)v, 0.f) + 1.f);
-  const int c = (int)(16.f * (x - l) / fmaxf(h - l, 1e-6f));
-  return c < 0 ? 0 : (c > 15 ? 15 : c);
+  const int c = (int)((float)kSide * (x - l) / fmaxf(h - l, 1e-6f));
+  return c < 0 ? 0 : (c > kSide - 1 ? kSide - 1 : c);
 }
 
 __device__ __forceinline__ int query_bucket(const SsgEstView& E, int32_t m, double v0, double v1,
@@ -126,7 +131,7 @@ __device__ __forceinline__ int query_bucket(const SsgEstView& E, int32_t m, doub
   const SsgModelDesc& d = E.models[m];
   const int c0 = feature_cell(v0, d.lower[0], d.upper[0]);
   const int c1 = (d.nf > 1 && has_f1) ? feature_cell(v1, d.lower[1], d.upper[1]) : 0;
-  return m * kCells + c0 * 16 + c1;
+  return m * kCells + c0 * kSide + c1;
 }
 
 constexpr int kTile = 4096;  // queries per block in the grouping passes
@@ -436,8 +441,17 @@ void launch_predict(const DeviceEstimator& de, int64_t n, const int32_t* slots, 
   const int64_t cap = static_cast<int64_t>(ctx.num_sms) * 8;  // 8 x 256 threads resident per SM
   if (blocks > cap) blocks = cap;
   const int nb = de.view.nmodels * kCells + 1;
+  constexpr size_t kSmemMax = 200 * 1024;  // per-block bucket histograms (opt-in above 48 KB)
   const bool group = slots && n >= (1 << 16) && n < INT32_MAX &&
-                     nb * sizeof(unsigned) <= 48 * 1024 && std::getenv("SSG_NO_GROUPING") == nullptr;
+                     nb * sizeof(unsigned) <= kSmemMax && std::getenv("SSG_NO_GROUPING") == nullptr;
+  static const bool smem_attr = [] {
+    cuda_check(cudaFuncSetAttribute(k_bucket_hist, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kSmemMax)), "smem attr");
+    cuda_check(cudaFuncSetAttribute(k_bucket_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kSmemMax)), "smem attr");
+    return true;
+  }();
+  (void)smem_attr;
   if (group) {
     // scratch on the launch stream (stream-ordered pool: freed behind the kernels)
     StreamScope scope(s);
