@@ -7,4 +7,4 @@ dev = torch.device("cuda", 0)
 import paper_2405_05465_b200 as ssg
 ssg.init(0)
 r = bench.predictor_bench(torch, dev, 10_000_000, 1, 1)
-print(r["value"], r["e2e"], r["roofline"]["bytes_per_query"])
+print(r["value"], r["e2e"], r["roofline"].get("compulsory_bytes_per_query"))
