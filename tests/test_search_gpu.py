@@ -179,3 +179,23 @@ def test_search_deep_speculation_same_answers(ssg, ref, tmp_path, monkeypatch):
         chunk_sizes=(512,), max_gpus_total=4, probe_requests=600, num_requests=600,
         device_docs={"small": SMALL_GPU})
     compare(ssg.search(path), ref.search(path, workers=os.cpu_count() or 1))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("knobs", [
+    # every under-loaded rule forced on for the whole grid: speculative SLO runs at
+    # every capacity a settling round can end with, lag depth, a six-rung ladder and
+    # bisection sub-trees under every ladder bracket
+    {"SSG_SPEC_SLO": "8", "SSG_SPEC_LAG": "2", "SSG_SPEC_LADDER": "6", "SSG_SPEC_PRE": "2"},
+    # and every one forced off, on one lane
+    {"SSG_SPEC_SLO": "0", "SSG_SPEC_LAG": "0", "SSG_SPEC_LADDER": "4", "SSG_SPEC_PRE": "0",
+     "SSG_LANES": "1"},
+])
+def test_full_grid_speculation_rules_same_answers(ssg, knobs, tmp_path, monkeypatch):
+    """The sweep's scheduling rules (search.cpp SweepKnobs: which rates and SLO runs a
+    round speculates, how many candidate lanes) only move work between rounds: cfg #4
+    under either extreme is byte-identical to the reference's run_search."""
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    path, theirs = _golden_case(ssg, "cfg4", tmp_path)
+    compare(ssg.search(path), theirs)
