@@ -711,7 +711,9 @@ struct SweepKnobs {
                     // cfg #4 1/2 shard 0.352 -> 0.333 s, 1/4 0.249 -> 0.241 s, DESIGN 6.7)
   int depth = 2;   // bisection levels probed per round (2^depth - 1 rates); 3 until the
                    // kernel diet (DESIGN 6.4): 0.83 s vs 0.96 s at 3, 0.94 s at 1
-  int crit_extra = 2;  // extra levels for the candidates with the longest probes
+  int crit_extra = -1;  // extra levels for the candidates with the longest probes (-1: auto,
+                        // 1; 2 when under-loaded -- v9: full sweep 0.433-0.436 s at 1 vs
+                        // 0.439-0.445 at 2, 1/2 shard 0.315 at 2 vs 0.319 at 1)
   int crit_pct = 95;   // "longest": probes within this % of the group's longest (A/B: DESIGN 6.4)
   int lanes = -1;  // candidate groups advancing independently (streams): one group's
                    // launch tail overlaps the other's next round.  1 until the round-2
@@ -740,7 +742,7 @@ SweepKnobs knobs_from_env() {
   SweepKnobs k;
   if (const char* s = std::getenv("SSG_SPEC_LADDER")) k.ladder = std::atoi(s) >= 1 ? std::atoi(s) : -1;
   if (const char* s = std::getenv("SSG_SPEC_DEPTH")) k.depth = std::max(1, std::atoi(s));
-  if (const char* s = std::getenv("SSG_SPEC_CRIT")) k.crit_extra = std::max(0, std::atoi(s));
+  if (const char* s = std::getenv("SSG_SPEC_CRIT")) k.crit_extra = std::atoi(s);
   if (const char* s = std::getenv("SSG_SPEC_CRIT_PCT")) k.crit_pct = std::max(0, std::atoi(s));
   if (const char* s = std::getenv("SSG_LANES")) k.lanes = std::atoi(s) >= 1 ? std::atoi(s) : -1;
   if (const char* s = std::getenv("SSG_LANE_BLOCK")) k.block = s[0] == '1';
@@ -927,7 +929,9 @@ void run_group(SweepLane& lane, std::vector<Candidate>& cands, const std::vector
     int64_t longest = 1;
     for (auto k : live) longest = std::max(longest, cands[k].probe_iters);
     const bool under =
-        (knobs.spec_slo < 0 || knobs.lag < 0 || knobs.pre < 0 || knobs.ladder < 0) && sweeps_underloaded();
+        (knobs.spec_slo < 0 || knobs.lag < 0 || knobs.pre < 0 || knobs.ladder < 0 || knobs.crit_extra < 0) &&
+        sweeps_underloaded();
+    const int crit_extra = knobs.crit_extra >= 0 ? knobs.crit_extra : (under ? 2 : 1);
     const int ladder = knobs.ladder >= 1 ? knobs.ladder : (under ? 6 : 4);
     const int spec_slo = knobs.spec_slo >= 0 ? knobs.spec_slo : (under ? 8 : 0);
     const int lag = knobs.lag >= 0 ? knobs.lag : (under ? 2 : 0);
@@ -944,7 +948,7 @@ void run_group(SweepLane& lane, std::vector<Candidate>& cands, const std::vector
           // so their bisection finishes in one round
           const bool critical = C.probe_iters * 100 >= longest * knobs.crit_pct;
           std::vector<SpecRate> qs;
-          int depth = critical ? knobs.depth + knobs.crit_extra : knobs.depth;
+          int depth = critical ? knobs.depth + crit_extra : knobs.depth;
           if (need.phase == 2) {
             if (C.bisect_from < 0) C.bisect_from = C.rounds;
             // the first ladder round settles most candidates' brackets; one that is
